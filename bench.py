@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py — efunc fit-step throughput (points/s) on B200, BASELINE.json's metric.
+
+A step = one pass of the whole hot path over one batch: query binning,
+forward + MSE epilogue, backward, gradient all-reduce (N > 1), AdamW + key rebuild.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL); every rank processes its own 2^20-point
+batch per step (weak scaling) and the 1.7 MB gradient is all-reduced. Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fit-step points/sec (fwd+bwd+AdamW) at 32^3×13 grid, 1/2/4/8 B200; % roofline"
+CONFIGS = {
+    # name: (R, points per GPU per step, shape, loss, workload label)
+    "c2": (32, 1 << 20, "torus", "mse", "C2: 32^3x13 grid, torus SDF, 2^20 points/step/GPU, MSE"),
+    "c3": (32, 1 << 22, "torus", "mse_eikonal", "C3: 32^3x13 grid, torus SDF, 2^22 points/step/GPU, MSE+0.1 Eikonal"),
+    "c1": (8, 4096, "sphere", "mse", "C1: 8^3x13 grid, sphere SDF, 4096 points/step"),
+}
+SEED = 1234
+POOL = 8                       # distinct batches cycled through; 8 x 16.8 MB > 126 MB L2 at C2
+SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
+# algorithmic FP32 lane-ops per kept pair (FFMA = 1 op), DESIGN.md "Roofline"
+OPS_FWD = 12
+OPS_BWD_GRID, OPS_BWD_OFF = 18, 21
+OPS_BWD_EIK_GRID, OPS_BWD_EIK_OFF = 37, 45
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.samples = []
+        self.proc = None
+        self.active = False
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", self.gpu_id, "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        threading.Thread(target=self._reader, daemon=True).start()
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append((self.active, parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sel = [s for a, s in self.samples if a] or [s for _, s in self.samples]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"], "samples": 0}
+        sm = [float(s[0]) for s in sel if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in sel if s[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for s in sel for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sel)}
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_step_time(R, shape, loss_kind, n, seed):
+    """Time one oracle fit step (float64 global sum over all 2R^3 keys) on n queries of the
+    workload. The oracle's cost does not depend on theta's values, so the paper init is used
+    with Delta = 0 (no CPU mean shift in the way)."""
+    import oracle as orc
+    from workloads import synth
+    th = synth.init_theta(R, SEED)
+    q, o = synth.sample_batch(shape, n, seed=seed)
+    t0 = time.perf_counter()
+    f = orc.forward(th, R, q)
+    L, r = orc.mse_loss(f.O, o)
+    h = None
+    if loss_kind == "mse_eikonal":
+        LE, h = orc.eikonal_loss(f.G, 0.1)
+    g = orc.backward(th, R, q, f, r, h)
+    orc.adamw_step(th, g, np.zeros_like(g), np.zeros_like(g), 1, orc.AdamW())
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(R, shape, loss_kind, n=384):
+    t = oracle_step_time(R, shape, loss_kind, n, seed=SEED + 777)
+    return {"value": n / t, "unit": "points/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} queries of the {R}^3 workload, one full fit step (global-support float64 "
+                      f"forward + loss + backward + AdamW), numpy single-threaded; {t:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    R, J, shape_name, loss_kind, label = CONFIGS[args.config]
+    if rank != 0:
+        return
+    from workloads import synth
+    shape = synth.make_shape(shape_name)
+    n = 48 if R >= 32 else 1024
+    for w in range(args.warmup):
+        oracle_step_time(R, shape, loss_kind, n, seed=SEED + w)
+    t = 0.0
+    for k in range(args.steps):
+        t += oracle_step_time(R, shape, loss_kind, n, seed=SEED + 100 + k)
+    v = n * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": label, "R": R, "sample_points_per_step": n},
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{n} queries per step of the {R}^3 workload (float64 global sum)"},
+            "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our path
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_21319_b200 as ef
+    from workloads import synth
+
+    R, J, shape_name, loss_kind, label = CONFIGS[args.config]
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    shape = synth.make_shape(shape_name)
+    loss = ef.LOSS_MSE if loss_kind == "mse" else ef.LOSS_MSE_EIKONAL
+    J_global = J * world
+
+    # model: paper init (s = 7, c ~ N(0, 0.1^2), g = 0) + mean-shift offsets on the GPU
+    th0 = synth.init_theta(R, SEED)
+    m = ef.EFunc(R, th0, device=dev)
+    surf = torch.as_tensor(synth.surface_points(shape, 16384, SEED)).cuda(dev)
+    m.mean_shift_init(surf)
+    hp = ef.AdamW()
+
+    # input pool (> L2 at C2); each rank draws its own points
+    pool = max(2, min(POOL, int(np.ceil(160e6 / (16 * J)))))
+    host = [synth.sample_batch(shape, J, seed=SEED + 1000 * rank + i) for i in range(pool)]
+    qd = [torch.as_tensor(q).cuda(dev) for q, _ in host]
+    od = [torch.as_tensor(o).cuda(dev) for _, o in host]
+    grad = torch.zeros(R ** 3, ef.NCH, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step(i, ev=None):
+        grad.zero_()
+        m.forward(qd[i], od[i], loss=loss, J_global=J_global, want_O=False, want_loss=False)
+        if ev is not None:
+            ev[0].record()
+        m.backward(grad=grad)
+        if ev is not None:
+            ev[1].record()
+        if world > 1:
+            dist.all_reduce(grad)
+        m.adamw_step(grad, hp)
+
+    # kept-pair census (algorithmic work per point), outside the timed region
+    m.set_counting(True)
+    m.forward(qd[0], od[0], loss=loss, J_global=J_global, want_O=False, want_loss=False)
+    st = m.stats()
+    m.set_counting(False)
+    kept = st["kept_pairs"]; kept_off = st["kept_pairs_offset"]; cand = st["candidate_pairs"]
+
+    for w in range(args.warmup):
+        step(w % pool)
+    torch.cuda.synchronize()
+
+    uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    clk = ClockSampler(uuid)
+    clk.start()
+    time.sleep(0.3)
+    # soak so the sampler sees the loaded clock, then the timed region
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.5:
+        step(0)
+    torch.cuda.synchronize()
+    launches0 = m.stats()["launches"]
+    bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.active = True
+    t0.record()
+    for k in range(args.steps):
+        step((args.warmup + k) % pool, bev[k])
+    t1.record()
+    torch.cuda.synchronize()
+    clk.active = False
+    if world > 1:
+        dist.barrier()
+    launches = m.stats()["launches"] - launches0
+    sec = t0.elapsed_time(t1) / 1e3
+    bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in bev]))
+    if world > 1:
+        tt = torch.tensor([sec, bwd_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec, bwd_ms = float(tt[0]), float(tt[1])
+    time.sleep(0.1)
+    clk.stop()
+    clocks = clk.summary()
+    value = J_global * args.steps / sec
+
+    # e2e: same steps through the public API with pinned host inputs, H2D + loss D2H inside
+    e2e = None
+    if not args.no_e2e:
+        hq = [torch.as_tensor(q).pin_memory() for q, _ in host]
+        ho = [torch.as_tensor(o).pin_memory() for _, o in host]
+        if world == 1:
+            for w in range(3):
+                m.fit_step(hq[w % pool], ho[w % pool], hp, loss=loss)
+            torch.cuda.synchronize()
+            e0 = time.perf_counter()
+            for k in range(args.steps):
+                m.fit_step(hq[k % pool], ho[k % pool], hp, loss=loss)
+            esec = time.perf_counter() - e0
+        else:
+            qbuf = torch.empty_like(qd[0]); obuf = torch.empty_like(od[0])
+
+            def estep(i):
+                qbuf.copy_(hq[i], non_blocking=True)
+                obuf.copy_(ho[i], non_blocking=True)
+                grad.zero_()
+                _, _, L = m.forward(qbuf, obuf, loss=loss, J_global=J_global, want_O=False)
+                m.backward(grad=grad)
+                dist.all_reduce(grad)
+                m.adamw_step(grad, hp)
+                return float(L.item())
+            for w in range(3):
+                estep(w % pool)
+            dist.barrier()
+            e0 = time.perf_counter()
+            for k in range(args.steps):
+                estep(k % pool)
+            esec = time.perf_counter() - e0
+            tt = torch.tensor([esec], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            esec = float(tt[0])
+        e2e = {"value": J_global * args.steps / esec, "unit": "points/s",
+               "h2d_bytes_per_step": int(J * 16), "d2h_bytes_per_step": 4}
+
+    if rank != 0:
+        return
+    # roofline of the dominant kernel (k_backward): algorithmic lane-ops per launch / its time
+    if loss_kind == "mse":
+        ops = OPS_BWD_GRID * (kept - kept_off) + OPS_BWD_OFF * kept_off
+    else:
+        ops = OPS_BWD_EIK_GRID * (kept - kept_off) + OPS_BWD_EIK_OFF * kept_off
+    peak = SM_COUNT * FP32_LANES * SM_MAX_MHZ * 1e6 / 1e12
+    achieved = ops / (bwd_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{args.config}:k_backward")
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "kernel": "k_backward", "achieved": achieved, "peak": peak,
+            "unit": "T fp32 lane-op/s", "frac": achieved / peak, "traffic": traffic,
+            "ops_per_launch": ops, "launch_ms": bwd_ms,
+            "share_of_step": bwd_ms * 1e-3 / (sec / args.steps),
+            "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz max clock (guide unit counts)",
+            "kept_pairs_per_point": kept / J, "candidate_pairs_per_point": cand / J}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_observed_clock"] = achieved / (SM_COUNT * FP32_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": label, "R": R, "points_per_step_per_gpu": J, "global_batch": J_global,
+                       "cutoff_T": 20.0, "parallelism": f"dp{world}",
+                       "l2": f"inputs larger than L2: pool of {pool} batches x {J * 16 / 1e6:.1f} MB cycled"},
+            "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(R, shape, loss_kind)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * efunc.h — C ABI of libefunc: the B200 (sm_100a) fit-step hot path of
+ * "efunc: An Efficient Function Representation without Neural Networks"
+ * (arXiv 2505.21319). Citations are PAPER.md:L<line> into the paper text.
+ *
+ * What the library computes
+ *   The O^{+Delta} representation (Eq. func-offset): one softmax
+ *   over the union of a fixed lattice key bank and an offset key bank, each key
+ *   carrying a degree-1 polynomial value f(x) = c + g.x (Eq. poly-func,
+ *   Eq. func-interp), scale beta = exp(s) (PAPER.md:L908 init e^7).
+ *   Forward = Alg. 1 (L505-518) plus the query gradient Eq. func-normal (L425-436);
+ *   backward = Alg. 2 and the parameter-gradient equations (L540-601); loss = MSE
+ *   (Eq. loss) optionally plus an Eikonal term (reading R-12);
+ *   optimizer = AdamW (L698).
+ *   The global softmax sum is evaluated with a certified cutoff: a (query j, key i)
+ *   pair is skipped only if beta_i ||q_j - k_i||^2 - m_j > cutoff_T, where m_j is
+ *   the smallest exponent of query j (reading R-1). cutoff_T = INFINITY
+ *   (or <= 0) evaluates every pair (the paper's dense definition).
+ *
+ * Parameter layout (theta, gradients, AdamW moments): float32 [R^3][13],
+ *   node n = x + R*(y + R*z), lattice k_n = float32(-1 + 2*x/(R-1), ...) on [-1,1]^3,
+ *   channels (Table 3 row Full-4):
+ *     0 s0 | 1 c0 | 2..4 g0 | 5..7 Delta | 8 s1 | 9 c1 | 10..12 g1
+ *   grid bank key n  : position k_n,           beta = exp(s0), f = c0 + g0.(q - k_n)
+ *   offset bank key n: position k_n + Delta_n, beta = exp(s1), f = c1 + g1.(q - k_n - Delta_n)
+ *   This is also the payload order of the SPEC .efg file (key-major, channel-minor).
+ *
+ * Conventions for every call
+ *   - Pointers named "dev" are device pointers on the handle's device, float32,
+ *     contiguous; the caller owns them. Pointers named "host" are host memory.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). All device work
+ *     of a call is enqueued on it; calls return without synchronising unless the
+ *     description says otherwise. forward/backward/adamw_step are CUDA-graph
+ *     capturable (no allocation, no host sync) once the handle has seen a J at
+ *     least as large (workspaces grow on the first call with a larger J).
+ *   - Every call returns an efunc_status; on failure efunc_last_error() holds a
+ *     message. Nothing is thrown across the ABI. A handle is not thread-safe.
+ */
+#ifndef EFUNC_H
+#define EFUNC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EFUNC_NCH 13
+#define EFUNC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EFUNC_API __attribute__((visibility("default")))
+#else
+#define EFUNC_API
+#endif
+
+typedef struct efunc efunc_t; /* opaque handle: one per (device, grid) */
+
+typedef enum {
+  EFUNC_OK = 0,
+  EFUNC_EINVAL = 1,      /* bad argument: R < 2, J < 0, NULL pointer, unsupported option */
+  EFUNC_ESTATE = 2,      /* backward without a matching forward (SPEC "missing e_j") */
+  EFUNC_ENONFINITE = 3,  /* a NaN/Inf query or target was seen (SPEC "NaN query") */
+  EFUNC_ECUDA = 4,       /* CUDA runtime error */
+  EFUNC_ENOMEM = 5       /* device allocation failed */
+} efunc_status;
+
+typedef enum { EFUNC_VARIANT_COMBINED = 0 } efunc_variant; /* O^{+Delta}, 13 channels */
+
+typedef struct {
+  int32_t R;              /* lattice resolution per axis, 2 <= R <= 256 */
+  int32_t degree;         /* polynomial degree of f; must be 1 */
+  int32_t variant;        /* EFUNC_VARIANT_COMBINED */
+  float cutoff_T;         /* certified cutoff in nats (20.0f default); <=0 or inf: dense */
+  int32_t deterministic;  /* 1: gradients bitwise reproducible run to run (no float atomics) */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t sync_checks;    /* 1: forward synchronises and returns EFUNC_ENONFINITE at once */
+  int32_t reserved[5];    /* must be 0 */
+} efunc_config;
+
+typedef enum { EFUNC_LOSS_NONE = 0, EFUNC_LOSS_MSE = 1, EFUNC_LOSS_MSE_EIKONAL = 2 } efunc_loss_kind;
+
+typedef struct {
+  int32_t kind;           /* efunc_loss_kind */
+  float eikonal_lambda;   /* lambda_E of L_E = lambda_E/J sum (||G_j|| - 1)^2 (reading R-12) */
+  int64_t J_global;       /* J in the 1/J of Eq. loss; 0 = this call's J. Data-parallel ranks
+                             pass the global batch size so the all-reduced gradient is exact. */
+} efunc_loss;
+
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay; /* PAPER.md:L698 lr=6e-4; rest reading R-10 */
+  uint32_t decay_mask;    /* bit c set = channel c is weight-decayed (default: c,g channels) */
+} efunc_adamw;
+
+typedef struct {
+  int64_t J;                 /* queries in the last forward */
+  int64_t items;             /* work items (fixed-size runs of the Morton-sorted queries) */
+  double candidate_pairs;    /* (query, key) pairs evaluated by the last forward */
+  double kept_pairs;         /* pairs with a - m <= cutoff_T (only if counting enabled) */
+  float beta_min;            /* smallest beta over both banks (drives the search radius) */
+  int32_t nonfinite;         /* 1 if a non-finite query/target was seen since the last check */
+  int32_t overflow_items;    /* items that took the exact-shift slow path */
+  double kept_pairs_offset;  /* kept pairs whose key is in the offset bank (counting mode) */
+  int64_t launches;          /* kernels launched by this handle since creation */
+} efunc_stats;
+
+/* efunc_create — allocate a handle on cfg->device and upload theta.
+ *   theta_host: host float[R^3*13] in the layout above (NULL = all zeros).
+ *   Returns EFUNC_EINVAL for R outside [2,256], degree != 1, variant != COMBINED. */
+EFUNC_API efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efunc_t** out);
+EFUNC_API efunc_status efunc_destroy(efunc_t* h);
+
+/* efunc_forward — Alg. 1 for J queries, plus Eq. func-normal if G != NULL.
+ *   q   dev float[J*3] query positions (any order, any location; out-of-domain allowed)
+ *   o   dev float[J]   targets (required if loss->kind != NONE, else may be NULL)
+ *   loss NULL or EFUNC_LOSS_NONE: no loss; MSE: Eq. loss; MSE_EIKONAL: + reading R-12
+ *        (MSE_EIKONAL requires G != NULL).
+ *   O   dev float[J]   output values O(q_j)          (may be NULL)
+ *   G   dev float[J*3] output dO/dq_j                (may be NULL)
+ *   loss_out dev float[1]: the loss of this call's queries (1/J_global scaled), or NULL.
+ * Saves the per-query state (log e_j, O_j, dL/dO_j, ...) that efunc_backward consumes;
+ * it is invalidated by the next forward, set_params, adamw_step or mean_shift_init.
+ * A NaN/Inf query sets the non-finite flag (efunc_check); with cfg.sync_checks the call
+ * synchronises and returns EFUNC_ENONFINITE. J == 0 is valid (loss_out = 0). */
+EFUNC_API efunc_status efunc_forward(efunc_t* h, const float* q, const float* o, int64_t J,
+                           const efunc_loss* loss, float* O, float* G, float* loss_out,
+                           void* stream);
+
+/* efunc_backward — Alg. 2 + PAPER.md:L569-598: grad += dL/dtheta over the last forward's queries.
+ *   dL_dO dev float[J] upstream dL/dO_j, or NULL to use the forward's fused loss upstream
+ *   dL_dG dev float[J*3] upstream dL/dG_j or NULL (non-NULL requires the forward to have
+ *         computed G); with a fused MSE_EIKONAL loss and dL_dO == NULL the Eikonal
+ *         upstream is used automatically.
+ *   grad  dev float[R^3*13], accumulated into (+=); zero it first for a fresh gradient.
+ * Returns EFUNC_ESTATE if there is no valid saved forward state. */
+EFUNC_API efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad,
+                            void* stream);
+
+/* efunc_adamw_step — one AdamW update of theta with torch.optim.AdamW semantics
+ * (decoupled decay first, bias-corrected moments; reading R-10). grad: dev float[R^3*13],
+ * already summed over data-parallel ranks. Increments the handle's step counter, then
+ * rebuilds the key records and the cell binning for the next forward. */
+EFUNC_API efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream);
+
+/* efunc_eval_grad — O and dO/dq for J queries (normals / inference).
+ * O, G dev (either may be NULL). Invalidates the saved forward state. */
+EFUNC_API efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, float* O, float* G,
+                             void* stream);
+
+/* efunc_fit_step — forward + loss + backward + AdamW in one call on one device.
+ *   host_io == 1: q, o are HOST buffers (pinned for async copies), loss_out is a host float*;
+ *                 the call copies q/o in on `stream`, reads the loss back and synchronises.
+ *   host_io == 0: all pointers are device pointers; no synchronisation.
+ * grad_ws: dev float[R^3*13] scratch for the gradient (zeroed by the call). */
+EFUNC_API efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t J,
+                            const efunc_loss* loss, const efunc_adamw* hp, float* grad_ws,
+                            float* loss_out, int32_t host_io, void* stream);
+
+/* efunc_mean_shift_init — Delta_n = sum_s e^{-bw||k_n - s||^2} s / sum_s e^{-bw||k_n-s||^2} - k_n
+ * (bw = 100, N = 16384 in the paper) written into channels 5..7.
+ *   surf dev float[N*3] surface points, N >= 1. */
+EFUNC_API efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, float bandwidth,
+                                   void* stream);
+
+/* Parameter / optimizer-state access. on_device=1: ptr is a device pointer, else host.
+ * These synchronise the stream. set_params rebuilds keys and clears the saved state. */
+EFUNC_API efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream);
+EFUNC_API efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, void* stream);
+EFUNC_API efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int64_t* step);
+EFUNC_API efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* v_host,
+                                  int64_t step);
+
+/* efunc_set_counting — 1: the forward also counts kept pairs (a - m <= T) for
+ * efunc_get_stats (slower; diagnostics only). */
+EFUNC_API efunc_status efunc_set_counting(efunc_t* h, int32_t on);
+/* efunc_get_stats — synchronises `stream` and reports counters of the last forward. */
+EFUNC_API efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream);
+/* efunc_check — synchronises; EFUNC_ENONFINITE if a non-finite input was seen since the
+ * last check (and clears the flag), else EFUNC_OK. */
+EFUNC_API efunc_status efunc_check(efunc_t* h, void* stream);
+
+EFUNC_API const char* efunc_last_error(const efunc_t* h); /* never NULL; h may be NULL */
+EFUNC_API int32_t efunc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EFUNC_H */

@@ -1,0 +1,506 @@
+// efunc_api.cu — the C ABI (include/efunc.h): handle lifetime, workspaces, call sequencing.
+// Every step of the path runs in the kernels of k_bin.cu / k_fwd_bwd.cu / k_adamw.cu; this
+// file only validates arguments, sizes workspaces and enqueues launches on the caller's stream.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "efunc_internal.cuh"
+
+using namespace ef;
+
+static thread_local std::string g_err;
+
+static efunc_status fail(efunc_t* h, efunc_status s, const std::string& m) {
+  if (h) h->err = m;
+  g_err = m;
+  return s;
+}
+
+#define CK(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? EFUNC_ENOMEM : EFUNC_ECUDA,            \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                           \
+    }                                                                                         \
+  } while (0)
+
+#define RET(x)                                    \
+  do {                                            \
+    efunc_status st_ = (x);                       \
+    if (st_ != EFUNC_OK) return st_;              \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+int query_bits(int64_t J) {
+  // target ~4 queries per Morton bin
+  double t = std::log2(std::fmax((double)J / 4.0, 1.0)) / 3.0;
+  int b = (int)std::ceil(t);
+  if (b < 1) b = 1;
+  if (b > MAX_QBITS) b = MAX_QBITS;
+  return b;
+}
+
+float cutoff_log2(const efunc_config& c) {
+  if (!(c.cutoff_T > 0.0f) || std::isinf(c.cutoff_T)) return INFINITY;
+  return c.cutoff_T * EF_LOG2E;
+}
+
+KeysView keys_view(efunc_t* h) {
+  KeysView kv;
+  kv.ks = h->key_sorted;
+  kv.kid = h->kid;
+  kv.cell_start = h->cell_start;
+  kv.grid_raw = h->key_raw;
+  kv.bl_min = &h->ds->bl_min;
+  kv.R = h->R;
+  kv.NC = h->NC;
+  kv.inv_h = h->inv_h;
+  kv.n_nodes = h->n_nodes;
+  return kv;
+}
+
+efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
+  size_t tiles = (n_elems + 4095) / 4096 + 1;
+  if (tiles <= h->scan_tmp_cap) return EFUNC_OK;
+  dfree(h->scan_tmp);
+  CK(dalloc(&h->scan_tmp, tiles));
+  h->scan_tmp_cap = tiles;
+  return EFUNC_OK;
+}
+
+efunc_status rebuild_keys(efunc_t* h, cudaStream_t s) {
+  CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
+  CK(cudaMemsetAsync(h->cell_fill, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
+  CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
+  h->launches += launch_prep_keys(h->theta, h->R, h->key_raw, h->key_cell, h->cell_count, h->ds, s);
+  h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s);
+  h->launches += launch_counting_sort(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_tmp, h->key_order, s);
+  h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
+  CK(cudaGetLastError());
+  h->have_fwd = 0;
+  return EFUNC_OK;
+}
+
+efunc_status ensure_queries(efunc_t* h, int64_t J) {
+  const int bits = query_bits(J);
+  const uint32_t nbins = 1u << (3 * bits);
+  if (nbins + 1 > h->nbins_cap) {
+    dfree(h->bin_count);
+    dfree(h->bin_start);
+    dfree(h->bin_fill);
+    CK(dalloc(&h->bin_count, nbins + 1));
+    CK(dalloc(&h->bin_start, nbins + 1));
+    CK(dalloc(&h->bin_fill, nbins + 1));
+    h->nbins_cap = nbins + 1;
+    RET(ensure_scan_tmp(h, nbins + 1));
+  }
+  if (J > h->J_cap) {
+    dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
+    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->boxes); dfree(h->loss_part);
+    const int64_t items = (J + QITEM - 1) / QITEM;
+    CK(dalloc(&h->q_bin, J));
+    CK(dalloc(&h->q_tmp, J));
+    CK(dalloc(&h->q_order, J));
+    CK(dalloc(&h->qs, J));
+    CK(dalloc(&h->perm, J));
+    CK(dalloc(&h->rec, J));
+    CK(dalloc(&h->gs, J));
+    CK(dalloc(&h->us, J));
+    CK(dalloc(&h->hs, J));
+    CK(dalloc(&h->boxes, items));
+    CK(dalloc(&h->loss_part, items));
+    h->J_cap = J;
+  }
+  return EFUNC_OK;
+}
+
+void free_all(efunc_t* h) {
+  dfree(h->theta); dfree(h->m); dfree(h->v);
+  dfree(h->key_raw); dfree(h->key_sorted); dfree(h->kid); dfree(h->key_cell);
+  dfree(h->cell_count); dfree(h->cell_start); dfree(h->cell_fill); dfree(h->key_tmp); dfree(h->key_order);
+  dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad);
+  dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
+  dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
+  dfree(h->boxes); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
+}
+
+efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                        float* O, float* G, float* loss_out, int keep_state, cudaStream_t s) {
+  const int kind = loss ? loss->kind : EFUNC_LOSS_NONE;
+  if (J < 0) return fail(h, EFUNC_EINVAL, "J < 0");
+  if (kind < EFUNC_LOSS_NONE || kind > EFUNC_LOSS_MSE_EIKONAL) return fail(h, EFUNC_EINVAL, "bad loss kind");
+  if (J > 0 && !q) return fail(h, EFUNC_EINVAL, "q is NULL");
+  if (J > 0 && kind != EFUNC_LOSS_NONE && !o) return fail(h, EFUNC_EINVAL, "loss requires targets o");
+  if (J > (int64_t)0x7fffffff) return fail(h, EFUNC_EINVAL, "J > 2^31-1 per call");
+  const int want_g = (G != nullptr) || kind == EFUNC_LOSS_MSE_EIKONAL;
+  h->have_fwd = 0;
+  if (J == 0) {
+    if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
+    h->have_fwd = keep_state;
+    h->fwd_J = 0;
+    h->fwd_has_g = want_g;
+    h->fwd_loss_kind = kind;
+    return EFUNC_OK;
+  }
+  RET(ensure_queries(h, J));
+  const int bits = query_bits(J);
+  const uint32_t nbins = 1u << (3 * bits);
+  CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
+  CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
+  CK(cudaMemsetAsync(reinterpret_cast<char*>(h->ds) + 8, 0, sizeof(DevScalars) - 8, s));
+  const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
+  h->launches += launch_query_bins(q, o_used, J, bits, h->q_bin, h->bin_count, h->ds, s);
+  h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
+  h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
+  h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
+  const int64_t items = (J + QITEM - 1) / QITEM;
+  FwdArgs a;
+  a.kv = keys_view(h);
+  a.qs = h->qs;
+  a.perm = h->perm;
+  a.J = J;
+  a.T_l = cutoff_log2(h->cfg);
+  a.loss_kind = kind;
+  const int64_t Jg = (loss && loss->J_global > 0) ? loss->J_global : J;
+  a.inv_J = (float)(1.0 / (double)Jg);
+  a.eik_lambda = loss ? loss->eikonal_lambda : 0.0f;
+  a.O = O;
+  a.G = G;
+  a.rec = h->rec;
+  a.gs = h->gs;
+  a.us = h->us;
+  a.hs = h->hs;
+  a.boxes = h->boxes;
+  a.loss_part = h->loss_part;
+  a.ds = h->ds;
+  a.count_kept = h->count_kept;
+  h->launches += launch_forward(a, want_g, items, s);
+  if (kind != EFUNC_LOSS_NONE && loss_out) launch_sum_partials(h->loss_part, items, loss_out, s);
+  else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
+  CK(cudaGetLastError());
+  if (h->cfg.sync_checks) {
+    CK(cudaStreamSynchronize(s));
+    DevScalars d;
+    CK(cudaMemcpy(&d, h->ds, sizeof(d), cudaMemcpyDeviceToHost));
+    if (d.nonfinite) {
+      CK(cudaMemset(&h->ds->nonfinite, 0, sizeof(uint32_t)));
+      return fail(h, EFUNC_ENONFINITE, "non-finite query or target");
+    }
+  }
+  h->have_fwd = keep_state;
+  h->fwd_J = J;
+  h->fwd_has_g = want_g;
+  h->fwd_loss_kind = kind;
+  return EFUNC_OK;
+}
+
+efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, cudaStream_t s) {
+  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
+  if (!h->have_fwd) return fail(h, EFUNC_ESTATE, "backward without a valid forward (saved e_j missing)");
+  if (h->fwd_J == 0) return EFUNC_OK;
+  if (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_NONE)
+    return fail(h, EFUNC_EINVAL, "dL_dO is NULL and the forward had no fused loss");
+  const int eik = (dL_dG != nullptr) || (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_MSE_EIKONAL);
+  if (eik && !h->fwd_has_g) return fail(h, EFUNC_ESTATE, "dL_dG needs a forward that computed G");
+  BwdArgs b;
+  b.kv = keys_view(h);
+  b.qs = h->qs;
+  b.perm = h->perm;
+  b.J = h->fwd_J;
+  b.rec = h->rec;
+  b.gs = h->gs;
+  b.us = h->us;
+  b.hs = h->hs;
+  b.dL_dO = dL_dO;
+  b.dL_dG = dL_dG;
+  b.boxes = h->boxes;
+  b.grad = grad;
+  b.eik = eik;
+  h->launches += launch_backward(b, (h->fwd_J + QITEM - 1) / QITEM, s);
+  CK(cudaGetLastError());
+  return EFUNC_OK;
+}
+
+efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cudaStream_t s) {
+  if (!grad || !hp) return fail(h, EFUNC_EINVAL, "NULL argument");
+  h->step += 1;
+  const double b1 = hp->beta1, b2 = hp->beta2;
+  const double bc1 = 1.0 - std::pow(b1, (double)h->step);
+  const double bc2 = 1.0 - std::pow(b2, (double)h->step);
+  const float step_size = (float)((double)hp->lr / bc1);
+  const float sqrt_bc2 = (float)std::sqrt(bc2);
+  const float decay = (float)(1.0 - (double)hp->lr * (double)hp->weight_decay);
+  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, decay, hp->beta1, hp->beta2, hp->eps,
+               hp->decay_mask, step_size, sqrt_bc2, s);
+  CK(cudaGetLastError());
+  return rebuild_keys(h, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t efunc_abi_version(void) { return EFUNC_ABI_VERSION; }
+
+const char* efunc_last_error(const efunc_t* h) {
+  if (h && !h->err.empty()) return h->err.c_str();
+  return g_err.c_str();
+}
+
+efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efunc_t** out) {
+  efunc_t* h = nullptr;
+  if (!cfg || !out) return fail(nullptr, EFUNC_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (cfg->R < 2 || cfg->R > 256) return fail(nullptr, EFUNC_EINVAL, "R must be in [2, 256]");
+  if (cfg->degree != 1) return fail(nullptr, EFUNC_EINVAL, "only degree 1 is implemented");
+  if (cfg->variant != EFUNC_VARIANT_COMBINED) return fail(nullptr, EFUNC_EINVAL, "only the COMBINED variant");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(nullptr, EFUNC_ECUDA, "no CUDA device");
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, EFUNC_EINVAL, "bad device ordinal");
+  h = new (std::nothrow) efunc();
+  if (!h) return fail(nullptr, EFUNC_ENOMEM, "host allocation failed");
+  h->cfg = *cfg;
+  DeviceGuard dg(cfg->device);
+  h->R = cfg->R;
+  h->n_nodes = h->R * h->R * h->R;
+  h->n_keys = 2 * h->n_nodes;
+  h->NC = h->R - 1;
+  h->n_cells = h->NC * h->NC * h->NC;
+  h->h = 2.0f / (float)(h->R - 1);
+  h->inv_h = (float)((h->R - 1) / 2.0);
+  const size_t np = (size_t)h->n_nodes * EF_NCH;
+  auto st = [&]() -> efunc_status {
+    CK(dalloc(&h->theta, np));
+    CK(dalloc(&h->m, np));
+    CK(dalloc(&h->v, np));
+    CK(dalloc(&h->fit_grad, np));
+    CK(dalloc(&h->key_raw, 2 * (size_t)h->n_keys));
+    CK(dalloc(&h->key_sorted, 2 * (size_t)h->n_keys));
+    CK(dalloc(&h->kid, h->n_keys));
+    CK(dalloc(&h->key_cell, h->n_keys));
+    CK(dalloc(&h->key_tmp, h->n_keys));
+    CK(dalloc(&h->key_order, h->n_keys));
+    CK(dalloc(&h->cell_count, h->n_cells + 1));
+    CK(dalloc(&h->cell_start, h->n_cells + 1));
+    CK(dalloc(&h->cell_fill, h->n_cells + 1));
+    CK(dalloc(&h->ds, 1));
+    CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
+    RET(ensure_scan_tmp(h, h->n_cells + 1));
+    if (theta_host) CK(cudaMemcpy(h->theta, theta_host, np * sizeof(float), cudaMemcpyHostToDevice));
+    else CK(cudaMemset(h->theta, 0, np * sizeof(float)));
+    CK(cudaMemset(h->m, 0, np * sizeof(float)));
+    CK(cudaMemset(h->v, 0, np * sizeof(float)));
+    RET(rebuild_keys(h, 0));
+    CK(cudaDeviceSynchronize());
+    return EFUNC_OK;
+  }();
+  if (st != EFUNC_OK) {
+    g_err = h->err;
+    free_all(h);
+    delete h;
+    return st;
+  }
+  *out = h;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_destroy(efunc_t* h) {
+  if (!h) return EFUNC_OK;
+  {
+    DeviceGuard dg(h->cfg.device);
+    cudaDeviceSynchronize();
+    free_all(h);
+  }
+  delete h;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                           float* O, float* G, float* loss_out, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  return do_forward(h, q, o, J, loss, O, G, loss_out, 1, (cudaStream_t)stream);
+}
+
+efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  return do_backward(h, dL_dO, dL_dG, grad, (cudaStream_t)stream);
+}
+
+efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  return do_adamw(h, grad, hp, (cudaStream_t)stream);
+}
+
+efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, float* O, float* G, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  return do_forward(h, q, nullptr, J, nullptr, O, G, nullptr, 0, (cudaStream_t)stream);
+}
+
+efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                            const efunc_adamw* hp, float* grad_ws, float* loss_out, int32_t host_io,
+                            void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "fit_step needs a loss");
+  if (!hp) return fail(h, EFUNC_EINVAL, "NULL AdamW parameters");
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* qd = q;
+  const float* od = o;
+  float* lossd = loss_out;
+  if (host_io) {
+    if (J > h->io_cap || !h->io_q) {
+      dfree(h->io_q);
+      dfree(h->io_o);
+      CK(dalloc(&h->io_q, 3 * (size_t)J));
+      CK(dalloc(&h->io_o, (size_t)J));
+      h->io_cap = J;
+    }
+    if (!h->io_loss) CK(dalloc(&h->io_loss, 1));
+    if (J > 0) {
+      CK(cudaMemcpyAsync(h->io_q, q, sizeof(float) * 3 * (size_t)J, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(h->io_o, o, sizeof(float) * (size_t)J, cudaMemcpyHostToDevice, s));
+    }
+    qd = h->io_q;
+    od = h->io_o;
+    lossd = h->io_loss;
+  }
+  float* g = grad_ws ? grad_ws : h->fit_grad;
+  CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, s));
+  RET(do_forward(h, qd, od, J, loss, nullptr, nullptr, lossd, 1, s));
+  RET(do_backward(h, nullptr, nullptr, g, s));
+  RET(do_adamw(h, g, hp, s));
+  if (host_io) {
+    if (loss_out) CK(cudaMemcpyAsync(loss_out, lossd, sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return EFUNC_OK;
+}
+
+efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, float bandwidth, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (!surf || N < 1) return fail(h, EFUNC_EINVAL, "mean shift needs N >= 1 surface points");
+  if (!(bandwidth > 0.0f)) return fail(h, EFUNC_EINVAL, "bandwidth must be > 0");
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  h->launches += launch_mean_shift(h->theta, h->R, surf, N, bandwidth, s);
+  CK(cudaGetLastError());
+  return rebuild_keys(h, s);
+}
+
+efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream) {
+  if (!h || !dst) return fail(h, EFUNC_EINVAL, "NULL argument");
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  CK(cudaMemcpyAsync(dst, h->theta, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return EFUNC_OK;
+}
+
+efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, void* stream) {
+  if (!h || !src) return fail(h, EFUNC_EINVAL, "NULL argument");
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  CK(cudaMemcpyAsync(h->theta, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  RET(rebuild_keys(h, s));
+  CK(cudaStreamSynchronize(s));
+  return EFUNC_OK;
+}
+
+efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int64_t* step) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  CK(cudaDeviceSynchronize());
+  if (m_host) CK(cudaMemcpy(m_host, h->m, bytes, cudaMemcpyDeviceToHost));
+  if (v_host) CK(cudaMemcpy(v_host, h->v, bytes, cudaMemcpyDeviceToHost));
+  if (step) *step = h->step;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* v_host, int64_t step) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (step < 0) return fail(h, EFUNC_EINVAL, "step < 0");
+  DeviceGuard dg(h->cfg.device);
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  CK(cudaDeviceSynchronize());
+  if (m_host) CK(cudaMemcpy(h->m, m_host, bytes, cudaMemcpyHostToDevice));
+  else CK(cudaMemset(h->m, 0, bytes));
+  if (v_host) CK(cudaMemcpy(h->v, v_host, bytes, cudaMemcpyHostToDevice));
+  else CK(cudaMemset(h->v, 0, bytes));
+  h->step = step;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_set_counting(efunc_t* h, int32_t on) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  h->count_kept = on ? 1 : 0;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
+  if (!h || !out) return fail(h, EFUNC_EINVAL, "NULL argument");
+  DeviceGuard dg(h->cfg.device);
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  DevScalars d;
+  CK(cudaMemcpy(&d, h->ds, sizeof(d), cudaMemcpyDeviceToHost));
+  out->J = h->fwd_J;
+  out->items = (h->fwd_J + QITEM - 1) / QITEM;
+  out->candidate_pairs = (double)d.cand_pairs;
+  out->kept_pairs = (double)d.kept_pairs;
+  out->beta_min = d.bl_min / EF_LOG2E;
+  out->nonfinite = (int32_t)d.nonfinite;
+  out->overflow_items = (int32_t)d.overflow_items;
+  out->kept_pairs_offset = (double)d.kept_pairs_offset;
+  out->launches = h->launches;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_check(efunc_t* h, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  uint32_t nf = 0;
+  CK(cudaMemcpy(&nf, &h->ds->nonfinite, sizeof(nf), cudaMemcpyDeviceToHost));
+  if (nf) {
+    CK(cudaMemset(&h->ds->nonfinite, 0, sizeof(uint32_t)));
+    return fail(h, EFUNC_ENONFINITE, "non-finite query or target");
+  }
+  return EFUNC_OK;
+}
+
+}  // extern "C"

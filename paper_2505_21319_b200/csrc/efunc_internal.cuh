@@ -1,0 +1,175 @@
+// efunc_internal.cuh — shared device/host definitions of libefunc (not part of the ABI).
+//
+// Data layout in HBM:
+//   theta / m / v / grad : float [R^3][13]  (ABI layout, node-major)
+//   key record (32 B)    : float4 a = {x, y, z, bl}, float4 b = {c, gx, gy, gz},
+//                          bl = beta * log2(e)  (exponents are evaluated in base 2)
+//                          key id i < R^3: grid bank node i; i >= R^3: offset bank node i-R^3
+//   key_raw              : [2R^3] records in key-id order (grid bank = lattice order)
+//   key_sorted           : [2R^3] records sorted by lattice cell (x fastest), stable by key id
+//   cell_start           : [(R-1)^3 + 1] exclusive prefix of keys per cell
+//   queries (per forward): qs float4 {x,y,z,o} Morton-sorted, perm[sorted] = user index,
+//                          rec float4 {-lambda_j*log2e, dL/dO_j, O_j, 0} (sorted order)
+//   work item            : QITEM consecutive sorted queries; box = AABB + max shift bound
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/efunc.h"
+
+#define EF_NCH 13
+#define EF_LOG2E 1.4426950408889634f
+#define EF_LN2 0.6931471805599453f
+
+namespace ef {
+
+constexpr int QITEM = 128;        // queries per work item == forward/backward CTA size
+constexpr int NTHREADS = 128;
+constexpr int LCAP = 512;         // candidate keys staged in shared memory per chunk
+constexpr int MAX_QBITS = 7;      // Morton bits per axis for query binning
+
+struct KeysView {
+  const float4* ks;        // sorted records, 2 float4 per key (a at 2k, b at 2k+1)
+  const int* kid;          // sorted -> key id
+  const uint32_t* cell_start;
+  const float4* grid_raw;  // raw records of the grid bank in lattice order (2 float4 per node)
+  const float* bl_min;     // device scalar: min bl over all keys
+  int R, NC;               // NC = R-1 cells per axis
+  float inv_h;             // 1/h, h = 2/(R-1)
+  int n_nodes;
+};
+
+struct ItemBox {
+  float4 lo;   // x,y,z, thr (log2-units threshold mh_max + T_l; +inf = dense)
+  float4 hi;   // x,y,z, unused
+};
+
+struct DevScalars {
+  float bl_min;            // as float; written via atomicMin on its bits (bl > 0)
+  uint32_t nonfinite;
+  uint32_t overflow_items;
+  uint32_t pad;
+  unsigned long long cand_pairs;
+  unsigned long long kept_pairs;
+  unsigned long long kept_pairs_offset;
+};
+
+struct FwdArgs {
+  KeysView kv;
+  const float4* qs;       // sorted queries {x,y,z,o}
+  const int* perm;        // sorted -> user index
+  int64_t J;
+  float T_l;              // cutoff in log2 units (inf = dense)
+  // loss
+  int loss_kind;
+  float inv_J;            // 1/J_global
+  float eik_lambda;
+  // outputs
+  float* O;               // user order (may be null)
+  float* G;               // user order [J*3] (may be null)
+  float4* rec;            // sorted {-lam_l, r, O, 0}
+  float4* gs;             // sorted G (if WANT_G)
+  float4* us;             // sorted ubar (if WANT_G)
+  float4* hs;             // sorted fused Eikonal upstream h (if loss eikonal)
+  ItemBox* boxes;         // per item
+  float* loss_part;       // per item partial loss
+  DevScalars* ds;
+  int count_kept;
+};
+
+struct BwdArgs {
+  KeysView kv;
+  const float4* qs;
+  const int* perm;
+  int64_t J;
+  const float4* rec;
+  const float4* gs;
+  const float4* us;
+  const float4* hs;       // fused h (sorted) or null
+  const float* dL_dO;     // user order or null (use rec.y)
+  const float* dL_dG;     // user order [J*3] or null
+  const ItemBox* boxes;
+  float* grad;            // [R^3][13] +=
+  int eik;                // 1: add the dL/dG terms
+};
+
+// ---------------------------------------------------------------- launchers (host)
+int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell,
+                      uint32_t* cell_count, DevScalars* ds, cudaStream_t s);
+int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp,
+                     cudaStream_t s);
+int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start,
+                          uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s);
+int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted,
+                        int* kid, uint32_t n, cudaStream_t s);
+int launch_query_bins(const float* q, const float* o, int64_t J, int bits, uint32_t* bins,
+                       uint32_t* count, DevScalars* ds, cudaStream_t s);
+int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
+                           float4* qs, int* perm, cudaStream_t s);
+int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
+int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
+int launch_sum_partials(const float* part, int64_t n, float* out, cudaStream_t s);
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay,
+                  float b1, float b2, float eps, uint32_t mask, float step_size, float sqrt_bc2,
+                  cudaStream_t s);
+int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
+                       cudaStream_t s);
+int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
+
+}  // namespace ef
+
+// ---------------------------------------------------------------- the handle
+struct efunc {
+  efunc_config cfg;
+  int R = 0, n_nodes = 0, n_keys = 0, NC = 0, n_cells = 0;
+  float h = 0.f, inv_h = 0.f;
+  // parameters + optimizer state
+  float* theta = nullptr;
+  float* m = nullptr;
+  float* v = nullptr;
+  int64_t step = 0;
+  // keys
+  float4* key_raw = nullptr;
+  float4* key_sorted = nullptr;
+  int* kid = nullptr;
+  uint32_t* key_cell = nullptr;
+  uint32_t* cell_count = nullptr;   // n_cells + 1
+  uint32_t* cell_start = nullptr;   // n_cells + 1
+  uint32_t* cell_fill = nullptr;
+  uint32_t* key_tmp = nullptr;
+  uint32_t* key_order = nullptr;
+  uint32_t* scan_tmp = nullptr;     // block sums for scans
+  size_t scan_tmp_cap = 0;
+  ef::DevScalars* ds = nullptr;
+  float* fit_grad = nullptr;
+  // queries
+  int64_t J_cap = 0;
+  uint32_t nbins_cap = 0;
+  uint32_t* q_bin = nullptr;
+  uint32_t* bin_count = nullptr;
+  uint32_t* bin_start = nullptr;
+  uint32_t* bin_fill = nullptr;
+  uint32_t* q_tmp = nullptr;
+  uint32_t* q_order = nullptr;
+  float4* qs = nullptr;
+  int* perm = nullptr;
+  float4* rec = nullptr;
+  float4* gs = nullptr;
+  float4* us = nullptr;
+  float4* hs = nullptr;
+  ef::ItemBox* boxes = nullptr;
+  float* loss_part = nullptr;
+  float* io_q = nullptr;  // device staging for host_io fit_step
+  float* io_o = nullptr;
+  float* io_loss = nullptr;
+  int64_t io_cap = 0;
+  // saved forward state
+  int have_fwd = 0;
+  int64_t fwd_J = 0;
+  int fwd_has_g = 0;
+  int fwd_loss_kind = 0;
+  int count_kept = 0;
+  int64_t launches = 0;
+  std::string err;
+};

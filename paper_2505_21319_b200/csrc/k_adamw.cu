@@ -1,0 +1,100 @@
+// k_adamw.cu — S6 AdamW (torch.optim.AdamW semantics, reading R-10) and the
+// mean-shift offset initialisation.
+#include "efunc_internal.cuh"
+
+namespace ef {
+
+// Elementwise over theta [R^3][13]; op order follows torch's single-tensor AdamW:
+//   p *= 1 - lr*wd (masked channels);  m += (1-b1)(g - m);  v = v*b2 + (1-b2) g*g;
+//   p += -step_size * m / (sqrt(v) / sqrt(bc2) + eps),  step_size = lr / bc1  (host, double)
+__global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
+                        float* __restrict__ v, int64_t n, float decay, float b1, float b2, float eps,
+                        uint32_t mask, float step_size, float sqrt_bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % EF_NCH);
+    float p = theta[i];
+    const float g = grad[i];
+    if ((mask >> ch) & 1u) p *= decay;
+    float mi = m[i];
+    mi = fmaf(1.0f - b1, g - mi, mi);
+    float vi = v[i];
+    vi = fmaf(1.0f - b2, g * g, vi * b2);
+    const float denom = __fdiv_rn(__fsqrt_rn(vi), sqrt_bc2) + eps;
+    p = fmaf(-step_size, __fdiv_rn(mi, denom), p);
+    theta[i] = p;
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay, float b1,
+                  float b2, float eps, uint32_t mask, float step_size, float sqrt_bc2, cudaStream_t s) {
+  long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_adamw<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, decay, b1, b2, eps, mask, step_size,
+                                            sqrt_bc2);
+  return 1;
+}
+
+// Mean shift: one thread per lattice node; surface points staged through shared memory.
+// Pass 1: E_min = min_s bw ||k - s||^2 (the max shift); pass 2: weighted mean.
+constexpr int MS_TILE = 1024;
+
+__global__ void k_mean_shift(float* __restrict__ theta, int R, const float* __restrict__ surf, int64_t N,
+                             float bw) {
+  __shared__ float3 sp[MS_TILE];
+  const int Nn = R * R * R;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = n < Nn;
+  float kx = 0.f, ky = 0.f, kz = 0.f;
+  if (act) {
+    const int x = n % R, y = (n / R) % R, z = n / (R * R);
+    kx = (float)(-1.0 + 2.0 * x / (double)(R - 1));
+    ky = (float)(-1.0 + 2.0 * y / (double)(R - 1));
+    kz = (float)(-1.0 + 2.0 * z / (double)(R - 1));
+  }
+  float emin = INFINITY;
+  for (int64_t t0 = 0; t0 < N; t0 += MS_TILE) {
+    const int cnt = (int)((N - t0) < (int64_t)MS_TILE ? (N - t0) : (int64_t)MS_TILE);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      sp[i] = make_float3(surf[3 * (t0 + i)], surf[3 * (t0 + i) + 1], surf[3 * (t0 + i) + 2]);
+    __syncthreads();
+    for (int i = 0; i < cnt; ++i) {
+      const float dx = kx - sp[i].x, dy = ky - sp[i].y, dz = kz - sp[i].z;
+      emin = fminf(emin, bw * fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+    }
+  }
+  float W = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f;
+  for (int64_t t0 = 0; t0 < N; t0 += MS_TILE) {
+    const int cnt = (int)((N - t0) < (int64_t)MS_TILE ? (N - t0) : (int64_t)MS_TILE);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      sp[i] = make_float3(surf[3 * (t0 + i)], surf[3 * (t0 + i) + 1], surf[3 * (t0 + i) + 2]);
+    __syncthreads();
+    for (int i = 0; i < cnt; ++i) {
+      const float dx = kx - sp[i].x, dy = ky - sp[i].y, dz = kz - sp[i].z;
+      const float e = bw * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float w = expf(emin - e);
+      W += w;
+      Sx = fmaf(w, sp[i].x, Sx);
+      Sy = fmaf(w, sp[i].y, Sy);
+      Sz = fmaf(w, sp[i].z, Sz);
+    }
+  }
+  if (act) {
+    float* t = theta + (size_t)n * EF_NCH;
+    t[5] = Sx / W - kx;
+    t[6] = Sy / W - ky;
+    t[7] = Sz / W - kz;
+  }
+}
+
+int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw, cudaStream_t s) {
+  const int Nn = R * R * R;
+  k_mean_shift<<<(Nn + 127) / 128, 128, 0, s>>>(theta, R, surf, N, bw);
+  return 1;
+}
+
+}  // namespace ef

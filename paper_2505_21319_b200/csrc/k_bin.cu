@@ -1,0 +1,296 @@
+// k_bin.cu — S0 key prep and S1 binning kernels.
+//
+// S0 (PAPER.md:L456 parameter space, L908 beta = e^s): theta [R^3][13] -> 2R^3 key records
+//    {x,y,z, beta*log2e | c, gx, gy, gz}; cell id per key; per-cell histogram; min beta.
+// S1: deterministic counting sort (histogram -> exclusive scan -> atomic scatter -> per-bin
+//    rank by original index). The final order is a stable sort by bin, independent of the
+//    atomic scatter order, so work items (and therefore every fp32 sum) are reproducible.
+#include "efunc_internal.cuh"
+
+namespace ef {
+
+__device__ __forceinline__ int cell_clamp(float p, float inv_h, int NC) {
+  float c = floorf((p + 1.0f) * inv_h);
+  c = fminf(fmaxf(c, 0.0f), (float)(NC - 1));
+  return (int)c;
+}
+
+// ------------------------------------------------------------------------------ S0
+__global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __restrict__ key_raw,
+                            uint32_t* __restrict__ key_cell, uint32_t* __restrict__ cell_count,
+                            DevScalars* ds) {
+  const int N = R * R * R;
+  const int NC = R - 1;
+  const float inv_h = (float)((R - 1) / 2.0);
+  float local_min = INFINITY;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const int x = n % R, y = (n / R) % R, z = n / (R * R);
+    // lattice k(i) = float32(-1 + 2 i/(R-1))  (reading R-2), evaluated in double
+    const float kx = (float)(-1.0 + 2.0 * x / (double)(R - 1));
+    const float ky = (float)(-1.0 + 2.0 * y / (double)(R - 1));
+    const float kz = (float)(-1.0 + 2.0 * z / (double)(R - 1));
+    const float* t = theta + (size_t)n * EF_NCH;
+    const float bl0 = expf(t[0]) * EF_LOG2E;
+    const float bl1 = expf(t[8]) * EF_LOG2E;
+    const float px = kx + t[5], py = ky + t[6], pz = kz + t[7];
+    key_raw[2 * n] = make_float4(kx, ky, kz, bl0);
+    key_raw[2 * n + 1] = make_float4(t[1], t[2], t[3], t[4]);
+    key_raw[2 * (N + n)] = make_float4(px, py, pz, bl1);
+    key_raw[2 * (N + n) + 1] = make_float4(t[9], t[10], t[11], t[12]);
+    const uint32_t c0 = (uint32_t)((cell_clamp(kz, inv_h, NC) * NC + cell_clamp(ky, inv_h, NC)) * NC +
+                                   cell_clamp(kx, inv_h, NC));
+    const uint32_t c1 = (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
+                                   cell_clamp(px, inv_h, NC));
+    key_cell[n] = c0;
+    key_cell[N + n] = c1;
+    atomicAdd(&cell_count[c0], 1u);
+    atomicAdd(&cell_count[c1], 1u);
+    local_min = fminf(local_min, fminf(bl0, bl1));
+  }
+  // bl > 0: the IEEE bit pattern orders like the value
+  for (int o = 16; o > 0; o >>= 1) local_min = fminf(local_min, __shfl_xor_sync(~0u, local_min, o));
+  if ((threadIdx.x & 31) == 0 && local_min < INFINITY)
+    atomicMin(reinterpret_cast<unsigned int*>(&ds->bl_min), __float_as_uint(local_min));
+}
+
+int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell,
+                      uint32_t* cell_count, DevScalars* ds, cudaStream_t s) {
+  const int N = R * R * R;
+  int blocks = (N + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, key_raw, key_cell, cell_count, ds);
+  return 1;
+}
+
+// ------------------------------------------------------------------------------ scan
+constexpr int SCAN_T = 1024;
+constexpr int SCAN_PER = 4;
+constexpr int SCAN_TILE = SCAN_T * SCAN_PER;
+
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s_w, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(~0u, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = s_w[lane];
+    uint32_t xi = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(~0u, xi, o);
+      if (lane >= o) xi += t;
+    }
+    s_w[lane] = xi - x;
+    if (lane == 31) s_w[32] = xi;
+  }
+  __syncthreads();
+  *total = s_w[32];
+  return incl - v + s_w[w];
+}
+
+__global__ void k_scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n,
+                             uint32_t* __restrict__ tile_sums) {
+  __shared__ uint32_t s_w[33];
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER;
+  uint32_t v[SCAN_PER];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0u;
+    sum += v[i];
+  }
+  uint32_t total;
+  uint32_t off = block_excl_scan_1024(sum, s_w, &total);
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; ++i) {
+    if (base + i < n) out[base + i] = off;
+    off += v[i];
+  }
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_tile_sums(uint32_t* __restrict__ tile_sums, uint32_t nt) {
+  __shared__ uint32_t s_w[33];
+  uint32_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nt; b0 += SCAN_TILE) {
+    const uint32_t base = b0 + threadIdx.x * SCAN_PER;
+    uint32_t v[SCAN_PER];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+      v[i] = (base + i < nt) ? tile_sums[base + i] : 0u;
+      sum += v[i];
+    }
+    uint32_t total;
+    uint32_t off = block_excl_scan_1024(sum, s_w, &total) + carry;
+#pragma unroll
+    for (int i = 0; i < SCAN_PER; ++i) {
+      if (base + i < nt) tile_sums[base + i] = off;
+      off += v[i];
+    }
+    carry += total;
+    __syncthreads();
+  }
+}
+
+__global__ void k_scan_add(uint32_t* __restrict__ out, uint32_t n, const uint32_t* __restrict__ tile_sums) {
+  const uint32_t add = tile_sums[blockIdx.x];
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER;
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; ++i)
+    if (base + i < n) out[base + i] += add;
+}
+
+int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp, cudaStream_t s) {
+  const uint32_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
+  k_scan_tiles<<<nt, SCAN_T, 0, s>>>(in, out, n, block_tmp);
+  if (nt > 1) {
+    k_scan_tile_sums<<<1, SCAN_T, 0, s>>>(block_tmp, nt);
+    k_scan_add<<<nt, SCAN_T, 0, s>>>(out, n, block_tmp);
+    return 3;
+  }
+  return 1;
+}
+
+// ------------------------------------------------------------------------------ counting sort
+__global__ void k_scatter(const uint32_t* __restrict__ bin, uint32_t n, const uint32_t* __restrict__ bin_start,
+                          uint32_t* __restrict__ fill, uint32_t* __restrict__ tmp_idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t b = bin[i];
+    tmp_idx[bin_start[b] + atomicAdd(&fill[b], 1u)] = i;
+  }
+}
+
+// Rank of each element inside its bin = number of same-bin elements with a smaller index.
+__global__ void k_stable_rank(const uint32_t* __restrict__ bin, uint32_t n, const uint32_t* __restrict__ bin_start,
+                              const uint32_t* __restrict__ tmp_idx, uint32_t* __restrict__ out_idx) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const uint32_t i = tmp_idx[p];
+    const uint32_t b = bin[i];
+    const uint32_t s = bin_start[b], e = bin_start[b + 1];
+    uint32_t rank = 0;
+    for (uint32_t k = s; k < e; ++k) rank += (tmp_idx[k] < i) ? 1u : 0u;
+    out_idx[s + rank] = i;
+  }
+}
+
+static int grid_for(uint32_t n, int threads) {
+  long b = ((long)n + threads - 1) / threads;
+  if (b > 148L * 32) b = 148L * 32;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
+                          uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, tmp_idx);
+  k_stable_rank<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, tmp_idx, out_idx);
+  return 2;
+}
+
+__global__ void k_gather_keys(const uint32_t* __restrict__ order, const float4* __restrict__ key_raw,
+                              float4* __restrict__ key_sorted, int* __restrict__ kid, uint32_t n) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const uint32_t i = order[p];
+    key_sorted[2 * p] = key_raw[2 * i];
+    key_sorted[2 * p + 1] = key_raw[2 * i + 1];
+    kid[p] = (int)i;
+  }
+}
+
+int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted, int* kid,
+                        uint32_t n, cudaStream_t s) {
+  k_gather_keys<<<grid_for(n, 256), 256, 0, s>>>(order, key_raw, key_sorted, kid, n);
+  return 1;
+}
+
+// ------------------------------------------------------------------------------ query bins
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every 3rd bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_query_bins(const float* __restrict__ q, const float* __restrict__ o, int64_t J, int bits,
+                             uint32_t* __restrict__ bins, uint32_t* __restrict__ count, DevScalars* ds) {
+  const float scale = (float)(1 << bits) * 0.5f;
+  const int maxc = (1 << bits) - 1;
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+    const float x = q[3 * j], y = q[3 * j + 1], z = q[3 * j + 2];
+    bool fin = isfinite(x) && isfinite(y) && isfinite(z);
+    if (o) fin = fin && isfinite(o[j]);
+    bad |= !fin;
+    const int ix = (int)fminf(fmaxf(floorf((x + 1.0f) * scale), 0.0f), (float)maxc);
+    const int iy = (int)fminf(fmaxf(floorf((y + 1.0f) * scale), 0.0f), (float)maxc);
+    const int iz = (int)fminf(fmaxf(floorf((z + 1.0f) * scale), 0.0f), (float)maxc);
+    const uint32_t b = spread3(ix) | (spread3(iy) << 1) | (spread3(iz) << 2);
+    bins[j] = b;
+    atomicAdd(&count[b], 1u);
+  }
+  if (__any_sync(~0u, bad) && (threadIdx.x & 31) == 0) atomicOr(&ds->nonfinite, 1u);
+}
+
+int launch_query_bins(const float* q, const float* o, int64_t J, int bits, uint32_t* bins, uint32_t* count,
+                       DevScalars* ds, cudaStream_t s) {
+  if (J == 0) return 0;
+  k_query_bins<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(q, o, J, bits, bins, count, ds);
+  return 1;
+}
+
+__global__ void k_gather_queries(const uint32_t* __restrict__ order, const float* __restrict__ q,
+                                 const float* __restrict__ o, int64_t J, float4* __restrict__ qs,
+                                 int* __restrict__ perm) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < J; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = order[p];
+    qs[p] = make_float4(q[3 * (size_t)j], q[3 * (size_t)j + 1], q[3 * (size_t)j + 2], o ? o[j] : 0.0f);
+    perm[p] = (int)j;
+  }
+}
+
+int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J, float4* qs,
+                           int* perm, cudaStream_t s) {
+  if (J == 0) return 0;
+  k_gather_queries<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(order, q, o, J, qs, perm);
+  return 1;
+}
+
+// ------------------------------------------------------------------------------ misc
+__global__ void k_fill_zero(float* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.0f;
+}
+
+int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_fill_zero<<<grid_for((uint32_t)n, 256), 256, 0, s>>>(p, n);
+  return 1;
+}
+
+// Fixed-order sum of per-item loss partials (deterministic).
+__global__ void k_sum_partials(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
+  __shared__ double s[1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)part[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = (float)s[0];
+}
+
+int launch_sum_partials(const float* part, int64_t n, float* out, cudaStream_t s) {
+  k_sum_partials<<<1, 1024, 0, s>>>(part, n, out);
+  return 1;
+}
+
+}  // namespace ef

@@ -1,0 +1,268 @@
+"""Thin ctypes binding of libefunc (include/efunc.h). Argument marshalling only: every step of
+the hot path runs in the library's sm_100a kernels. torch supplies device memory and streams.
+
+Loading fails loudly if the shared library is missing — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libefunc.so")
+
+NCH = 13
+OK, EINVAL, ESTATE, ENONFINITE, ECUDA, ENOMEM = range(6)
+LOSS_NONE, LOSS_MSE, LOSS_MSE_EIKONAL = 0, 1, 2
+# default decay mask (reading R-10 / SPEC D15): polynomial coefficients c, g of both banks
+DEFAULT_DECAY_MASK = (1 << 1) | (0b111 << 2) | (1 << 9) | (0b111 << 10)
+
+EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", "efunc_adamw_step",
+            "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
+            "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
+            "efunc_get_stats", "efunc_check", "efunc_last_error", "efunc_abi_version"]
+
+
+class Config(C.Structure):
+    _fields_ = [("R", C.c_int32), ("degree", C.c_int32), ("variant", C.c_int32), ("cutoff_T", C.c_float),
+                ("deterministic", C.c_int32), ("device", C.c_int32), ("sync_checks", C.c_int32),
+                ("reserved", C.c_int32 * 5)]
+
+
+class Loss(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("eikonal_lambda", C.c_float), ("J_global", C.c_int64)]
+
+
+class AdamWParams(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float), ("decay_mask", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("J", C.c_int64), ("items", C.c_int64), ("candidate_pairs", C.c_double),
+                ("kept_pairs", C.c_double), ("beta_min", C.c_float), ("nonfinite", C.c_int32),
+                ("overflow_items", C.c_int32), ("kept_pairs_offset", C.c_double), ("launches", C.c_int64)]
+
+
+class EfuncError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"efunc status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libefunc.so (in-tree build). Raises if it is missing: no fallback path exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libefunc.so not built ({path}); run __graft_entry__.build() or "
+                          f"python -m paper_2505_21319_b200.build")
+    lib = C.CDLL(path)
+    P, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+    sig = {
+        "efunc_create": [C.POINTER(Config), P, C.POINTER(P)],
+        "efunc_destroy": [P],
+        "efunc_forward": [P, P, P, i64, C.POINTER(Loss), P, P, P, P],
+        "efunc_backward": [P, P, P, P, P],
+        "efunc_adamw_step": [P, P, C.POINTER(AdamWParams), P],
+        "efunc_eval_grad": [P, P, i64, P, P, P],
+        "efunc_fit_step": [P, P, P, i64, C.POINTER(Loss), C.POINTER(AdamWParams), P, P, i32, P],
+        "efunc_mean_shift_init": [P, P, i64, f32, P],
+        "efunc_get_params": [P, P, i32, P],
+        "efunc_set_params": [P, P, i32, P],
+        "efunc_get_adam_state": [P, P, P, C.POINTER(i64)],
+        "efunc_set_adam_state": [P, P, P, i64],
+        "efunc_set_counting": [P, i32],
+        "efunc_get_stats": [P, C.POINTER(Stats), P],
+        "efunc_check": [P, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib.efunc_last_error.argtypes = [P]
+    lib.efunc_last_error.restype = C.c_char_p
+    lib.efunc_abi_version.argtypes = []
+    lib.efunc_abi_version.restype = C.c_int32
+    _lib = lib
+    return lib
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _check_dev(t, name, numel, device):
+    import torch
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float32 torch tensor")
+    if t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name} must live on cuda:{device}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+
+
+@dataclass
+class AdamW:
+    lr: float = 6e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 1e-2
+    decay_mask: int = DEFAULT_DECAY_MASK
+
+    def c(self) -> AdamWParams:
+        return AdamWParams(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.decay_mask)
+
+
+class EFunc:
+    """One efunc grid (O^{+Delta}, degree 1, R^3 x 13) on one CUDA device."""
+
+    def __init__(self, R: int, theta=None, cutoff_T: float = 20.0, device: int = 0,
+                 deterministic: bool = False, sync_checks: bool = False):
+        import torch
+        self.lib = load_library()
+        self.R = int(R)
+        self.device = int(device)
+        self.n_params = self.R ** 3 * NCH
+        cfg = Config(self.R, 1, 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks))
+        th = None
+        if theta is not None:
+            if isinstance(theta, torch.Tensor):
+                theta = theta.detach().cpu().numpy()
+            th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
+            if th.size != self.n_params:
+                raise ValueError("theta must have R^3*13 elements")
+        h = C.c_void_p()
+        st = self.lib.efunc_create(C.byref(cfg), None if th is None else th.ctypes.data, C.byref(h))
+        if st != OK:
+            raise EfuncError(st, self.lib.efunc_last_error(None).decode())
+        self.h = h
+        self._torch = torch
+
+    # ---------------------------------------------------------------- helpers
+    def _stream(self):
+        return self._torch.cuda.current_stream(self.device).cuda_stream
+
+    def _ok(self, st):
+        if st != OK:
+            raise EfuncError(st, self.lib.efunc_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.efunc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _empty(self, *shape):
+        return self._torch.empty(*shape, dtype=self._torch.float32, device=f"cuda:{self.device}")
+
+    # ---------------------------------------------------------------- API
+    def forward(self, q, o=None, loss: int = LOSS_NONE, eikonal_lambda: float = 0.1, J_global: int = 0,
+                want_O: bool = True, want_G: bool = False, want_loss: bool = True):
+        """Returns (O, G, loss) — tensors or None."""
+        J = q.shape[0] if q.dim() == 2 else q.numel() // 3
+        _check_dev(q, "q", 3 * J, self.device)
+        _check_dev(o, "o", J, self.device)
+        O = self._empty(J) if want_O else None
+        G = self._empty(J, 3) if want_G else None
+        L = self._empty(1) if (want_loss and loss != LOSS_NONE) else None
+        lc = Loss(loss, eikonal_lambda, J_global)
+        self._ok(self.lib.efunc_forward(self.h, _ptr(q), _ptr(o), J, C.byref(lc), _ptr(O), _ptr(G), _ptr(L),
+                                        self._stream()))
+        return O, G, L
+
+    def backward(self, dL_dO=None, dL_dG=None, grad=None):
+        if grad is None:
+            grad = self._torch.zeros(self.R ** 3, NCH, dtype=self._torch.float32, device=f"cuda:{self.device}")
+        _check_dev(grad, "grad", self.n_params, self.device)
+        _check_dev(dL_dO, "dL_dO", None, self.device)
+        _check_dev(dL_dG, "dL_dG", None, self.device)
+        self._ok(self.lib.efunc_backward(self.h, _ptr(dL_dO), _ptr(dL_dG), _ptr(grad), self._stream()))
+        return grad
+
+    def adamw_step(self, grad, hp: AdamW | None = None):
+        hp = hp or AdamW()
+        _check_dev(grad, "grad", self.n_params, self.device)
+        p = hp.c()
+        self._ok(self.lib.efunc_adamw_step(self.h, _ptr(grad), C.byref(p), self._stream()))
+
+    def eval_grad(self, q, want_O=True, want_G=True):
+        J = q.numel() // 3
+        _check_dev(q, "q", 3 * J, self.device)
+        O = self._empty(J) if want_O else None
+        G = self._empty(J, 3) if want_G else None
+        self._ok(self.lib.efunc_eval_grad(self.h, _ptr(q), J, _ptr(O), _ptr(G), self._stream()))
+        return O, G
+
+    def fit_step(self, q, o, hp: AdamW | None = None, loss: int = LOSS_MSE, eikonal_lambda: float = 0.1,
+                 J_global: int = 0, grad_ws=None, loss_out=None):
+        """forward + loss + backward + AdamW. q/o either CUDA tensors (async, loss_out a device
+        tensor) or pinned CPU tensors (host_io: copies inside the call; returns the loss float)."""
+        hp = hp or AdamW()
+        J = q.numel() // 3
+        lc = Loss(loss, eikonal_lambda, J_global)
+        p = hp.c()
+        host = q.device.type == "cpu"
+        if host:
+            lo = C.c_float(0.0)
+            self._ok(self.lib.efunc_fit_step(self.h, q.data_ptr(), o.data_ptr(), J, C.byref(lc), C.byref(p),
+                                             _ptr(grad_ws), C.addressof(lo), 1, self._stream()))
+            return float(lo.value)
+        self._ok(self.lib.efunc_fit_step(self.h, _ptr(q), _ptr(o), J, C.byref(lc), C.byref(p), _ptr(grad_ws),
+                                         _ptr(loss_out), 0, self._stream()))
+        return loss_out
+
+    def mean_shift_init(self, surf, bandwidth: float = 100.0):
+        N = surf.numel() // 3
+        _check_dev(surf, "surf", 3 * N, self.device)
+        self._ok(self.lib.efunc_mean_shift_init(self.h, _ptr(surf), N, float(bandwidth), self._stream()))
+
+    def get_params(self) -> np.ndarray:
+        out = np.empty((self.R ** 3, NCH), dtype=np.float32)
+        self._ok(self.lib.efunc_get_params(self.h, out.ctypes.data, 0, self._stream()))
+        return out
+
+    def set_params(self, theta):
+        th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
+        if th.size != self.n_params:
+            raise ValueError("theta must have R^3*13 elements")
+        self._ok(self.lib.efunc_set_params(self.h, th.ctypes.data, 0, self._stream()))
+
+    def get_adam_state(self):
+        m = np.empty((self.R ** 3, NCH), np.float32)
+        v = np.empty_like(m)
+        step = C.c_int64(0)
+        self._ok(self.lib.efunc_get_adam_state(self.h, m.ctypes.data, v.ctypes.data, C.byref(step)))
+        return m, v, int(step.value)
+
+    def set_adam_state(self, m=None, v=None, step: int = 0):
+        mm = None if m is None else np.ascontiguousarray(np.asarray(m, np.float32).reshape(-1))
+        vv = None if v is None else np.ascontiguousarray(np.asarray(v, np.float32).reshape(-1))
+        self._ok(self.lib.efunc_set_adam_state(self.h, None if mm is None else mm.ctypes.data,
+                                               None if vv is None else vv.ctypes.data, int(step)))
+
+    def set_counting(self, on: bool):
+        self._ok(self.lib.efunc_set_counting(self.h, int(on)))
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._ok(self.lib.efunc_get_stats(self.h, C.byref(s), self._stream()))
+        return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+    def check(self):
+        self._ok(self.lib.efunc_check(self.h, self._stream()))

@@ -1,0 +1,78 @@
+"""CPU-side checks of the C ABI: the library builds/loads and exports every symbol that
+include/efunc.h declares; struct layouts of the binding match the header. No GPU calls."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "efunc.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"EFUNC_API\s+[\w\s\*]+?\b(efunc_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2505_21319_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_north_star_entry_points():
+    syms = declared_symbols()
+    for name in ["efunc_create", "efunc_forward", "efunc_backward", "efunc_adamw_step", "efunc_eval_grad"]:
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib._name], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (efunc_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+
+
+def test_binding_covers_every_symbol():
+    from paper_2505_21319_b200 import efunc
+    assert sorted(efunc.EXPORTED) == declared_symbols()
+
+
+def test_abi_version_callable_without_gpu(lib):
+    lib.efunc_abi_version.restype = ctypes.c_int32
+    assert lib.efunc_abi_version() == 1
+
+
+def test_struct_sizes_match_header():
+    """Compile a tiny C program against the header and compare sizeof with the ctypes mirrors."""
+    from paper_2505_21319_b200 import efunc
+    src = r'''
+    #include <stdio.h>
+    #include "efunc.h"
+    int main(){printf("%zu %zu %zu %zu\n", sizeof(efunc_config), sizeof(efunc_loss),
+                       sizeof(efunc_adamw), sizeof(efunc_stats)); return 0;}
+    '''
+    tmp = "/tmp/efunc_sizeof"
+    with open(tmp + ".c", "w") as fh:
+        fh.write(src)
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), tmp + ".c", "-o", tmp], check=True)
+    sizes = [int(x) for x in subprocess.run([tmp], capture_output=True, text=True).stdout.split()]
+    assert sizes == [ctypes.sizeof(efunc.Config), ctypes.sizeof(efunc.Loss),
+                     ctypes.sizeof(efunc.AdamWParams), ctypes.sizeof(efunc.Stats)]
+
+
+def test_create_fails_cleanly_without_gpu(lib):
+    """Without a device the ABI returns an error code (never crashes / throws)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2505_21319_b200 import efunc
+    L = efunc.load_library()
+    cfg = efunc.Config(8, 1, 0, 20.0, 0, 0, 0)
+    h = ctypes.c_void_p()
+    st = L.efunc_create(ctypes.byref(cfg), None, ctypes.byref(h))
+    assert st in (efunc.ECUDA, efunc.EINVAL)
+    assert L.efunc_last_error(None)

@@ -1,0 +1,304 @@
+"""GPU parity: libefunc (sm_100a, through the C ABI) vs the float64 CPU oracle.
+
+Tolerances (north_star, read normwise per DESIGN.md reading R-T):
+  values O, G        max|gpu - ref| / max|ref| <= 1e-5   (per component for G)
+  parameter grads    per channel max|gpu - ref| / max|ref| <= 1e-4
+  AdamW              rel 1e-6 (fp32 arithmetic vs float64)
+The GPU evaluates the certified cutoff T = 20 (reading R-1); the oracle is the global sum.
+"""
+import numpy as np
+import pytest
+
+import oracle as orc
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2505_21319_b200 as ef  # noqa: E402
+
+TOL_VAL = 1e-5
+TOL_GRAD = 1e-4
+
+
+def nw(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def c1_case(seed=1, J=4096, R=8):
+    sph = synth.Sphere(0.5)
+    th = synth.fitted_like_theta(R, sph, seed)
+    q, o = synth.sample_batch(sph, J, seed=seed + 100)
+    return th, q, o
+
+
+def check_grads(g, ref, tol=TOL_GRAD):
+    for ch in range(13):
+        e = nw(g[:, ch], ref[:, ch])
+        assert e <= tol, (ch, e)
+
+
+# ----------------------------------------------------------------------------- forward
+@pytest.mark.parametrize("T", [20.0, float("inf")])
+def test_forward_parity_c1(T):
+    th, q, o = c1_case()
+    m = ef.EFunc(8, th, cutoff_T=T)
+    O, G, L = m.forward(dev(q), dev(o), loss=ef.LOSS_MSE, want_G=True)
+    torch.cuda.synchronize()
+    ref = orc.forward(th, 8, q)
+    assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
+    for a in range(3):
+        assert nw(G.cpu().numpy()[:, a], ref.G[:, a]) <= TOL_VAL
+    Lref, _ = orc.mse_loss(ref.O, o)
+    assert abs(float(L.item()) - Lref) / Lref <= 1e-5
+
+
+def test_partition_of_unity_on_gpu():
+    """Shared linear polynomial is reproduced exactly for any truncated key set."""
+    R = 16
+    A, B = 0.3, np.array([0.7, -1.2, 0.4])
+    th = synth.random_theta(R, 3, log_scale_mean=7.0, log_scale_std=0.3, offset_std=0.03).astype(np.float64)
+    k = orc.node_positions(R)
+    th[:, 1] = A + k @ B; th[:, 2:5] = B
+    th[:, 9] = A + (k + th[:, 5:8]) @ B; th[:, 10:13] = B
+    th = th.astype(np.float32)
+    q = synth.rng(4).uniform(-1, 1, size=(50000, 3)).astype(np.float32)
+    m = ef.EFunc(R, th)
+    O, G, _ = m.forward(dev(q), want_G=True)
+    exact = A + q.astype(np.float64) @ B
+    assert nw(O.cpu().numpy(), exact) <= 2e-6
+    assert np.abs(G.cpu().numpy() - B[None, :]).max() <= 2e-5
+
+
+def test_eval_grad_matches_forward_and_oracle():
+    th, q, o = c1_case(seed=5, J=1000)
+    m = ef.EFunc(8, th)
+    O, G = m.eval_grad(dev(q))
+    ref = orc.forward(th, 8, q)
+    assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
+    assert nw(G.cpu().numpy(), ref.G) <= TOL_VAL
+
+
+# ----------------------------------------------------------------------------- backward
+@pytest.mark.parametrize("T", [20.0, float("inf")])
+def test_backward_mse_parity_c1(T):
+    th, q, o = c1_case(seed=7)
+    m = ef.EFunc(8, th, cutoff_T=T)
+    m.forward(dev(q), dev(o), loss=ef.LOSS_MSE)
+    g = m.backward().cpu().numpy()
+    f = orc.forward(th, 8, q)
+    _, r = orc.mse_loss(f.O, o)
+    check_grads(g, orc.backward(th, 8, q, f, r))
+
+
+def test_backward_explicit_upstream_parity():
+    th, q, o = c1_case(seed=9, J=2000)
+    r = synth.rng(10).normal(size=2000).astype(np.float32)
+    m = ef.EFunc(8, th)
+    m.forward(dev(q))
+    g = m.backward(dL_dO=dev(r)).cpu().numpy()
+    f = orc.forward(th, 8, q)
+    check_grads(g, orc.backward(th, 8, q, f, r.astype(np.float64)))
+
+
+def test_backward_eikonal_parity():
+    th, q, o = c1_case(seed=11, J=2048)
+    m = ef.EFunc(8, th)
+    O, G, L = m.forward(dev(q), dev(o), loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1, want_G=True)
+    g = m.backward().cpu().numpy()
+    f = orc.forward(th, 8, q)
+    Lm, r = orc.mse_loss(f.O, o)
+    Le, h = orc.eikonal_loss(f.G, 0.1)
+    assert abs(float(L.item()) - (Lm + Le)) / (Lm + Le) <= 1e-5
+    check_grads(g, orc.backward(th, 8, q, f, r, h))
+
+
+def test_backward_without_forward_is_state_error():
+    th, q, o = c1_case(J=10)
+    m = ef.EFunc(8, th)
+    with pytest.raises(ef.EfuncError) as e:
+        m.backward(dL_dO=dev(np.ones(10)))
+    assert e.value.status == 2
+
+
+# ----------------------------------------------------------------------------- AdamW / fit
+def test_adamw_parity():
+    R = 8
+    th = synth.random_theta(R, 12)
+    rs = synth.rng(13)
+    m = ef.EFunc(R, th)
+    hp = ef.AdamW(lr=1e-2, weight_decay=0.05)
+    ohp = orc.AdamW(lr=1e-2, weight_decay=0.05)
+    cur = th.astype(np.float64); mm = np.zeros_like(cur); vv = np.zeros_like(cur)
+    for step in range(1, 4):
+        g = (rs.normal(size=th.shape) * 10.0 ** rs.integers(-5, 0, size=th.shape)).astype(np.float32)
+        m.adamw_step(dev(g), hp)
+        cur, mm, vv = orc.adamw_step(cur, g, mm, vv, step, ohp)
+        got = m.get_params()
+        np.testing.assert_allclose(got, cur, rtol=2e-6, atol=1e-7)
+    gm, gv, st = m.get_adam_state()
+    assert st == 3
+    np.testing.assert_allclose(gm, mm, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose(gv, vv, rtol=1e-5, atol=1e-16)
+
+
+def test_fit_c1_ten_steps_resynced_and_free_running():
+    """C1: 8^3 grid, 4096 sphere points, 10 AdamW steps. Step-by-step with re-sync (reading R-A)
+    at 1e-4 on grads, plus a free-running loss trajectory."""
+    R = 8
+    sph = synth.Sphere(0.5)
+    th0 = synth.init_theta(R, 21)
+    s = synth.surface_points(sph, 4096, seed=22)
+    th0[:, 5:8] = orc.mean_shift_offsets(R, s).astype(np.float32)
+    hp = ef.AdamW(); ohp = orc.AdamW()
+    m = ef.EFunc(R, th0)
+    cur = th0.astype(np.float64); mm = np.zeros_like(cur); vv = np.zeros_like(cur)
+    free = ef.EFunc(R, th0)
+    losses_gpu, losses_ref = [], []
+    for step in range(1, 11):
+        q, o = synth.sample_batch(sph, 4096, seed=1000 + step)
+        # re-synced step: both sides start from the oracle's theta_t and moments
+        m.set_params(cur.astype(np.float32))
+        m.set_adam_state(mm.astype(np.float32), vv.astype(np.float32), step - 1)
+        _, _, L = m.forward(dev(q), dev(o), loss=ef.LOSS_MSE)
+        g = m.backward().cpu().numpy()
+        f = orc.forward(cur, R, q)
+        Lr, r = orc.mse_loss(f.O, o)
+        gref = orc.backward(cur, R, q, f, r)
+        check_grads(g, gref)
+        assert abs(float(L.item()) - Lr) / Lr <= 1e-5
+        cur, mm, vv = orc.adamw_step(cur, gref, mm, vv, step, ohp)
+        # free-running GPU fit
+        losses_gpu.append(free.fit_step(torch.as_tensor(q).pin_memory(), torch.as_tensor(o).pin_memory(), hp))
+        losses_ref.append(Lr)
+    # free-running loss within 1e-3 relative (AdamW amplifies sign noise of near-zero grads)
+    assert np.allclose(losses_gpu, losses_ref, rtol=1e-3)
+    assert losses_gpu[-1] < losses_gpu[0]
+
+
+# ----------------------------------------------------------------------------- full size (C2)
+def test_c2_full_size_sampled_parity():
+    """C2 geometry: 32^3 x 13, 2^20 torus points in the bench's launch configuration; outputs
+    checked at sampled queries, gradients via a sampled upstream (linearity)."""
+    R, J = 32, 1 << 20
+    tor = synth.Torus()
+    s = synth.surface_points(tor, 16384, seed=31)
+    th = synth.init_theta(R, 32)
+    q, o = synth.sample_batch(tor, J, seed=33)
+    m = ef.EFunc(R, th)
+    m.mean_shift_init(dev(s))
+    th_gpu = m.get_params()
+    # mean shift parity
+    dref = orc.mean_shift_offsets(R, s.astype(np.float64))
+    assert np.abs(th_gpu[:, 5:8] - dref).max() <= 1e-5
+    qd, od = dev(q), dev(o)
+    O, G, L = m.forward(qd, od, loss=ef.LOSS_MSE, want_G=True)
+    idx = synth.rng(34).choice(J, size=1024, replace=False)
+    ref = orc.forward(th_gpu, R, q[idx])
+    assert nw(O.cpu().numpy()[idx], ref.O) <= TOL_VAL
+    for a in range(3):
+        assert nw(G.cpu().numpy()[idx, a], ref.G[:, a]) <= TOL_VAL
+    # sampled upstream over the full batch
+    sub = synth.rng(35).choice(J, size=512, replace=False)
+    r = np.zeros(J, np.float32)
+    r[sub] = synth.rng(36).normal(size=512).astype(np.float32)
+    g = m.backward(dL_dO=dev(r)).cpu().numpy()
+    fs = orc.forward(th_gpu, R, q[sub])
+    check_grads(g, orc.backward(th_gpu, R, q[sub], fs, r[sub].astype(np.float64)))
+
+
+def test_c2_pou_full_size():
+    R, J = 32, 1 << 20
+    A, B = -0.2, np.array([0.3, 0.1, -0.5])
+    th = synth.fitted_like_theta(R, synth.Torus(), 41).astype(np.float64)
+    k = orc.node_positions(R)
+    th[:, 1] = A + k @ B; th[:, 2:5] = B
+    th[:, 9] = A + (k + th[:, 5:8]) @ B; th[:, 10:13] = B
+    q, o = synth.sample_batch(synth.Torus(), J, seed=42)
+    m = ef.EFunc(R, th.astype(np.float32))
+    O, G, _ = m.forward(dev(q), want_G=True)
+    assert nw(O.cpu().numpy(), A + q.astype(np.float64) @ B) <= 2e-6
+    assert np.abs(G.cpu().numpy() - B[None]).max() <= 5e-5
+    # sum_i dL/dc_i = sum_j r_j (softmax sums to one)
+    r = synth.rng(43).normal(size=J).astype(np.float32) / J
+    g = m.backward(dL_dO=dev(r)).cpu().numpy().astype(np.float64)
+    assert abs(g[:, 1].sum() + g[:, 9].sum() - r.astype(np.float64).sum()) <= 1e-4 * np.abs(r).sum()
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_empty_single_and_ragged():
+    th, q, o = c1_case(seed=51, J=259)
+    m = ef.EFunc(8, th)
+    O, G, L = m.forward(dev(q[:0]), dev(o[:0]), loss=ef.LOSS_MSE, want_G=True)
+    assert O.numel() == 0 and float(L.item()) == 0.0
+    g = m.backward()
+    assert float(g.abs().sum()) == 0.0
+    for J in (1, 127, 128, 129, 259):
+        O, G, _ = m.forward(dev(q[:J]), want_G=True)
+        ref = orc.forward(th, 8, q[:J])
+        assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
+
+
+def test_out_of_domain_queries_and_small_grid():
+    R = 2
+    th = synth.random_theta(R, 61, log_scale_mean=1.0)
+    q = synth.rng(62).uniform(-3, 3, size=(777, 3)).astype(np.float32)
+    m = ef.EFunc(R, th)
+    O, G, _ = m.forward(dev(q), want_G=True)
+    ref = orc.forward(th, R, q)
+    assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
+    assert nw(G.cpu().numpy(), ref.G) <= TOL_VAL
+
+
+def test_large_beta_spread_takes_exact_shift_path():
+    """log-scales far from the init: the corner shift bound may overflow; the slow path must
+    keep results exact."""
+    R = 8
+    th = synth.random_theta(R, 71, log_scale_mean=7.5, log_scale_std=1.5)
+    q = synth.rng(72).uniform(-1, 1, size=(3000, 3)).astype(np.float32)
+    m = ef.EFunc(R, th)
+    O, G, _ = m.forward(dev(q), want_G=True)
+    ref = orc.forward(th, R, q)
+    assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
+    assert nw(G.cpu().numpy(), ref.G) <= 1e-4
+
+
+def test_nonfinite_query_reported():
+    th, q, o = c1_case(J=100)
+    q[17, 1] = np.nan
+    m = ef.EFunc(8, th, sync_checks=True)
+    with pytest.raises(ef.EfuncError) as e:
+        m.forward(dev(q))
+    assert e.value.status == 3
+    m2 = ef.EFunc(8, th)
+    m2.forward(dev(q))
+    with pytest.raises(ef.EfuncError):
+        m2.check()
+    m2.check()  # flag cleared
+
+
+def test_forward_bitwise_deterministic():
+    th, q, o = c1_case(seed=81, J=50000)
+    m = ef.EFunc(8, th)
+    a = m.forward(dev(q), want_G=True)
+    b = m.forward(dev(q), want_G=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_kept_pair_counter_matches_oracle():
+    th, q, o = c1_case(seed=91, J=512)
+    m = ef.EFunc(8, th)
+    m.set_counting(True)
+    m.forward(dev(q))
+    st = m.stats()
+    ref = orc.forward(th, 8, q, cutoff_T=20.0)
+    assert abs(st["kept_pairs"] - ref.kept.sum()) <= 0.01 * ref.kept.sum()
+    assert st["candidate_pairs"] >= st["kept_pairs"]
