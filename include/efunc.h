@@ -88,7 +88,7 @@ typedef struct {
 } efunc_loss;
 
 typedef struct {
-  float lr, beta1, beta2, eps, weight_decay; /* PAPER.md:L698 lr=6e-4; rest reading R-10 */
+  double lr, beta1, beta2, eps, weight_decay; /* PAPER.md:L698 lr=6e-4; rest reading R-10 */
   uint32_t decay_mask;    /* bit c set = channel c is weight-decayed (default: c,g channels) */
 } efunc_adamw;
 

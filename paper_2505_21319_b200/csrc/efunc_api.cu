@@ -110,6 +110,14 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s) {
   return EFUNC_OK;
 }
 
+// Morton bits per axis of the coarse cells that work items may not straddle (edge ~4h).
+int coarse_bits(const efunc_t* h, int bits) {
+  int c = (int)std::lround(std::log2(std::fmax((h->R - 1) / 4.0, 1.0)));
+  if (c < 0) c = 0;
+  if (c > bits) c = bits;
+  return c;
+}
+
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
   const int bits = query_bits(J);
   const uint32_t nbins = 1u << (3 * bits);
@@ -123,10 +131,28 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
     h->nbins_cap = nbins + 1;
     RET(ensure_scan_tmp(h, nbins + 1));
   }
+  const int cb = coarse_bits(h, bits);
+  const uint32_t n_coarse = 1u << (3 * cb);
+  if (n_coarse + 1 > h->coarse_cap) {
+    dfree(h->item_cnt);
+    dfree(h->item_off);
+    CK(dalloc(&h->item_cnt, n_coarse + 1));
+    CK(dalloc(&h->item_off, n_coarse + 1));
+    h->coarse_cap = n_coarse + 1;
+  }
+  const int64_t bound = (J + QITEM - 1) / QITEM + n_coarse;
+  if (bound > h->items_cap) {
+    dfree(h->boxes); dfree(h->loss_part); dfree(h->items); dfree(h->lists); dfree(h->list_n);
+    CK(dalloc(&h->lists, (size_t)bound * LIST_CAP));
+    CK(dalloc(&h->list_n, bound));
+    CK(dalloc(&h->boxes, bound));
+    CK(dalloc(&h->loss_part, bound));
+    CK(dalloc(&h->items, bound));
+    h->items_cap = bound;
+  }
   if (J > h->J_cap) {
     dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
-    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->boxes); dfree(h->loss_part);
-    const int64_t items = (J + QITEM - 1) / QITEM;
+    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
     CK(dalloc(&h->q_bin, J));
     CK(dalloc(&h->q_tmp, J));
     CK(dalloc(&h->q_order, J));
@@ -136,8 +162,6 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
     CK(dalloc(&h->gs, J));
     CK(dalloc(&h->us, J));
     CK(dalloc(&h->hs, J));
-    CK(dalloc(&h->boxes, items));
-    CK(dalloc(&h->loss_part, items));
     h->J_cap = J;
   }
   return EFUNC_OK;
@@ -151,6 +175,7 @@ void free_all(efunc_t* h) {
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
   dfree(h->boxes); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
+  dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->lists); dfree(h->list_n);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -182,12 +207,24 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
   h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
   h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
-  const int64_t items = (J + QITEM - 1) / QITEM;
+  // work items: balanced runs of <= QITEM sorted queries inside each coarse Morton cell
+  const int cb = coarse_bits(h, bits);
+  const uint32_t n_coarse = 1u << (3 * cb);
+  const int shift = 3 * (bits - cb);
+  h->launches += launch_items_count(h->bin_start, shift, n_coarse, h->item_cnt, s);
+  h->launches += launch_scan_u32(h->item_cnt, h->item_off, n_coarse + 1, h->scan_tmp, s);
+  h->launches += launch_items_write(h->bin_start, shift, n_coarse, h->item_off, h->items, s);
+  const int64_t items = (J + QITEM - 1) / QITEM + n_coarse;  // launch bound; kernels read the count
+  const uint32_t* n_items = h->item_off + n_coarse;
+  h->fwd_items_bound = items;
+  h->fwd_n_coarse = n_coarse;
   FwdArgs a;
   a.kv = keys_view(h);
   a.qs = h->qs;
   a.perm = h->perm;
   a.J = J;
+  a.items = h->items;
+  a.n_items = n_items;
   a.T_l = cutoff_log2(h->cfg);
   a.loss_kind = kind;
   const int64_t Jg = (loss && loss->J_global > 0) ? loss->J_global : J;
@@ -203,8 +240,11 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   a.loss_part = h->loss_part;
   a.ds = h->ds;
   a.count_kept = h->count_kept;
+  a.lists = h->lists;
+  a.list_n = h->list_n;
+  a.list_cap = LIST_CAP;
   h->launches += launch_forward(a, want_g, items, s);
-  if (kind != EFUNC_LOSS_NONE && loss_out) launch_sum_partials(h->loss_part, items, loss_out, s);
+  if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, loss_out, s);
   else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   CK(cudaGetLastError());
   if (h->cfg.sync_checks) {
@@ -236,6 +276,12 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.qs = h->qs;
   b.perm = h->perm;
   b.J = h->fwd_J;
+  b.items = h->items;
+  b.n_items = h->item_off + h->fwd_n_coarse;
+  b.T_l = cutoff_log2(h->cfg);
+  b.lists = h->lists;
+  b.list_n = h->list_n;
+  b.list_cap = LIST_CAP;
   b.rec = h->rec;
   b.gs = h->gs;
   b.us = h->us;
@@ -245,7 +291,7 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.boxes = h->boxes;
   b.grad = grad;
   b.eik = eik;
-  h->launches += launch_backward(b, (h->fwd_J + QITEM - 1) / QITEM, s);
+  h->launches += launch_backward(b, h->fwd_items_bound, s);
   CK(cudaGetLastError());
   return EFUNC_OK;
 }
@@ -253,14 +299,16 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
 efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cudaStream_t s) {
   if (!grad || !hp) return fail(h, EFUNC_EINVAL, "NULL argument");
   h->step += 1;
+  // hyper-parameters are doubles (like torch's python floats); derived constants are rounded
+  // to fp32 once, here
   const double b1 = hp->beta1, b2 = hp->beta2;
   const double bc1 = 1.0 - std::pow(b1, (double)h->step);
   const double bc2 = 1.0 - std::pow(b2, (double)h->step);
-  const float step_size = (float)((double)hp->lr / bc1);
+  const float step_size = (float)(hp->lr / bc1);
   const float sqrt_bc2 = (float)std::sqrt(bc2);
-  const float decay = (float)(1.0 - (double)hp->lr * (double)hp->weight_decay);
-  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, decay, hp->beta1, hp->beta2, hp->eps,
-               hp->decay_mask, step_size, sqrt_bc2, s);
+  const float decay = (float)(1.0 - hp->lr * hp->weight_decay);
+  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, decay, (float)(1.0 - b1),
+                              (float)b2, (float)(1.0 - b2), (float)hp->eps, hp->decay_mask, step_size, sqrt_bc2, s);
   CK(cudaGetLastError());
   return rebuild_keys(h, s);
 }
@@ -479,7 +527,9 @@ efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
   DevScalars d;
   CK(cudaMemcpy(&d, h->ds, sizeof(d), cudaMemcpyDeviceToHost));
   out->J = h->fwd_J;
-  out->items = (h->fwd_J + QITEM - 1) / QITEM;
+  uint32_t ni = 0;
+  if (h->fwd_J > 0) CK(cudaMemcpy(&ni, h->item_off + h->fwd_n_coarse, sizeof(ni), cudaMemcpyDeviceToHost));
+  out->items = ni;
   out->candidate_pairs = (double)d.cand_pairs;
   out->kept_pairs = (double)d.kept_pairs;
   out->beta_min = d.bl_min / EF_LOG2E;

@@ -28,6 +28,7 @@ constexpr int QITEM = 128;        // queries per work item == forward/backward C
 constexpr int NTHREADS = 128;
 constexpr int LCAP = 512;         // candidate keys staged in shared memory per chunk
 constexpr int MAX_QBITS = 7;      // Morton bits per axis for query binning
+constexpr uint32_t LIST_CAP = 2048;  // per-item candidate list handed from forward to backward
 
 struct KeysView {
   const float4* ks;        // sorted records, 2 float4 per key (a at 2k, b at 2k+1)
@@ -60,6 +61,8 @@ struct FwdArgs {
   const float4* qs;       // sorted queries {x,y,z,o}
   const int* perm;        // sorted -> user index
   int64_t J;
+  const int2* items;      // work items {first sorted query, count}
+  const uint32_t* n_items;  // device count (grid is launched with an upper bound)
   float T_l;              // cutoff in log2 units (inf = dense)
   // loss
   int loss_kind;
@@ -76,6 +79,9 @@ struct FwdArgs {
   float* loss_part;       // per item partial loss
   DevScalars* ds;
   int count_kept;
+  uint32_t* lists;        // per item: sorted-key positions of its staged candidates (cap list_cap)
+  uint32_t* list_n;       // per item: list length (> list_cap: the backward re-stages)
+  uint32_t list_cap;
 };
 
 struct BwdArgs {
@@ -83,6 +89,9 @@ struct BwdArgs {
   const float4* qs;
   const int* perm;
   int64_t J;
+  const int2* items;
+  const uint32_t* n_items;
+  float T_l;              // cutoff in log2 units (inf = dense)
   const float4* rec;
   const float4* gs;
   const float4* us;
@@ -92,6 +101,9 @@ struct BwdArgs {
   const ItemBox* boxes;
   float* grad;            // [R^3][13] +=
   int eik;                // 1: add the dL/dG terms
+  const uint32_t* lists;
+  const uint32_t* list_n;
+  uint32_t list_cap;
 };
 
 // ---------------------------------------------------------------- launchers (host)
@@ -109,10 +121,14 @@ int launch_gather_queries(const uint32_t* order, const float* q, const float* o,
                            float4* qs, int* perm, cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
-int launch_sum_partials(const float* part, int64_t n, float* out, cudaStream_t s);
+int launch_sum_partials(const float* part, const uint32_t* n, float* out, cudaStream_t s);
+int launch_items_count(const uint32_t* bin_start, int shift, uint32_t n_coarse, uint32_t* cnt,
+                       cudaStream_t s);
+int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, const uint32_t* off,
+                       int2* items, cudaStream_t s);
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay,
-                  float b1, float b2, float eps, uint32_t mask, float step_size, float sqrt_bc2,
-                  cudaStream_t s);
+                 float omb1, float b2, float omb2, float eps, uint32_t mask, float step_size,
+                 float sqrt_bc2, cudaStream_t s);
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
                        cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
@@ -160,6 +176,15 @@ struct efunc {
   float4* hs = nullptr;
   ef::ItemBox* boxes = nullptr;
   float* loss_part = nullptr;
+  int64_t items_cap = 0;
+  int2* items = nullptr;          // [items bound]
+  uint32_t* lists = nullptr;      // [items bound][LIST_CAP]
+  uint32_t* list_n = nullptr;     // [items bound]
+  uint32_t* item_cnt = nullptr;   // [coarse cells + 1]
+  uint32_t* item_off = nullptr;   // [coarse cells + 1]; item_off[n_coarse] = item count
+  uint32_t coarse_cap = 0;
+  int64_t fwd_items_bound = 0;
+  uint32_t fwd_n_coarse = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;
   float* io_loss = nullptr;

@@ -6,19 +6,20 @@ namespace ef {
 
 // Elementwise over theta [R^3][13]; op order follows torch's single-tensor AdamW:
 //   p *= 1 - lr*wd (masked channels);  m += (1-b1)(g - m);  v = v*b2 + (1-b2) g*g;
-//   p += -step_size * m / (sqrt(v) / sqrt(bc2) + eps),  step_size = lr / bc1  (host, double)
+//   p += -step_size * m / (sqrt(v) / sqrt(bc2) + eps),  step_size = lr / bc1
+// All scalar constants are computed in double on the host and rounded to fp32 once.
 __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
-                        float* __restrict__ v, int64_t n, float decay, float b1, float b2, float eps,
-                        uint32_t mask, float step_size, float sqrt_bc2) {
+                        float* __restrict__ v, int64_t n, float decay, float omb1, float b2, float omb2,
+                        float eps, uint32_t mask, float step_size, float sqrt_bc2) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % EF_NCH);
     float p = theta[i];
     const float g = grad[i];
     if ((mask >> ch) & 1u) p *= decay;
     float mi = m[i];
-    mi = fmaf(1.0f - b1, g - mi, mi);
+    mi = fmaf(omb1, g - mi, mi);
     float vi = v[i];
-    vi = fmaf(1.0f - b2, g * g, vi * b2);
+    vi = fmaf(omb2, g * g, vi * b2);
     const float denom = __fdiv_rn(__fsqrt_rn(vi), sqrt_bc2) + eps;
     p = fmaf(-step_size, __fdiv_rn(mi, denom), p);
     theta[i] = p;
@@ -27,12 +28,13 @@ __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ gra
   }
 }
 
-int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay, float b1,
-                  float b2, float eps, uint32_t mask, float step_size, float sqrt_bc2, cudaStream_t s) {
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay, float omb1,
+                 float b2, float omb2, float eps, uint32_t mask, float step_size, float sqrt_bc2,
+                 cudaStream_t s) {
   long blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  k_adamw<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, decay, b1, b2, eps, mask, step_size,
+  k_adamw<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, decay, omb1, b2, omb2, eps, mask, step_size,
                                             sqrt_bc2);
   return 1;
 }

@@ -274,11 +274,54 @@ int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s) {
   return 1;
 }
 
+// ------------------------------------------------------------------------------ work items
+// Items never straddle a coarse Morton cell (edge ~4h): a fixed-size run of the Morton-sorted
+// stream can jump across the domain at a Morton boundary and then gets a huge box (and a huge
+// candidate list). Inside a coarse cell the queries are split into ceil(n/QITEM) balanced runs.
+__global__ void k_items_count(const uint32_t* __restrict__ bin_start, int shift, uint32_t n_coarse,
+                              uint32_t* __restrict__ cnt) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= n_coarse; c += gridDim.x * blockDim.x) {
+    if (c == n_coarse) {
+      cnt[c] = 0;
+      continue;
+    }
+    const uint32_t n = bin_start[(c + 1) << shift] - bin_start[c << shift];
+    cnt[c] = (n + QITEM - 1) / QITEM;
+  }
+}
+
+__global__ void k_items_write(const uint32_t* __restrict__ bin_start, int shift, uint32_t n_coarse,
+                              const uint32_t* __restrict__ off, int2* __restrict__ items) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_coarse; c += gridDim.x * blockDim.x) {
+    const uint32_t s = bin_start[c << shift];
+    const uint32_t n = bin_start[(c + 1) << shift] - s;
+    const uint32_t m = (n + QITEM - 1) / QITEM;
+    const uint32_t o = off[c];
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint32_t a = (uint32_t)(((uint64_t)i * n) / m), b = (uint32_t)(((uint64_t)(i + 1) * n) / m);
+      items[o + i] = make_int2((int)(s + a), (int)(b - a));
+    }
+  }
+}
+
+int launch_items_count(const uint32_t* bin_start, int shift, uint32_t n_coarse, uint32_t* cnt, cudaStream_t s) {
+  k_items_count<<<grid_for(n_coarse + 1, 256), 256, 0, s>>>(bin_start, shift, n_coarse, cnt);
+  return 1;
+}
+
+int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, const uint32_t* off, int2* items,
+                       cudaStream_t s) {
+  k_items_write<<<grid_for(n_coarse, 128), 128, 0, s>>>(bin_start, shift, n_coarse, off, items);
+  return 1;
+}
+
 // Fixed-order sum of per-item loss partials (deterministic).
-__global__ void k_sum_partials(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
+__global__ void k_sum_partials(const float* __restrict__ part, const uint32_t* __restrict__ np,
+                               float* __restrict__ out) {
   __shared__ double s[1024];
+  const uint32_t n = *np;
   double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)part[i];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)part[i];
   s[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -288,7 +331,7 @@ __global__ void k_sum_partials(const float* __restrict__ part, int64_t n, float*
   if (threadIdx.x == 0) *out = (float)s[0];
 }
 
-int launch_sum_partials(const float* part, int64_t n, float* out, cudaStream_t s) {
+int launch_sum_partials(const float* part, const uint32_t* n, float* out, cudaStream_t s) {
   k_sum_partials<<<1, 1024, 0, s>>>(part, n, out);
   return 1;
 }

@@ -1,21 +1,26 @@
 // k_fwd_bwd.cu — S2/S3 forward (+ loss epilogue) and S4 backward.
 //
-// One CTA = one work item = QITEM consecutive Morton-sorted queries. Both kernels walk the
-// same candidate key set of the item: keys in the lattice cells overlapping the item's AABB
-// grown by rho = sqrt(thr / bl_min), kept iff bl_k * dist^2(k, AABB) <= thr, where
-// thr = max_j mh_j + T_l (log2 units) and mh_j >= m_j is the exponent of the nearest of the
-// 8 lattice-corner grid keys of query j. A skipped pair therefore has a - m_j > cutoff_T
-// (reading R-1). Candidates are staged in shared memory (LCAP per chunk) and
-// broadcast to the lanes:
-//   forward : lanes = queries, loop over staged keys (Alg. 1; the
-//             shift of the paper's "maximum-reduce", L501, is the corner bound mh_j; an
-//             exact-min slow path runs if an item's sums overflow)
-//   backward: lanes = staged keys, loop over the item's queries in shared memory; per key
-//             register accumulators (Alg. 2, PAPER.md:L540-568 restricted to the item), one
-//             red.global.add per gradient channel per (item, key).
+// One CTA = one work item = up to QITEM Morton-consecutive queries inside one coarse cell,
+// split into 4 query groups of 32 (one per warp). Both kernels first stage, chunk by chunk,
+// the item's candidate keys in shared memory: keys of the lattice cells overlapping the
+// item's AABB grown by rho = sqrt(thr / bl_min), kept iff bl_k * dist^2(k, AABB) <= thr.
+// Every skipped pair therefore has a - m_j > cutoff_T (reading R-1):
+//   forward : thr = max_j mh_j + T_l, mh_j >= m_j the exponent of the best key among the 8
+//             lattice corners and the keys of the query's own cell (the shift of the paper's
+//             "maximum-reduce"). Each warp then filters the staged keys
+//             against its own 32-query sub-box and loops over its list with lanes = queries
+//             (Alg. 1). An exact-min slow path runs if sums overflow.
+//   backward: thr_g = max_{j in g} (-lambda_j log2e) + T_l per query group g (exact: the
+//             forward saved lambda_j). Each staged key gets a 4-bit mask of the groups within
+//             reach; keys are bucketed by mask so warps see uniform masks; lanes = keys loop
+//             over the queries of their groups with register accumulators (Alg. 2,
+//             PAPER.md:L540-568) and issue one red.global.add per channel per (item, key).
 #include "efunc_internal.cuh"
 
 namespace ef {
+
+constexpr int NWARP = NTHREADS / 32;
+constexpr int TRAV_UNR_MAX = 4;
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -29,21 +34,54 @@ __device__ __forceinline__ int cellc(float p, float inv_h, int NC) {
   return (int)c;
 }
 
-struct SmemList {
-  float4 a[LCAP];
-  float4 b[LCAP];
-  int id[LCAP];
-  uint32_t row_start[NTHREADS];
-  uint32_t row_off[NTHREADS];
-  uint32_t wcnt[NTHREADS / 32];
-  uint32_t wscan[NTHREADS / 32];
-};
-
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+
+struct Box {
+  float lx, ly, lz, hx, hy, hz, thr;
+};
+
+__device__ __forceinline__ bool within(const float4 a, const Box& b) {
+  const float dx = fmaxf(fmaxf(b.lx - a.x, a.x - b.hx), 0.0f);
+  const float dy = fmaxf(fmaxf(b.ly - a.y, a.y - b.hy), 0.0f);
+  const float dz = fmaxf(fmaxf(b.lz - a.z, a.z - b.hz), 0.0f);
+  return a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= b.thr;
+}
+
+// warp-level AABB + max(v) of the lanes with act; inactive lanes contribute nothing
+__device__ __forceinline__ Box warp_box(bool act, float x, float y, float z, float v) {
+  float r[7] = {act ? x : INFINITY, act ? y : INFINITY, act ? z : INFINITY, act ? -x : INFINITY,
+                act ? -y : INFINITY, act ? -z : INFINITY, act ? -v : INFINITY};
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r[i] = fminf(r[i], __shfl_xor_sync(~0u, r[i], o));
+  }
+  Box b;
+  b.lx = r[0]; b.ly = r[1]; b.lz = r[2];
+  b.hx = -r[3]; b.hy = -r[4]; b.hz = -r[5];
+  b.thr = -r[6];
+  return b;
+}
+
+struct SmemList {
+  float4 a[LCAP];
+  float4 b[LCAP];
+  int id[LCAP];
+  uint16_t widx[NWARP][LCAP];  // forward: per-warp index lists; backward: widx[0] = mask order
+  uint8_t mask[LCAP];
+  uint32_t row_start[NTHREADS];
+  uint32_t row_off[NTHREADS];
+  uint32_t wcnt[TRAV_UNR_MAX * NWARP];
+  uint32_t wscan[NWARP];
+  uint32_t hist[16];
+  uint32_t boff[17];
+  Box gbox[NWARP];
+  Box ibox;
+};
 
 // exclusive scan over the 128 threads of the CTA; returns offset, writes total
 __device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_w, uint32_t& total) {
@@ -58,7 +96,7 @@ __device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_w, uin
   __syncthreads();
   uint32_t off = 0, tot = 0;
 #pragma unroll
-  for (int k = 0; k < NTHREADS / 32; ++k) {
+  for (int k = 0; k < NWARP; ++k) {
     const uint32_t c = s_w[k];
     off += (k < w) ? c : 0u;
     tot += c;
@@ -67,20 +105,25 @@ __device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_w, uin
   return incl - v + off;
 }
 
-// Walk the candidate keys of an item in chunks of <= LCAP; proc(cnt) consumes sm.a/b/id[0,cnt).
-// Every thread of the CTA must call this (it contains __syncthreads). Returns candidates seen.
+// Stage the candidate keys of an item in chunks of <= LCAP; proc(cnt) consumes sm.a/b/id[0,cnt).
+// Every thread of the CTA must call this (it contains __syncthreads); proc is called by all.
+// Keys are visited in (row, position) order and compacted in that order, so the staged list is
+// deterministic. If gout != nullptr the sorted-key positions of the list are also written to
+// gout[0, gcap) (the forward hands its list to the backward). Returns the list length.
+constexpr int TRAV_UNR = 2;  // candidates per thread per round (loads in flight)
+
 template <bool NEED_ID, class Proc>
-__device__ __forceinline__ uint32_t traverse(const KeysView& kv, const ItemBox& box, SmemList& sm, Proc&& proc) {
+__device__ __forceinline__ uint32_t traverse(const KeysView& kv, const Box box, SmemList& sm, Proc&& proc,
+                                             uint32_t* gout = nullptr, uint32_t gcap = 0) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const float thr = box.lo.w;
-  const float rho = sqrtf(thr / *kv.bl_min);
+  const float rho = sqrtf(box.thr / *kv.bl_min);
   const int NC = kv.NC;
-  const int cx0 = cellc(box.lo.x - rho, kv.inv_h, NC), cx1 = cellc(box.hi.x + rho, kv.inv_h, NC);
-  const int cy0 = cellc(box.lo.y - rho, kv.inv_h, NC), cy1 = cellc(box.hi.y + rho, kv.inv_h, NC);
-  const int cz0 = cellc(box.lo.z - rho, kv.inv_h, NC), cz1 = cellc(box.hi.z + rho, kv.inv_h, NC);
+  const int cx0 = cellc(box.lx - rho, kv.inv_h, NC), cx1 = cellc(box.hx + rho, kv.inv_h, NC);
+  const int cy0 = cellc(box.ly - rho, kv.inv_h, NC), cy1 = cellc(box.hy + rho, kv.inv_h, NC);
+  const int cz0 = cellc(box.lz - rho, kv.inv_h, NC), cz1 = cellc(box.hz + rho, kv.inv_h, NC);
   const int ny = cy1 - cy0 + 1;
   const int nrows = ny * (cz1 - cz0 + 1);
-  uint32_t cnt = 0, seen = 0;
+  uint32_t cnt = 0, staged = 0;
   for (int rb = 0; rb < nrows; rb += NTHREADS) {
     const int r = rb + tid;
     uint32_t s = 0, len = 0;
@@ -95,45 +138,54 @@ __device__ __forceinline__ uint32_t traverse(const KeysView& kv, const ItemBox& 
     sm.row_start[tid] = s;
     sm.row_off[tid] = off;
     __syncthreads();
-    for (uint32_t f0 = 0; f0 < total; f0 += NTHREADS) {
-      const uint32_t f = f0 + tid;
-      bool pass = false;
-      float4 ka = make_float4(0.f, 0.f, 0.f, 0.f);
-      uint32_t kp = 0;
-      if (f < total) {
-        int lo = 0, hi = NTHREADS;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (sm.row_off[mid] <= f) lo = mid; else hi = mid;
-        }
-        kp = sm.row_start[lo] + (f - sm.row_off[lo]);
-        ka = __ldg(&kv.ks[2 * kp]);
-        const float dx = fmaxf(fmaxf(box.lo.x - ka.x, ka.x - box.hi.x), 0.0f);
-        const float dy = fmaxf(fmaxf(box.lo.y - ka.y, ka.y - box.hi.y), 0.0f);
-        const float dz = fmaxf(fmaxf(box.lo.z - ka.z, ka.z - box.hi.z), 0.0f);
-        pass = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= thr;
-      }
-      const uint32_t bal = __ballot_sync(~0u, pass);
-      if (lane == 0) sm.wcnt[w] = __popc(bal);
-      __syncthreads();
-      uint32_t woff = 0, btot = 0;
+    int row = 0;  // per-thread row cursor; f only grows, so the walk is amortised O(1)
+    for (uint32_t f0 = 0; f0 < total; f0 += TRAV_UNR * NTHREADS) {
+      bool pass[TRAV_UNR];
+      float4 ka[TRAV_UNR];
+      uint32_t kp[TRAV_UNR], bal[TRAV_UNR];
 #pragma unroll
-      for (int k = 0; k < NTHREADS / 32; ++k) {
-        const uint32_t c = sm.wcnt[k];
-        woff += (k < w) ? c : 0u;
-        btot += c;
+      for (int u = 0; u < TRAV_UNR; ++u) {
+        const uint32_t f = f0 + u * NTHREADS + tid;
+        pass[u] = false;
+        kp[u] = 0;
+        if (f < total) {
+          while (row + 1 < NTHREADS && sm.row_off[row + 1] <= f) ++row;
+          kp[u] = sm.row_start[row] + (f - sm.row_off[row]);
+          ka[u] = __ldg(&kv.ks[2 * kp[u]]);
+        }
       }
-      if (pass) {
-        const uint32_t slot = cnt + woff + __popc(bal & lanemask_lt());
-        sm.a[slot] = ka;
-        sm.b[slot] = __ldg(&kv.ks[2 * kp + 1]);
-        if (NEED_ID) sm.id[slot] = __ldg(&kv.kid[kp]);
+#pragma unroll
+      for (int u = 0; u < TRAV_UNR; ++u) {
+        const uint32_t f = f0 + u * NTHREADS + tid;
+        if (f < total) pass[u] = within(ka[u], box);
+        bal[u] = __ballot_sync(~0u, pass[u]);
+        if (lane == 0) sm.wcnt[u * NWARP + w] = __popc(bal[u]);
       }
-      cnt += btot;
       __syncthreads();
-      if (cnt > (uint32_t)(LCAP - NTHREADS)) {
+      uint32_t base = cnt;
+#pragma unroll
+      for (int u = 0; u < TRAV_UNR; ++u) {
+        uint32_t woff = 0, btot = 0;
+#pragma unroll
+        for (int k = 0; k < NWARP; ++k) {
+          const uint32_t c = sm.wcnt[u * NWARP + k];
+          woff += (k < w) ? c : 0u;
+          btot += c;
+        }
+        if (pass[u]) {
+          const uint32_t slot = base + woff + __popc(bal[u] & lanemask_lt());
+          sm.a[slot] = ka[u];
+          sm.b[slot] = __ldg(&kv.ks[2 * kp[u] + 1]);
+          if (NEED_ID) sm.id[slot] = __ldg(&kv.kid[kp[u]]);
+          if (gout && staged + (slot - cnt) < gcap) gout[staged + (slot - cnt)] = kp[u];
+        }
+        base += btot;
+      }
+      staged += base - cnt;
+      cnt = base;
+      __syncthreads();
+      if (cnt > (uint32_t)(LCAP - TRAV_UNR * NTHREADS)) {
         proc(cnt);
-        seen += cnt;
         cnt = 0;
         __syncthreads();
       }
@@ -141,29 +193,52 @@ __device__ __forceinline__ uint32_t traverse(const KeysView& kv, const ItemBox& 
   }
   if (cnt > 0) {
     proc(cnt);
-    seen += cnt;
     __syncthreads();
   }
-  return seen;
+  return staged;
+}
+
+// Stage a list saved by the forward (sorted-key positions) in chunks of <= LCAP.
+template <class Proc>
+__device__ __forceinline__ void stage_list(const KeysView& kv, const uint32_t* __restrict__ list, uint32_t n,
+                                           SmemList& sm, Proc&& proc) {
+  const int tid = threadIdx.x;
+  for (uint32_t c0 = 0; c0 < n; c0 += LCAP) {
+    const uint32_t cnt = min((uint32_t)LCAP, n - c0);
+    for (uint32_t k = tid; k < cnt; k += NTHREADS) {
+      const uint32_t kp = __ldg(&list[c0 + k]);
+      sm.a[k] = __ldg(&kv.ks[2 * kp]);
+      sm.b[k] = __ldg(&kv.ks[2 * kp + 1]);
+      sm.id[k] = __ldg(&kv.kid[kp]);
+    }
+    __syncthreads();
+    proc(cnt);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------------------ forward
 template <bool WANT_G>
 __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   __shared__ SmemList sm;
-  __shared__ float s_red[7][NTHREADS / 32];
+  __shared__ float s_red[NWARP];
   const KeysView& kv = A.kv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t j0 = (int64_t)blockIdx.x * QITEM;
-  const int nq = (int)((A.J - j0) < (int64_t)QITEM ? (A.J - j0) : (int64_t)QITEM);
+  const uint32_t item = blockIdx.x;
+  if (item >= *A.n_items) return;
+  const int2 it = A.items[item];
+  const int64_t j0 = it.x;
+  const int nq = it.y;
   const bool act = tid < nq;
+  const int nact_w = max(0, min(32, nq - 32 * w));  // active queries of this warp
   const float4 q = act ? A.qs[j0 + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
 
-  // shift bound mh_j: exponent (log2 units) of the best of the 8 lattice-corner grid keys
+  // shift bound mh_j >= m_j (log2 units): best of the 8 lattice-corner grid keys and of (up to
+  // 32) keys staged in the query's own cell; f0 = f of that key at q (accuracy shift, App. D)
   float mh = INFINITY, f0 = 0.0f;
   if (act) {
-    const int R = kv.R;
-    const int cx = cellc(q.x, kv.inv_h, kv.NC), cy = cellc(q.y, kv.inv_h, kv.NC), cz = cellc(q.z, kv.inv_h, kv.NC);
+    const int R = kv.R, NC = kv.NC;
+    const int cx = cellc(q.x, kv.inv_h, NC), cy = cellc(q.y, kv.inv_h, NC), cz = cellc(q.z, kv.inv_h, NC);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int n = (cx + (c & 1)) + R * ((cy + ((c >> 1) & 1)) + R * (cz + (c >> 2)));
@@ -178,68 +253,95 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
         }
       }
     }
+    const int cid = (cz * NC + cy) * NC + cx;
+    const uint32_t s = __ldg(&kv.cell_start[cid]);
+    const uint32_t e_ = min(__ldg(&kv.cell_start[cid + 1]), s + 32u);
+    for (uint32_t k = s; k < e_; ++k) {
+      const float4 ka = __ldg(&kv.ks[2 * k]);
+      const float dx = q.x - ka.x, dy = q.y - ka.y, dz = q.z - ka.z;
+      const float e = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      if (e < mh) {
+        mh = e;
+        if (WANT_G) {
+          const float4 kb = __ldg(&kv.ks[2 * k + 1]);
+          f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
+        }
+      }
+    }
   }
-  // item box: AABB of the active queries + max shift bound
-  float r7[7] = {act ? q.x : INFINITY, act ? q.y : INFINITY, act ? q.z : INFINITY,
-                 act ? -q.x : INFINITY, act ? -q.y : INFINITY, act ? -q.z : INFINITY,
-                 act ? -mh : INFINITY};
-#pragma unroll
-  for (int i = 0; i < 7; ++i) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r7[i] = fminf(r7[i], __shfl_xor_sync(~0u, r7[i], o));
-    if (lane == 0) s_red[i][w] = r7[i];
+  // warp sub-box and item box (union of the warp boxes)
+  Box wb = warp_box(act, q.x, q.y, q.z, mh);
+  wb.thr += A.T_l;
+  if (lane == 0) sm.gbox[w] = wb;
+  __syncthreads();
+  if (tid == 0) {
+    Box ib = sm.gbox[0];
+    for (int k = 1; k < NWARP; ++k) {
+      const Box g = sm.gbox[k];
+      ib.lx = fminf(ib.lx, g.lx); ib.ly = fminf(ib.ly, g.ly); ib.lz = fminf(ib.lz, g.lz);
+      ib.hx = fmaxf(ib.hx, g.hx); ib.hy = fmaxf(ib.hy, g.hy); ib.hz = fmaxf(ib.hz, g.hz);
+      ib.thr = fmaxf(ib.thr, g.thr);
+    }
+    sm.ibox = ib;
   }
   __syncthreads();
-  ItemBox box;
-  {
-    float v[7];
-#pragma unroll
-    for (int i = 0; i < 7; ++i) {
-      v[i] = s_red[i][0];
-#pragma unroll
-      for (int k = 1; k < NTHREADS / 32; ++k) v[i] = fminf(v[i], s_red[i][k]);
-    }
-    box.lo = make_float4(v[0], v[1], v[2], -v[6] + A.T_l);
-    box.hi = make_float4(-v[3], -v[4], -v[5], 0.0f);
-  }
-  if (tid == 0) A.boxes[blockIdx.x] = box;
+  const Box ibox = sm.ibox;
 
   float Z = 0.f, M = 0.f;
   float sgx = 0.f, sgy = 0.f, sgz = 0.f, sux = 0.f, suy = 0.f, suz = 0.f, sfx = 0.f, sfy = 0.f, sfz = 0.f;
   float shift = mh;
+  unsigned long long cand = 0;
   auto accum = [&](uint32_t cnt) {
+    if (nact_w == 0) return;  // warp-uniform
+    // per-warp filter against the warp's own sub-box
+    uint32_t nw = 0;
+    for (uint32_t base = 0; base < cnt; base += 32) {
+      const uint32_t k = base + lane;
+      const bool pass = (k < cnt) && within(sm.a[k], wb);
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      if (pass) sm.widx[w][nw + __popc(bal & lanemask_lt())] = (uint16_t)k;
+      nw += __popc(bal);
+    }
+    __syncwarp();
+    cand += (unsigned long long)nw;
     if (!act) return;
 #pragma unroll 4
-    for (uint32_t k = 0; k < cnt; ++k) {
+    for (uint32_t i = 0; i < nw; ++i) {
+      const uint32_t k = sm.widx[w][i];
       const float4 a = sm.a[k];
       const float4 b = sm.b[k];
       const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
       const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
       const float wgt = ex2f(fmaf(-a.w, dd, shift));
-      float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
       Z += wgt;
       if (WANT_G) {
-        f -= f0;
+        const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x - f0)));
         sgx = fmaf(wgt, b.y, sgx);
         sgy = fmaf(wgt, b.z, sgy);
         sgz = fmaf(wgt, b.w, sgz);
-        const float wb = wgt * a.w;
-        sux = fmaf(wb, dx, sux);
-        suy = fmaf(wb, dy, suy);
-        suz = fmaf(wb, dz, suz);
-        const float wbf = wb * f;
+        const float wbl = wgt * a.w;
+        sux = fmaf(wbl, dx, sux);
+        suy = fmaf(wbl, dy, suy);
+        suz = fmaf(wbl, dz, suz);
+        const float wbf = wbl * f;
         sfx = fmaf(wbf, dx, sfx);
         sfy = fmaf(wbf, dy, sfy);
         sfz = fmaf(wbf, dz, sfz);
+        M = fmaf(wgt, f, M);
+      } else {
+        const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+        M = fmaf(wgt, f, M);
       }
-      M = fmaf(wgt, f, M);
     }
   };
-  uint32_t cand = traverse<false>(kv, box, sm, accum);
+  {
+    const uint32_t n = traverse<false>(kv, ibox, sm, accum, A.lists + (size_t)item * A.list_cap, A.list_cap);
+    if (tid == 0) A.list_n[item] = n;
+  }
 
   const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
   if (__syncthreads_or(bad)) {
-    // exact-shift slow path: shift = min over the candidate set (contains the argmin key)
+    // exact-shift slow path: shift = min over the staged set (it contains every argmin key)
     float mexact = INFINITY;
     auto minpass = [&](uint32_t cnt) {
       if (!act) return;
@@ -249,16 +351,17 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
         mexact = fminf(mexact, a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
       }
     };
-    traverse<false>(kv, box, sm, minpass);
+    traverse<false>(kv, ibox, sm, minpass);
     shift = mexact;
     Z = M = 0.f;
     sgx = sgy = sgz = sux = suy = suz = sfx = sfy = sfz = 0.f;
-    traverse<false>(kv, box, sm, accum);
+    cand = 0;
+    traverse<false>(kv, ibox, sm, accum);
     if (tid == 0) atomicAdd(&A.ds->overflow_items, 1u);
   }
 
   if (A.count_kept) {
-    // diagnostic: exact per-query min over candidates, then count pairs with e - m <= T_l
+    // diagnostic: exact per-query min over the staged set, then count pairs with e - m <= T_l
     float mexact = INFINITY;
     auto minpass = [&](uint32_t cnt) {
       if (!act) return;
@@ -268,7 +371,7 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
         mexact = fminf(mexact, a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
       }
     };
-    traverse<false>(kv, box, sm, minpass);
+    traverse<false>(kv, ibox, sm, minpass);
     unsigned long long kept = 0, kept_off = 0;
     auto countpass = [&](uint32_t cnt) {
       if (!act) return;
@@ -280,7 +383,7 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
         kept_off += (kp && sm.id[k] >= kv.n_nodes) ? 1ull : 0ull;
       }
     };
-    traverse<true>(kv, box, sm, countpass);
+    traverse<true>(kv, ibox, sm, countpass);
     for (int o = 16; o > 0; o >>= 1) {
       kept += __shfl_xor_sync(~0u, kept, o);
       kept_off += __shfl_xor_sync(~0u, kept_off, o);
@@ -290,7 +393,7 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       atomicAdd(&A.ds->kept_pairs_offset, kept_off);
     }
   }
-  if (tid == 0) atomicAdd(&A.ds->cand_pairs, (unsigned long long)cand * (unsigned long long)nq);
+  if (lane == 0 && nact_w > 0) atomicAdd(&A.ds->cand_pairs, cand * (unsigned long long)nact_w);
 
   // epilogue: O, lambda, G, loss and its upstream
   float lossj = 0.0f;
@@ -332,13 +435,12 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   }
   if (A.loss_kind >= EFUNC_LOSS_MSE) {
     for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
-    __syncthreads();
-    if (lane == 0) s_red[0][w] = lossj;
+    if (lane == 0) s_red[w] = lossj;
     __syncthreads();
     if (tid == 0) {
       float t = 0.f;
-      for (int k = 0; k < NTHREADS / 32; ++k) t += s_red[0][k];
-      A.loss_part[blockIdx.x] = t;
+      for (int k = 0; k < NWARP; ++k) t += s_red[k];
+      A.loss_part[item] = t;
     }
   }
 }
@@ -358,12 +460,18 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   __shared__ float4 sv[QITEM];  // r, O, h.ubar, h.G
   __shared__ float4 sh[EIK ? QITEM : 1];
   const KeysView& kv = A.kv;
-  const int tid = threadIdx.x;
-  const int64_t j0 = (int64_t)blockIdx.x * QITEM;
-  const int nq = (int)((A.J - j0) < (int64_t)QITEM ? (A.J - j0) : (int64_t)QITEM);
-  if (tid < nq) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t item = blockIdx.x;
+  if (item >= *A.n_items) return;
+  const int2 it = A.items[item];
+  const int64_t j0 = it.x;
+  const int nq = it.y;
+  const int ng = (nq + 31) / 32;
+  const bool act = tid < nq;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (act) {
     const int64_t js = j0 + tid;
-    const float4 q = A.qs[js];
+    q = A.qs[js];
     const float4 rc = A.rec[js];
     const int ju = A.perm[js];
     const float r = A.dL_dO ? A.dL_dO[ju] : rc.y;
@@ -377,67 +485,116 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
       T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
       sh[tid] = hv;
     }
-    sq[tid] = make_float4(q.x, q.y, q.z, rc.x);
+    q.w = rc.x;
+    sq[tid] = q;
     sv[tid] = make_float4(r, rc.z, hub, T);
   }
-  const ItemBox box = A.boxes[blockIdx.x];
+  // query-group boxes with the exact threshold max_j(-lambda_l) + T_l (pairs with p < 2^-T_l skip)
+  Box gb = warp_box(act, q.x, q.y, q.z, q.w);
+  gb.thr += A.T_l;
+  if (lane == 0) sm.gbox[w] = gb;
   __syncthreads();
+  if (tid == 0) {
+    Box ib = sm.gbox[0];
+    for (int k = 1; k < ng; ++k) {
+      const Box g = sm.gbox[k];
+      ib.lx = fminf(ib.lx, g.lx); ib.ly = fminf(ib.ly, g.ly); ib.lz = fminf(ib.lz, g.lz);
+      ib.hx = fmaxf(ib.hx, g.hx); ib.hy = fmaxf(ib.hy, g.hy); ib.hz = fmaxf(ib.hz, g.hz);
+      ib.thr = fmaxf(ib.thr, g.thr);
+    }
+    sm.ibox = ib;
+  }
+  __syncthreads();
+  const Box ibox = sm.ibox;
 
   auto proc = [&](uint32_t cnt) {
+    // 1. mask of query groups within reach, histogram over masks
+    if (tid < 16) sm.hist[tid] = 0;
+    __syncthreads();
     for (uint32_t k = tid; k < cnt; k += NTHREADS) {
+      const float4 a = sm.a[k];
+      uint32_t m = 0;
+      for (int g = 0; g < ng; ++g) m |= within(a, sm.gbox[g]) ? (1u << g) : 0u;
+      sm.mask[k] = (uint8_t)m;
+      if (m) atomicAdd(&sm.hist[m], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t o = 0;
+      for (int m = 0; m < 16; ++m) {
+        sm.boff[m] = o;
+        o += sm.hist[m];
+      }
+      sm.boff[16] = o;
+    }
+    __syncthreads();
+    const uint32_t nz = sm.boff[16];
+    for (uint32_t k = tid; k < cnt; k += NTHREADS) {
+      const uint32_t m = sm.mask[k];
+      if (m) sm.widx[0][atomicAdd(&sm.boff[m], 1u)] = (uint16_t)k;
+    }
+    __syncthreads();
+    // 2. lanes = keys (mask-bucketed), loop over the queries of the groups in the mask
+    for (uint32_t i = tid; i < nz; i += NTHREADS) {
+      const uint32_t k = sm.widx[0][i];
+      const uint32_t m = sm.mask[k];
       const float4 a = sm.a[k];
       const float4 b = sm.b[k];
       const int id = sm.id[k];
       const float beta = a.w * EF_LN2;
       float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
       float phx = 0.f, phy = 0.f, phz = 0.f, pdx = 0.f, pdy = 0.f, pdz = 0.f;  // EIK only
+      for (int g = 0; g < ng; ++g) {
+        if (!((m >> g) & 1u)) continue;
+        const int jend = min(nq, 32 * g + 32);
 #pragma unroll 4
-      for (int j = 0; j < nq; ++j) {
-        const float4 P = sq[j];
-        const float4 V = sv[j];
-        const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
-        const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        const float p = ex2f(fmaf(-a.w, dd, P.w));
-        const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
-        const float del = f - V.y;
-        if (!EIK) {
-          // Alg. 2: dO/dc = p, dO/dg = p d, dO/ds = -p a (f - O), dO/dk = p(-g + 2 beta d (f - O))
-          const float t = V.x * p;
-          const float u = t * del;
-          sc += t;
-          sgx = fmaf(t, dx, sgx);
-          sgy = fmaf(t, dy, sgy);
-          sgz = fmaf(t, dz, sgz);
-          ss = fmaf(u, dd, ss);
-          sdx = fmaf(u, dx, sdx);
-          sdy = fmaf(u, dy, sdy);
-          sdz = fmaf(u, dz, sdz);
-        } else {
-          // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
-          const float4 H = sh[j];
-          const float hd = fmaf(H.x, dx, fmaf(H.y, dy, H.z * dz));
-          const float hu = 2.0f * beta * hd;
-          const float hg = fmaf(H.x, b.y, fmaf(H.y, b.z, H.z * b.w));
-          const float tt = fmaf(-hu, del, hg);
-          const float alpha = V.x + V.z - hu;
-          const float gam = fmaf(V.x + V.z, del, tt - V.w);
-          const float pa = p * alpha;
-          sc += pa;
-          sgx = fmaf(pa, dx, sgx);
-          sgy = fmaf(pa, dy, sgy);
-          sgz = fmaf(pa, dz, sgz);
-          phx = fmaf(p, H.x, phx);
-          phy = fmaf(p, H.y, phy);
-          phz = fmaf(p, H.z, phz);
-          ss = fmaf(p, fmaf(beta * dd, gam, hu * del), ss);
-          const float pg = p * gam;
-          sdx = fmaf(pg, dx, sdx);
-          sdy = fmaf(pg, dy, sdy);
-          sdz = fmaf(pg, dz, sdz);
-          const float pdel = p * del;
-          pdx = fmaf(pdel, H.x, pdx);
-          pdy = fmaf(pdel, H.y, pdy);
-          pdz = fmaf(pdel, H.z, pdz);
+        for (int j = 32 * g; j < jend; ++j) {
+          const float4 P = sq[j];
+          const float4 V = sv[j];
+          const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
+          const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          const float p = ex2f(fmaf(-a.w, dd, P.w));
+          const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+          const float del = f - V.y;
+          if (!EIK) {
+            // Alg. 2: dO/dc = p, dO/dg = p d, dO/ds = -p a (f - O), dO/dk = p(-g + 2 beta d (f - O))
+            const float t = V.x * p;
+            const float u = t * del;
+            sc += t;
+            sgx = fmaf(t, dx, sgx);
+            sgy = fmaf(t, dy, sgy);
+            sgz = fmaf(t, dz, sgz);
+            ss = fmaf(u, dd, ss);
+            sdx = fmaf(u, dx, sdx);
+            sdy = fmaf(u, dy, sdy);
+            sdz = fmaf(u, dz, sdz);
+          } else {
+            // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
+            const float4 H = sh[j];
+            const float hd = fmaf(H.x, dx, fmaf(H.y, dy, H.z * dz));
+            const float hu = 2.0f * beta * hd;
+            const float hg = fmaf(H.x, b.y, fmaf(H.y, b.z, H.z * b.w));
+            const float tt = fmaf(-hu, del, hg);
+            const float alpha = V.x + V.z - hu;
+            const float gam = fmaf(V.x + V.z, del, tt - V.w);
+            const float pa = p * alpha;
+            sc += pa;
+            sgx = fmaf(pa, dx, sgx);
+            sgy = fmaf(pa, dy, sgy);
+            sgz = fmaf(pa, dz, sgz);
+            phx = fmaf(p, H.x, phx);
+            phy = fmaf(p, H.y, phy);
+            phz = fmaf(p, H.z, phz);
+            ss = fmaf(p, fmaf(beta * dd, gam, hu * del), ss);
+            const float pg = p * gam;
+            sdx = fmaf(pg, dx, sdx);
+            sdy = fmaf(pg, dy, sdy);
+            sdz = fmaf(pg, dz, sdz);
+            const float pdel = p * del;
+            pdx = fmaf(pdel, H.x, pdx);
+            pdy = fmaf(pdel, H.y, pdy);
+            pdz = fmaf(pdel, H.z, pdz);
+          }
         }
       }
       float dsv, dgx, dgy, dgz, dkx, dky, dkz;
@@ -455,26 +612,28 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
         dkz = fmaf(-b.w, sc, 2.0f * beta * (sdz + pdz));
       }
       if (id < kv.n_nodes) {
-        float* g = A.grad + (size_t)id * EF_NCH;
-        atomicAdd(g + 0, dsv);
-        atomicAdd(g + 1, sc);
-        atomicAdd(g + 2, dgx);
-        atomicAdd(g + 3, dgy);
-        atomicAdd(g + 4, dgz);
+        float* gp = A.grad + (size_t)id * EF_NCH;
+        atomicAdd(gp + 0, dsv);
+        atomicAdd(gp + 1, sc);
+        atomicAdd(gp + 2, dgx);
+        atomicAdd(gp + 3, dgy);
+        atomicAdd(gp + 4, dgz);
       } else {
-        float* g = A.grad + (size_t)(id - kv.n_nodes) * EF_NCH;
-        atomicAdd(g + 5, dkx);
-        atomicAdd(g + 6, dky);
-        atomicAdd(g + 7, dkz);
-        atomicAdd(g + 8, dsv);
-        atomicAdd(g + 9, sc);
-        atomicAdd(g + 10, dgx);
-        atomicAdd(g + 11, dgy);
-        atomicAdd(g + 12, dgz);
+        float* gp = A.grad + (size_t)(id - kv.n_nodes) * EF_NCH;
+        atomicAdd(gp + 5, dkx);
+        atomicAdd(gp + 6, dky);
+        atomicAdd(gp + 7, dkz);
+        atomicAdd(gp + 8, dsv);
+        atomicAdd(gp + 9, sc);
+        atomicAdd(gp + 10, dgx);
+        atomicAdd(gp + 11, dgy);
+        atomicAdd(gp + 12, dgz);
       }
     }
   };
-  traverse<true>(kv, box, sm, proc);
+  const uint32_t ln = A.list_n[item];
+  if (ln <= A.list_cap) stage_list(kv, A.lists + (size_t)item * A.list_cap, ln, sm, proc);
+  else traverse<true>(kv, ibox, sm, proc);
 }
 
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {

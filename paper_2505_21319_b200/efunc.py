@@ -37,8 +37,8 @@ class Loss(C.Structure):
 
 
 class AdamWParams(C.Structure):
-    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("weight_decay", C.c_float), ("decay_mask", C.c_uint32)]
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("decay_mask", C.c_uint32)]
 
 
 class Stats(C.Structure):

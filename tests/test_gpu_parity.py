@@ -62,10 +62,13 @@ def test_forward_parity_c1(T):
 
 
 def test_partition_of_unity_on_gpu():
-    """Shared linear polynomial is reproduced exactly for any truncated key set."""
-    R = 16
-    A, B = 0.3, np.array([0.7, -1.2, 0.4])
+    """Shared linear polynomial is reproduced exactly for any truncated key set.
+    R = 17 (h = 1/8), dyadic A, B and offsets make the float32 theta an EXACT partition-of-unity
+    configuration, so O = P(q) and G = B up to arithmetic rounding only."""
+    R = 17
+    A, B = 0.25, np.array([0.5, -0.25, 0.125])
     th = synth.random_theta(R, 3, log_scale_mean=7.0, log_scale_std=0.3, offset_std=0.03).astype(np.float64)
+    th[:, 5:8] = np.round(th[:, 5:8] * 4096.0) / 4096.0
     k = orc.node_positions(R)
     th[:, 1] = A + k @ B; th[:, 2:5] = B
     th[:, 9] = A + (k + th[:, 5:8]) @ B; th[:, 10:13] = B
@@ -74,8 +77,10 @@ def test_partition_of_unity_on_gpu():
     m = ef.EFunc(R, th)
     O, G, _ = m.forward(dev(q), want_G=True)
     exact = A + q.astype(np.float64) @ B
-    assert nw(O.cpu().numpy(), exact) <= 2e-6
-    assert np.abs(G.cpu().numpy() - B[None, :]).max() <= 2e-5
+    eO = nw(O.cpu().numpy(), exact)
+    eG = nw(G.cpu().numpy(), np.broadcast_to(B, (q.shape[0], 3)))
+    assert eO <= 2e-6, eO
+    assert eG <= 1e-5, eG
 
 
 def test_eval_grad_matches_forward_and_oracle():
@@ -146,8 +151,9 @@ def test_adamw_parity():
         np.testing.assert_allclose(got, cur, rtol=2e-6, atol=1e-7)
     gm, gv, st = m.get_adam_state()
     assert st == 3
-    np.testing.assert_allclose(gm, mm, rtol=1e-5, atol=1e-12)
-    np.testing.assert_allclose(gv, vv, rtol=1e-5, atol=1e-16)
+    # moments: fp32 rounding relative to the size of the gradients that built them
+    assert np.abs(gm - mm).max() <= 1e-6 * np.abs(mm).max()
+    assert np.abs(gv - vv).max() <= 1e-6 * np.abs(vv).max()
 
 
 def test_fit_c1_ten_steps_resynced_and_free_running():
