@@ -142,11 +142,9 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   }
   const int64_t bound = (J + QITEM - 1) / QITEM + n_coarse;
   if (bound > h->items_cap) {
-    dfree(h->boxes); dfree(h->loss_part); dfree(h->items); dfree(h->lists); dfree(h->list_n);
-    CK(dalloc(&h->lists, (size_t)bound * LIST_CAP));
-    CK(dalloc(&h->list_n, bound));
+    dfree(h->boxes); dfree(h->loss_part); dfree(h->items);
     CK(dalloc(&h->boxes, bound));
-    CK(dalloc(&h->loss_part, bound));
+    CK(dalloc(&h->loss_part, 4 * bound));
     CK(dalloc(&h->items, bound));
     h->items_cap = bound;
   }
@@ -175,7 +173,7 @@ void free_all(efunc_t* h) {
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
   dfree(h->boxes); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
-  dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->lists); dfree(h->list_n);
+  dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -240,11 +238,8 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   a.loss_part = h->loss_part;
   a.ds = h->ds;
   a.count_kept = h->count_kept;
-  a.lists = h->lists;
-  a.list_n = h->list_n;
-  a.list_cap = LIST_CAP;
   h->launches += launch_forward(a, want_g, items, s);
-  if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, loss_out, s);
+  if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, 4, loss_out, s);
   else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   CK(cudaGetLastError());
   if (h->cfg.sync_checks) {
@@ -279,9 +274,7 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.items = h->items;
   b.n_items = h->item_off + h->fwd_n_coarse;
   b.T_l = cutoff_log2(h->cfg);
-  b.lists = h->lists;
-  b.list_n = h->list_n;
-  b.list_cap = LIST_CAP;
+  b.gpad = h->gpad;
   b.rec = h->rec;
   b.gs = h->gs;
   b.us = h->us;
@@ -292,6 +285,7 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.grad = grad;
   b.eik = eik;
   h->launches += launch_backward(b, h->fwd_items_bound, s);
+  h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
   CK(cudaGetLastError());
   return EFUNC_OK;
 }
@@ -361,6 +355,8 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->cell_start, h->n_cells + 1));
     CK(dalloc(&h->cell_fill, h->n_cells + 1));
     CK(dalloc(&h->ds, 1));
+    CK(dalloc(&h->gpad, (size_t)h->n_nodes * 16));
+    CK(cudaMemset(h->gpad, 0, sizeof(float) * (size_t)h->n_nodes * 16));
     CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
     RET(ensure_scan_tmp(h, h->n_cells + 1));
     if (theta_host) CK(cudaMemcpy(h->theta, theta_host, np * sizeof(float), cudaMemcpyHostToDevice));

@@ -28,7 +28,6 @@ constexpr int QITEM = 128;        // queries per work item == forward/backward C
 constexpr int NTHREADS = 128;
 constexpr int LCAP = 512;         // candidate keys staged in shared memory per chunk
 constexpr int MAX_QBITS = 7;      // Morton bits per axis for query binning
-constexpr uint32_t LIST_CAP = 2048;  // per-item candidate list handed from forward to backward
 
 struct KeysView {
   const float4* ks;        // sorted records, 2 float4 per key (a at 2k, b at 2k+1)
@@ -79,9 +78,6 @@ struct FwdArgs {
   float* loss_part;       // per item partial loss
   DevScalars* ds;
   int count_kept;
-  uint32_t* lists;        // per item: sorted-key positions of its staged candidates (cap list_cap)
-  uint32_t* list_n;       // per item: list length (> list_cap: the backward re-stages)
-  uint32_t list_cap;
 };
 
 struct BwdArgs {
@@ -101,9 +97,7 @@ struct BwdArgs {
   const ItemBox* boxes;
   float* grad;            // [R^3][13] +=
   int eik;                // 1: add the dL/dG terms
-  const uint32_t* lists;
-  const uint32_t* list_n;
-  uint32_t list_cap;
+  float* gpad;            // [R^3][16] padded accumulation buffer (zero on entry, zeroed by k_fold)
 };
 
 // ---------------------------------------------------------------- launchers (host)
@@ -121,7 +115,8 @@ int launch_gather_queries(const uint32_t* order, const float* q, const float* o,
                            float4* qs, int* perm, cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
-int launch_sum_partials(const float* part, const uint32_t* n, float* out, cudaStream_t s);
+int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
+int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
 int launch_items_count(const uint32_t* bin_start, int shift, uint32_t n_coarse, uint32_t* cnt,
                        cudaStream_t s);
 int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, const uint32_t* off,
@@ -178,8 +173,7 @@ struct efunc {
   float* loss_part = nullptr;
   int64_t items_cap = 0;
   int2* items = nullptr;          // [items bound]
-  uint32_t* lists = nullptr;      // [items bound][LIST_CAP]
-  uint32_t* list_n = nullptr;     // [items bound]
+  float* gpad = nullptr;          // [R^3][16] padded gradient accumulator (kept zero between calls)
   uint32_t* item_cnt = nullptr;   // [coarse cells + 1]
   uint32_t* item_off = nullptr;   // [coarse cells + 1]; item_off[n_coarse] = item count
   uint32_t coarse_cap = 0;

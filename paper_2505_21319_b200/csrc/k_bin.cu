@@ -316,10 +316,10 @@ int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, 
 }
 
 // Fixed-order sum of per-item loss partials (deterministic).
-__global__ void k_sum_partials(const float* __restrict__ part, const uint32_t* __restrict__ np,
+__global__ void k_sum_partials(const float* __restrict__ part, const uint32_t* __restrict__ np, int mult,
                                float* __restrict__ out) {
   __shared__ double s[1024];
-  const uint32_t n = *np;
+  const uint32_t n = *np * (uint32_t)mult;
   double acc = 0.0;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)part[i];
   s[threadIdx.x] = acc;
@@ -331,8 +331,8 @@ __global__ void k_sum_partials(const float* __restrict__ part, const uint32_t* _
   if (threadIdx.x == 0) *out = (float)s[0];
 }
 
-int launch_sum_partials(const float* part, const uint32_t* n, float* out, cudaStream_t s) {
-  k_sum_partials<<<1, 1024, 0, s>>>(part, n, out);
+int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s) {
+  k_sum_partials<<<1, 1024, 0, s>>>(part, n, mult, out);
   return 1;
 }
 

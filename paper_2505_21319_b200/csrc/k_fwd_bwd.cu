@@ -1,26 +1,28 @@
 // k_fwd_bwd.cu — S2/S3 forward (+ loss epilogue) and S4 backward.
 //
-// One CTA = one work item = up to QITEM Morton-consecutive queries inside one coarse cell,
-// split into 4 query groups of 32 (one per warp). Both kernels first stage, chunk by chunk,
-// the item's candidate keys in shared memory: keys of the lattice cells overlapping the
-// item's AABB grown by rho = sqrt(thr / bl_min), kept iff bl_k * dist^2(k, AABB) <= thr.
-// Every skipped pair therefore has a - m_j > cutoff_T (reading R-1):
-//   forward : thr = max_j mh_j + T_l, mh_j >= m_j the exponent of the best key among the 8
-//             lattice corners and the keys of the query's own cell (the shift of the paper's
-//             "maximum-reduce"). Each warp then filters the staged keys
-//             against its own 32-query sub-box and loops over its list with lanes = queries
-//             (Alg. 1). An exact-min slow path runs if sums overflow.
-//   backward: thr_g = max_{j in g} (-lambda_j log2e) + T_l per query group g (exact: the
-//             forward saved lambda_j). Each staged key gets a 4-bit mask of the groups within
-//             reach; keys are bucketed by mask so warps see uniform masks; lanes = keys loop
-//             over the queries of their groups with register accumulators (Alg. 2,
-//             PAPER.md:L540-568) and issue one red.global.add per channel per (item, key).
+// A work item is up to QITEM Morton-consecutive queries inside one coarse cell; each of the
+// CTA's 4 warps owns one group of 32 of them and runs independently (no block barrier on the
+// hot path). A warp enumerates the lattice cells overlapping its group's AABB grown by
+// rho = sqrt(thr / bl_min), keeps key k iff bl_k * dist^2(k, AABB) <= thr (warp-level
+// flattened row scan, deterministic order), stages the kept keys in its own shared-memory
+// slice and consumes them 32 at a time:
+//   forward : thr = max_j mh_j + T_l, mh_j >= m_j the exponent of the best key among the
+//             query's 8 lattice corners and its own cell (the shift of the paper's
+//             "maximum-reduce"). Every skipped pair has a - m_j > cutoff_T
+//             (reading R-1). Lanes = queries, staged keys broadcast (Alg. 1,
+//             PAPER.md:L505-518, and the G sums of Eq. func-normal). An exact-min
+//             slow path runs if a query's sums overflow.
+//   backward: thr = max_j(-lambda_j log2e) + T_l (the forward saved lambda_j; a skipped pair
+//             has p_ij < e^-T). Lanes = staged keys, the group's queries broadcast from shared
+//             memory, register accumulators (Alg. 2); per (key, group) two
+//             red.global.add.v4.f32 into a 16-float-per-node padded gradient, folded into the
+//             ABI layout by k_fold.
 #include "efunc_internal.cuh"
 
 namespace ef {
 
 constexpr int NWARP = NTHREADS / 32;
-constexpr int TRAV_UNR_MAX = 4;
+constexpr int WSLICE = 64;  // staged keys per warp
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -38,6 +40,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+__device__ __forceinline__ void red_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
 }
 
 struct Box {
@@ -67,55 +74,12 @@ __device__ __forceinline__ Box warp_box(bool act, float x, float y, float z, flo
   return b;
 }
 
-struct SmemList {
-  float4 a[LCAP];
-  float4 b[LCAP];
-  int id[LCAP];
-  uint16_t widx[NWARP][LCAP];  // forward: per-warp index lists; backward: widx[0] = mask order
-  uint8_t mask[LCAP];
-  uint32_t row_start[NTHREADS];
-  uint32_t row_off[NTHREADS];
-  uint32_t wcnt[TRAV_UNR_MAX * NWARP];
-  uint32_t wscan[NWARP];
-  uint32_t hist[16];
-  uint32_t boff[17];
-  Box gbox[NWARP];
-  Box ibox;
-};
-
-// exclusive scan over the 128 threads of the CTA; returns offset, writes total
-__device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_w, uint32_t& total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(~0u, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) s_w[w] = incl;
-  __syncthreads();
-  uint32_t off = 0, tot = 0;
-#pragma unroll
-  for (int k = 0; k < NWARP; ++k) {
-    const uint32_t c = s_w[k];
-    off += (k < w) ? c : 0u;
-    tot += c;
-  }
-  total = tot;
-  return incl - v + off;
-}
-
-// Stage the candidate keys of an item in chunks of <= LCAP; proc(cnt) consumes sm.a/b/id[0,cnt).
-// Every thread of the CTA must call this (it contains __syncthreads); proc is called by all.
-// Keys are visited in (row, position) order and compacted in that order, so the staged list is
-// deterministic. If gout != nullptr the sorted-key positions of the list are also written to
-// gout[0, gcap) (the forward hands its list to the backward). Returns the list length.
-constexpr int TRAV_UNR = 2;  // candidates per thread per round (loads in flight)
-
-template <bool NEED_ID, class Proc>
-__device__ __forceinline__ uint32_t traverse(const KeysView& kv, const Box box, SmemList& sm, Proc&& proc,
-                                             uint32_t* gout = nullptr, uint32_t gcap = 0) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+// Warp-level candidate enumeration. Visits the keys of the lattice-cell rows (x-runs) that
+// overlap the box grown by rho in (row, position) order, 32 at a time; calls
+// stage(pass, kp, a) on every lane for each batch (warp-uniform call; a valid iff pass).
+template <class Stage>
+__device__ __forceinline__ void enumerate(const KeysView& kv, const Box& box, Stage&& stage) {
+  const int lane = threadIdx.x & 31;
   const float rho = sqrtf(box.thr / *kv.bl_min);
   const int NC = kv.NC;
   const int cx0 = cellc(box.lx - rho, kv.inv_h, NC), cx1 = cellc(box.hx + rho, kv.inv_h, NC);
@@ -123,9 +87,8 @@ __device__ __forceinline__ uint32_t traverse(const KeysView& kv, const Box box, 
   const int cz0 = cellc(box.lz - rho, kv.inv_h, NC), cz1 = cellc(box.hz + rho, kv.inv_h, NC);
   const int ny = cy1 - cy0 + 1;
   const int nrows = ny * (cz1 - cz0 + 1);
-  uint32_t cnt = 0, staged = 0;
-  for (int rb = 0; rb < nrows; rb += NTHREADS) {
-    const int r = rb + tid;
+  for (int rb = 0; rb < nrows; rb += 32) {
+    const int r = rb + lane;
     uint32_t s = 0, len = 0;
     if (r < nrows) {
       const int cy = cy0 + r % ny, cz = cz0 + r / ny;
@@ -133,257 +96,193 @@ __device__ __forceinline__ uint32_t traverse(const KeysView& kv, const Box box, 
       s = __ldg(&kv.cell_start[base + cx0]);
       len = __ldg(&kv.cell_start[base + cx1 + 1]) - s;
     }
-    uint32_t total;
-    const uint32_t off = cta_excl_scan(len, sm.wscan, total);
-    sm.row_start[tid] = s;
-    sm.row_off[tid] = off;
-    __syncthreads();
-    int row = 0;  // per-thread row cursor; f only grows, so the walk is amortised O(1)
-    for (uint32_t f0 = 0; f0 < total; f0 += TRAV_UNR * NTHREADS) {
-      bool pass[TRAV_UNR];
-      float4 ka[TRAV_UNR];
-      uint32_t kp[TRAV_UNR], bal[TRAV_UNR];
+    uint32_t incl = len;
 #pragma unroll
-      for (int u = 0; u < TRAV_UNR; ++u) {
-        const uint32_t f = f0 + u * NTHREADS + tid;
-        pass[u] = false;
-        kp[u] = 0;
-        if (f < total) {
-          while (row + 1 < NTHREADS && sm.row_off[row + 1] <= f) ++row;
-          kp[u] = sm.row_start[row] + (f - sm.row_off[row]);
-          ka[u] = __ldg(&kv.ks[2 * kp[u]]);
-        }
-      }
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(~0u, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(~0u, incl, 31);
+    const uint32_t off = incl - len;
+    for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+      const uint32_t f = f0 + lane;
+      // source row: the largest lane l with off_l <= f (empty rows resolve to the next one)
+      int lo = 0;
 #pragma unroll
-      for (int u = 0; u < TRAV_UNR; ++u) {
-        const uint32_t f = f0 + u * NTHREADS + tid;
-        if (f < total) pass[u] = within(ka[u], box);
-        bal[u] = __ballot_sync(~0u, pass[u]);
-        if (lane == 0) sm.wcnt[u * NWARP + w] = __popc(bal[u]);
+      for (int st = 16; st > 0; st >>= 1) {
+        const uint32_t o = __shfl_sync(~0u, off, lo + st);
+        if (o <= f) lo += st;
       }
-      __syncthreads();
-      uint32_t base = cnt;
-#pragma unroll
-      for (int u = 0; u < TRAV_UNR; ++u) {
-        uint32_t woff = 0, btot = 0;
-#pragma unroll
-        for (int k = 0; k < NWARP; ++k) {
-          const uint32_t c = sm.wcnt[u * NWARP + k];
-          woff += (k < w) ? c : 0u;
-          btot += c;
-        }
-        if (pass[u]) {
-          const uint32_t slot = base + woff + __popc(bal[u] & lanemask_lt());
-          sm.a[slot] = ka[u];
-          sm.b[slot] = __ldg(&kv.ks[2 * kp[u] + 1]);
-          if (NEED_ID) sm.id[slot] = __ldg(&kv.kid[kp[u]]);
-          if (gout && staged + (slot - cnt) < gcap) gout[staged + (slot - cnt)] = kp[u];
-        }
-        base += btot;
+      const uint32_t srow = __shfl_sync(~0u, s, lo);
+      const uint32_t soff = __shfl_sync(~0u, off, lo);
+      const bool valid = f < total;
+      const uint32_t kp = srow + (f - soff);
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      bool pass = false;
+      if (valid) {
+        a = __ldg(&kv.ks[2 * kp]);
+        pass = within(a, box);
       }
-      staged += base - cnt;
-      cnt = base;
-      __syncthreads();
-      if (cnt > (uint32_t)(LCAP - TRAV_UNR * NTHREADS)) {
-        proc(cnt);
-        cnt = 0;
-        __syncthreads();
-      }
+      stage(pass, kp, a);
     }
   }
-  if (cnt > 0) {
-    proc(cnt);
-    __syncthreads();
-  }
-  return staged;
 }
 
-// Stage a list saved by the forward (sorted-key positions) in chunks of <= LCAP.
-template <class Proc>
-__device__ __forceinline__ void stage_list(const KeysView& kv, const uint32_t* __restrict__ list, uint32_t n,
-                                           SmemList& sm, Proc&& proc) {
-  const int tid = threadIdx.x;
-  for (uint32_t c0 = 0; c0 < n; c0 += LCAP) {
-    const uint32_t cnt = min((uint32_t)LCAP, n - c0);
-    for (uint32_t k = tid; k < cnt; k += NTHREADS) {
-      const uint32_t kp = __ldg(&list[c0 + k]);
-      sm.a[k] = __ldg(&kv.ks[2 * kp]);
-      sm.b[k] = __ldg(&kv.ks[2 * kp + 1]);
-      sm.id[k] = __ldg(&kv.kid[kp]);
+// Shift bound mh_j >= m_j (log2 units): best of the 8 lattice-corner grid keys and of (up to 32)
+// keys in the query's own cell; f0 = f of that key at q (accuracy shift of SURVEY App. D).
+__device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, float& mh, float& f0) {
+  const int R = kv.R, NC = kv.NC;
+  const int cx = cellc(q.x, kv.inv_h, NC), cy = cellc(q.y, kv.inv_h, NC), cz = cellc(q.z, kv.inv_h, NC);
+  mh = INFINITY;
+  f0 = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int n = (cx + (c & 1)) + R * ((cy + ((c >> 1) & 1)) + R * (cz + (c >> 2)));
+    const float4 ka = __ldg(&kv.grid_raw[2 * n]);
+    const float dx = q.x - ka.x, dy = q.y - ka.y, dz = q.z - ka.z;
+    const float e = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (e < mh) {
+      mh = e;
+      const float4 kb = __ldg(&kv.grid_raw[2 * n + 1]);
+      f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
     }
-    __syncthreads();
-    proc(cnt);
-    __syncthreads();
   }
+  const int cid = (cz * NC + cy) * NC + cx;
+  const uint32_t s = __ldg(&kv.cell_start[cid]);
+  const uint32_t e_ = min(__ldg(&kv.cell_start[cid + 1]), s + 32u);
+  for (uint32_t k = s; k < e_; ++k) {
+    const float4 ka = __ldg(&kv.ks[2 * k]);
+    const float dx = q.x - ka.x, dy = q.y - ka.y, dz = q.z - ka.z;
+    const float e = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (e < mh) {
+      mh = e;
+      const float4 kb = __ldg(&kv.ks[2 * k + 1]);
+      f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
+    }
+  }
+}
+
+__device__ __forceinline__ float exponent(const float4 q, const float4 a) {
+  const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
+  return a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 
 // ------------------------------------------------------------------------------ forward
+struct FwdAcc {
+  float Z, M, sgx, sgy, sgz, sux, suy, suz, sfx, sfy, sfz;
+};
+
+template <bool WANT_G>
+__device__ __forceinline__ void fwd_pair(const float4 q, const float4 a, const float4 b, float shift, float f0,
+                                         FwdAcc& s) {
+  const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
+  const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float wgt = ex2f(fmaf(-a.w, dd, shift));
+  s.Z += wgt;
+  if (WANT_G) {
+    const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x - f0)));
+    s.sgx = fmaf(wgt, b.y, s.sgx);
+    s.sgy = fmaf(wgt, b.z, s.sgy);
+    s.sgz = fmaf(wgt, b.w, s.sgz);
+    const float wbl = wgt * a.w;
+    s.sux = fmaf(wbl, dx, s.sux);
+    s.suy = fmaf(wbl, dy, s.suy);
+    s.suz = fmaf(wbl, dz, s.suz);
+    const float wbf = wbl * f;
+    s.sfx = fmaf(wbf, dx, s.sfx);
+    s.sfy = fmaf(wbf, dy, s.sfy);
+    s.sfz = fmaf(wbf, dz, s.sfz);
+    s.M = fmaf(wgt, f, s.M);
+  } else {
+    const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+    s.M = fmaf(wgt, f, s.M);
+  }
+}
+
 template <bool WANT_G>
 __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
-  __shared__ SmemList sm;
-  __shared__ float s_red[NWARP];
+  __shared__ float4 ws_a[NWARP][WSLICE];
+  __shared__ float4 ws_b[NWARP][WSLICE];
+  __shared__ int ws_id[NWARP][WSLICE];
   const KeysView& kv = A.kv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t item = blockIdx.x;
   if (item >= *A.n_items) return;
   const int2 it = A.items[item];
-  const int64_t j0 = it.x;
-  const int nq = it.y;
-  const bool act = tid < nq;
-  const int nact_w = max(0, min(32, nq - 32 * w));  // active queries of this warp
-  const float4 q = act ? A.qs[j0 + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
-
-  // shift bound mh_j >= m_j (log2 units): best of the 8 lattice-corner grid keys and of (up to
-  // 32) keys staged in the query's own cell; f0 = f of that key at q (accuracy shift, App. D)
-  float mh = INFINITY, f0 = 0.0f;
+  const int nact = min(32, it.y - 32 * w);  // queries of this warp's group
+  if (nact <= 0) {                           // (warps are independent: no block barrier below)
+    if (lane == 0 && A.loss_kind >= EFUNC_LOSS_MSE) A.loss_part[item * NWARP + w] = 0.0f;
+    return;
+  }
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + 32 * w + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY, f0 = 0.f;
   if (act) {
-    const int R = kv.R, NC = kv.NC;
-    const int cx = cellc(q.x, kv.inv_h, NC), cy = cellc(q.y, kv.inv_h, NC), cz = cellc(q.z, kv.inv_h, NC);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int n = (cx + (c & 1)) + R * ((cy + ((c >> 1) & 1)) + R * (cz + (c >> 2)));
-      const float4 ka = __ldg(&kv.grid_raw[2 * n]);
-      const float dx = q.x - ka.x, dy = q.y - ka.y, dz = q.z - ka.z;
-      const float e = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      if (e < mh) {
-        mh = e;
-        if (WANT_G) {
-          const float4 kb = __ldg(&kv.grid_raw[2 * n + 1]);
-          f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
-        }
-      }
-    }
-    const int cid = (cz * NC + cy) * NC + cx;
-    const uint32_t s = __ldg(&kv.cell_start[cid]);
-    const uint32_t e_ = min(__ldg(&kv.cell_start[cid + 1]), s + 32u);
-    for (uint32_t k = s; k < e_; ++k) {
-      const float4 ka = __ldg(&kv.ks[2 * k]);
-      const float dx = q.x - ka.x, dy = q.y - ka.y, dz = q.z - ka.z;
-      const float e = ka.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      if (e < mh) {
-        mh = e;
-        if (WANT_G) {
-          const float4 kb = __ldg(&kv.ks[2 * k + 1]);
-          f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
-        }
-      }
-    }
+    q = A.qs[js];
+    shift_bound(kv, q, mh, f0);
   }
-  // warp sub-box and item box (union of the warp boxes)
-  Box wb = warp_box(act, q.x, q.y, q.z, mh);
-  wb.thr += A.T_l;
-  if (lane == 0) sm.gbox[w] = wb;
-  __syncthreads();
-  if (tid == 0) {
-    Box ib = sm.gbox[0];
-    for (int k = 1; k < NWARP; ++k) {
-      const Box g = sm.gbox[k];
-      ib.lx = fminf(ib.lx, g.lx); ib.ly = fminf(ib.ly, g.ly); ib.lz = fminf(ib.lz, g.lz);
-      ib.hx = fmaxf(ib.hx, g.hx); ib.hy = fmaxf(ib.hy, g.hy); ib.hz = fmaxf(ib.hz, g.hz);
-      ib.thr = fmaxf(ib.thr, g.thr);
-    }
-    sm.ibox = ib;
-  }
-  __syncthreads();
-  const Box ibox = sm.ibox;
+  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  box.thr += A.T_l;
 
-  float Z = 0.f, M = 0.f;
-  float sgx = 0.f, sgy = 0.f, sgz = 0.f, sux = 0.f, suy = 0.f, suz = 0.f, sfx = 0.f, sfy = 0.f, sfz = 0.f;
-  float shift = mh;
-  unsigned long long cand = 0;
-  auto accum = [&](uint32_t cnt) {
-    if (nact_w == 0) return;  // warp-uniform
-    // per-warp filter against the warp's own sub-box
-    uint32_t nw = 0;
-    for (uint32_t base = 0; base < cnt; base += 32) {
-      const uint32_t k = base + lane;
-      const bool pass = (k < cnt) && within(sm.a[k], wb);
-      const uint32_t bal = __ballot_sync(~0u, pass);
-      if (pass) sm.widx[w][nw + __popc(bal & lanemask_lt())] = (uint16_t)k;
-      nw += __popc(bal);
-    }
-    __syncwarp();
-    cand += (unsigned long long)nw;
-    if (!act) return;
+  // mode 0: accumulate with `shift`; 1: exact min of the exponent; 2: count kept pairs
+  FwdAcc s = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float shift = mh, mexact = INFINITY;
+  unsigned long long cand = 0, kept = 0, kept_off = 0;
+  float4* sa = ws_a[w];
+  float4* sb = ws_b[w];
+  int* sid = ws_id[w];
+  auto run = [&](const int mode) {
+    uint32_t cnt = 0;
+    auto consume = [&]() {
+      __syncwarp();
+      if (mode == 0) cand += cnt;
+      if (act) {
+        if (mode == 0) {
 #pragma unroll 4
-    for (uint32_t i = 0; i < nw; ++i) {
-      const uint32_t k = sm.widx[w][i];
-      const float4 a = sm.a[k];
-      const float4 b = sm.b[k];
-      const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
-      const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const float wgt = ex2f(fmaf(-a.w, dd, shift));
-      Z += wgt;
-      if (WANT_G) {
-        const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x - f0)));
-        sgx = fmaf(wgt, b.y, sgx);
-        sgy = fmaf(wgt, b.z, sgy);
-        sgz = fmaf(wgt, b.w, sgz);
-        const float wbl = wgt * a.w;
-        sux = fmaf(wbl, dx, sux);
-        suy = fmaf(wbl, dy, suy);
-        suz = fmaf(wbl, dz, suz);
-        const float wbf = wbl * f;
-        sfx = fmaf(wbf, dx, sfx);
-        sfy = fmaf(wbf, dy, sfy);
-        sfz = fmaf(wbf, dz, sfz);
-        M = fmaf(wgt, f, M);
-      } else {
-        const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
-        M = fmaf(wgt, f, M);
+          for (uint32_t i = 0; i < cnt; ++i) fwd_pair<WANT_G>(q, sa[i], sb[i], shift, f0, s);
+        } else if (mode == 1) {
+          for (uint32_t i = 0; i < cnt; ++i) mexact = fminf(mexact, exponent(q, sa[i]));
+        } else {
+          for (uint32_t i = 0; i < cnt; ++i) {
+            const bool kp = exponent(q, sa[i]) - mexact <= A.T_l;
+            kept += kp ? 1ull : 0ull;
+            kept_off += (kp && sid[i] >= kv.n_nodes) ? 1ull : 0ull;
+          }
+        }
       }
-    }
+      __syncwarp();
+      cnt = 0;
+    };
+    enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      if (pass) {
+        const uint32_t slot = cnt + __popc(bal & lanemask_lt());
+        sa[slot] = a;
+        if (mode == 0) sb[slot] = __ldg(&kv.ks[2 * kp + 1]);
+        if (mode == 2) sid[slot] = __ldg(&kv.kid[kp]);
+      }
+      cnt += __popc(bal);
+      if (cnt >= WSLICE - 32) consume();
+    });
+    if (cnt) consume();
   };
-  {
-    const uint32_t n = traverse<false>(kv, ibox, sm, accum, A.lists + (size_t)item * A.list_cap, A.list_cap);
-    if (tid == 0) A.list_n[item] = n;
-  }
 
-  const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
-  if (__syncthreads_or(bad)) {
-    // exact-shift slow path: shift = min over the staged set (it contains every argmin key)
-    float mexact = INFINITY;
-    auto minpass = [&](uint32_t cnt) {
-      if (!act) return;
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const float4 a = sm.a[k];
-        const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
-        mexact = fminf(mexact, a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-      }
-    };
-    traverse<false>(kv, ibox, sm, minpass);
+  run(0);
+  const bool bad = act && !(isfinite(s.Z) && isfinite(s.M) && s.Z > 0.0f);
+  if (__any_sync(~0u, bad)) {
+    // exact-shift slow path: the warp's candidate set contains every argmin key
+    run(1);
     shift = mexact;
-    Z = M = 0.f;
-    sgx = sgy = sgz = sux = suy = suz = sfx = sfy = sfz = 0.f;
+    s = FwdAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     cand = 0;
-    traverse<false>(kv, ibox, sm, accum);
-    if (tid == 0) atomicAdd(&A.ds->overflow_items, 1u);
+    run(0);
+    if (lane == 0) atomicAdd(&A.ds->overflow_items, 1u);
   }
-
   if (A.count_kept) {
-    // diagnostic: exact per-query min over the staged set, then count pairs with e - m <= T_l
-    float mexact = INFINITY;
-    auto minpass = [&](uint32_t cnt) {
-      if (!act) return;
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const float4 a = sm.a[k];
-        const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
-        mexact = fminf(mexact, a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-      }
-    };
-    traverse<false>(kv, ibox, sm, minpass);
-    unsigned long long kept = 0, kept_off = 0;
-    auto countpass = [&](uint32_t cnt) {
-      if (!act) return;
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const float4 a = sm.a[k];
-        const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
-        const bool kp = a.w * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) - mexact <= A.T_l;
-        kept += kp ? 1ull : 0ull;
-        kept_off += (kp && sm.id[k] >= kv.n_nodes) ? 1ull : 0ull;
-      }
-    };
-    traverse<true>(kv, ibox, sm, countpass);
+    mexact = INFINITY;
+    run(1);
+    run(2);
     for (int o = 16; o > 0; o >>= 1) {
       kept += __shfl_xor_sync(~0u, kept, o);
       kept_off += __shfl_xor_sync(~0u, kept_off, o);
@@ -393,26 +292,25 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       atomicAdd(&A.ds->kept_pairs_offset, kept_off);
     }
   }
-  if (lane == 0 && nact_w > 0) atomicAdd(&A.ds->cand_pairs, cand * (unsigned long long)nact_w);
+  if (lane == 0) atomicAdd(&A.ds->cand_pairs, cand * (unsigned long long)nact);
 
   // epilogue: O, lambda, G, loss and its upstream
   float lossj = 0.0f;
   if (act) {
-    const float iz = 1.0f / Z;
-    const float O = (WANT_G ? f0 : 0.0f) + M * iz;
-    const float nlam = shift - log2f(Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
-    const int64_t js = j0 + tid;
+    const float iz = 1.0f / s.Z;
+    const float O = (WANT_G ? f0 : 0.0f) + s.M * iz;
+    const float nlam = shift - log2f(s.Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
     const int ju = A.perm[js];
     float r = 0.0f;
     float Gx = 0.f, Gy = 0.f, Gz = 0.f;
     if (WANT_G) {
       const float c2 = 2.0f * EF_LN2 * iz;
       const float Of = O - f0;
-      Gx = sgx * iz + c2 * fmaf(Of, sux, -sfx);
-      Gy = sgy * iz + c2 * fmaf(Of, suy, -sfy);
-      Gz = sgz * iz + c2 * fmaf(Of, suz, -sfz);
+      Gx = s.sgx * iz + c2 * fmaf(Of, s.sux, -s.sfx);
+      Gy = s.sgy * iz + c2 * fmaf(Of, s.suy, -s.sfy);
+      Gz = s.sgz * iz + c2 * fmaf(Of, s.suz, -s.sfz);
       A.gs[js] = make_float4(Gx, Gy, Gz, 0.f);
-      A.us[js] = make_float4(c2 * sux, c2 * suy, c2 * suz, 0.f);
+      A.us[js] = make_float4(c2 * s.sux, c2 * s.suy, c2 * s.suz, 0.f);
       if (A.G) {
         A.G[3 * (size_t)ju] = Gx;
         A.G[3 * (size_t)ju + 1] = Gy;
@@ -425,23 +323,17 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       lossj = diff * diff * A.inv_J;
     }
     if (WANT_G && A.loss_kind == EFUNC_LOSS_MSE_EIKONAL) {
-      const float n = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
-      lossj = fmaf(A.eik_lambda * (n - 1.0f) * (n - 1.0f), A.inv_J, lossj);
-      const float s = n > 0.0f ? 2.0f * A.eik_lambda * (n - 1.0f) / n * A.inv_J : 0.0f;
-      A.hs[js] = make_float4(s * Gx, s * Gy, s * Gz, 0.f);
+      const float nrm = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
+      lossj = fmaf(A.eik_lambda * (nrm - 1.0f) * (nrm - 1.0f), A.inv_J, lossj);
+      const float sc = nrm > 0.0f ? 2.0f * A.eik_lambda * (nrm - 1.0f) / nrm * A.inv_J : 0.0f;
+      A.hs[js] = make_float4(sc * Gx, sc * Gy, sc * Gz, 0.f);
     }
     A.rec[js] = make_float4(nlam, r, O, 0.f);
     if (A.O) A.O[ju] = O;
   }
   if (A.loss_kind >= EFUNC_LOSS_MSE) {
     for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
-    if (lane == 0) s_red[w] = lossj;
-    __syncthreads();
-    if (tid == 0) {
-      float t = 0.f;
-      for (int k = 0; k < NWARP; ++k) t += s_red[k];
-      A.loss_part[item] = t;
-    }
+    if (lane == 0) A.loss_part[item * NWARP + w] = lossj;
   }
 }
 
@@ -455,22 +347,23 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 // ------------------------------------------------------------------------------ backward
 template <bool EIK>
 __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
-  __shared__ SmemList sm;
-  __shared__ float4 sq[QITEM];  // x, y, z, -lambda_l
-  __shared__ float4 sv[QITEM];  // r, O, h.ubar, h.G
-  __shared__ float4 sh[EIK ? QITEM : 1];
+  __shared__ float4 sq[NWARP][32];  // x, y, z, -lambda_l
+  __shared__ float4 sv[NWARP][32];  // r, O, h.ubar, h.G
+  __shared__ float4 sh[EIK ? NWARP : 1][32];
+  __shared__ float4 ka_s[NWARP][WSLICE];
+  __shared__ float4 kb_s[NWARP][WSLICE];
+  __shared__ int kid_s[NWARP][WSLICE];
   const KeysView& kv = A.kv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t item = blockIdx.x;
   if (item >= *A.n_items) return;
   const int2 it = A.items[item];
-  const int64_t j0 = it.x;
-  const int nq = it.y;
-  const int ng = (nq + 31) / 32;
-  const bool act = tid < nq;
+  const int nact = min(32, it.y - 32 * w);
+  if (nact <= 0) return;
+  const bool act = lane < nact;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
   if (act) {
-    const int64_t js = j0 + tid;
+    const int64_t js = (int64_t)it.x + 32 * w + lane;
     q = A.qs[js];
     const float4 rc = A.rec[js];
     const int ju = A.perm[js];
@@ -483,163 +376,161 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
       const float4 G = A.gs[js], ub = A.us[js];
       hub = hv.x * ub.x + hv.y * ub.y + hv.z * ub.z;
       T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
-      sh[tid] = hv;
+      sh[w][lane] = hv;
     }
     q.w = rc.x;
-    sq[tid] = q;
-    sv[tid] = make_float4(r, rc.z, hub, T);
+    sq[w][lane] = q;
+    sv[w][lane] = make_float4(r, rc.z, hub, T);
   }
-  // query-group boxes with the exact threshold max_j(-lambda_l) + T_l (pairs with p < 2^-T_l skip)
-  Box gb = warp_box(act, q.x, q.y, q.z, q.w);
-  gb.thr += A.T_l;
-  if (lane == 0) sm.gbox[w] = gb;
-  __syncthreads();
-  if (tid == 0) {
-    Box ib = sm.gbox[0];
-    for (int k = 1; k < ng; ++k) {
-      const Box g = sm.gbox[k];
-      ib.lx = fminf(ib.lx, g.lx); ib.ly = fminf(ib.ly, g.ly); ib.lz = fminf(ib.lz, g.lz);
-      ib.hx = fmaxf(ib.hx, g.hx); ib.hy = fmaxf(ib.hy, g.hy); ib.hz = fmaxf(ib.hz, g.hz);
-      ib.thr = fmaxf(ib.thr, g.thr);
-    }
-    sm.ibox = ib;
-  }
-  __syncthreads();
-  const Box ibox = sm.ibox;
+  // group box with the exact threshold max_j(-lambda_l) + T_l
+  Box box = warp_box(act, q.x, q.y, q.z, q.w);
+  box.thr += A.T_l;
+  __syncwarp();
+  const float4* Q = sq[w];
+  const float4* V = sv[w];
+  const float4* H = sh[EIK ? w : 0];
+  float4* sa = ka_s[w];
+  float4* sb = kb_s[w];
+  int* sid = kid_s[w];
+  float* gpad = A.gpad;
+  const int n_nodes = kv.n_nodes;
 
-  auto proc = [&](uint32_t cnt) {
-    // 1. mask of query groups within reach, histogram over masks
-    if (tid < 16) sm.hist[tid] = 0;
-    __syncthreads();
-    for (uint32_t k = tid; k < cnt; k += NTHREADS) {
-      const float4 a = sm.a[k];
-      uint32_t m = 0;
-      for (int g = 0; g < ng; ++g) m |= within(a, sm.gbox[g]) ? (1u << g) : 0u;
-      sm.mask[k] = (uint8_t)m;
-      if (m) atomicAdd(&sm.hist[m], 1u);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t o = 0;
-      for (int m = 0; m < 16; ++m) {
-        sm.boff[m] = o;
-        o += sm.hist[m];
-      }
-      sm.boff[16] = o;
-    }
-    __syncthreads();
-    const uint32_t nz = sm.boff[16];
-    for (uint32_t k = tid; k < cnt; k += NTHREADS) {
-      const uint32_t m = sm.mask[k];
-      if (m) sm.widx[0][atomicAdd(&sm.boff[m], 1u)] = (uint16_t)k;
-    }
-    __syncthreads();
-    // 2. lanes = keys (mask-bucketed), loop over the queries of the groups in the mask
-    for (uint32_t i = tid; i < nz; i += NTHREADS) {
-      const uint32_t k = sm.widx[0][i];
-      const uint32_t m = sm.mask[k];
-      const float4 a = sm.a[k];
-      const float4 b = sm.b[k];
-      const int id = sm.id[k];
-      const float beta = a.w * EF_LN2;
-      float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
-      float phx = 0.f, phy = 0.f, phz = 0.f, pdx = 0.f, pdy = 0.f, pdz = 0.f;  // EIK only
-      for (int g = 0; g < ng; ++g) {
-        if (!((m >> g) & 1u)) continue;
-        const int jend = min(nq, 32 * g + 32);
+  // lanes = keys: lane i takes staged key head + i, loops over the group's queries
+  auto consume = [&](uint32_t head, uint32_t count) {
+    __syncwarp();
+    const bool has = (uint32_t)lane < count;
+    const uint32_t slot = (head + lane) % WSLICE;
+    const float4 a = has ? sa[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = has ? sb[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int id = has ? sid[slot] : 0;
+    __syncwarp();
+    if (!has) return;
+    const float beta = a.w * EF_LN2;
+    float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
+    float phx = 0.f, phy = 0.f, phz = 0.f, pdx = 0.f, pdy = 0.f, pdz = 0.f;  // EIK only
 #pragma unroll 4
-        for (int j = 32 * g; j < jend; ++j) {
-          const float4 P = sq[j];
-          const float4 V = sv[j];
-          const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
-          const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-          const float p = ex2f(fmaf(-a.w, dd, P.w));
-          const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
-          const float del = f - V.y;
-          if (!EIK) {
-            // Alg. 2: dO/dc = p, dO/dg = p d, dO/ds = -p a (f - O), dO/dk = p(-g + 2 beta d (f - O))
-            const float t = V.x * p;
-            const float u = t * del;
-            sc += t;
-            sgx = fmaf(t, dx, sgx);
-            sgy = fmaf(t, dy, sgy);
-            sgz = fmaf(t, dz, sgz);
-            ss = fmaf(u, dd, ss);
-            sdx = fmaf(u, dx, sdx);
-            sdy = fmaf(u, dy, sdy);
-            sdz = fmaf(u, dz, sdz);
-          } else {
-            // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
-            const float4 H = sh[j];
-            const float hd = fmaf(H.x, dx, fmaf(H.y, dy, H.z * dz));
-            const float hu = 2.0f * beta * hd;
-            const float hg = fmaf(H.x, b.y, fmaf(H.y, b.z, H.z * b.w));
-            const float tt = fmaf(-hu, del, hg);
-            const float alpha = V.x + V.z - hu;
-            const float gam = fmaf(V.x + V.z, del, tt - V.w);
-            const float pa = p * alpha;
-            sc += pa;
-            sgx = fmaf(pa, dx, sgx);
-            sgy = fmaf(pa, dy, sgy);
-            sgz = fmaf(pa, dz, sgz);
-            phx = fmaf(p, H.x, phx);
-            phy = fmaf(p, H.y, phy);
-            phz = fmaf(p, H.z, phz);
-            ss = fmaf(p, fmaf(beta * dd, gam, hu * del), ss);
-            const float pg = p * gam;
-            sdx = fmaf(pg, dx, sdx);
-            sdy = fmaf(pg, dy, sdy);
-            sdz = fmaf(pg, dz, sdz);
-            const float pdel = p * del;
-            pdx = fmaf(pdel, H.x, pdx);
-            pdy = fmaf(pdel, H.y, pdy);
-            pdz = fmaf(pdel, H.z, pdz);
-          }
-        }
-      }
-      float dsv, dgx, dgy, dgz, dkx, dky, dkz;
+    for (int j = 0; j < nact; ++j) {
+      const float4 P = Q[j];
+      const float4 U = V[j];
+      const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
+      const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float p = ex2f(fmaf(-a.w, dd, P.w));
+      const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+      const float del = f - U.y;
       if (!EIK) {
-        dsv = -beta * ss;
-        dgx = sgx; dgy = sgy; dgz = sgz;
+        // Alg. 2: dO/dc = p, dO/dg = p d, dO/ds = -p a (f - O), dO/dk = p(-g + 2 beta d (f - O))
+        const float t = U.x * p;
+        const float u = t * del;
+        sc += t;
+        sgx = fmaf(t, dx, sgx);
+        sgy = fmaf(t, dy, sgy);
+        sgz = fmaf(t, dz, sgz);
+        ss = fmaf(u, dd, ss);
+        sdx = fmaf(u, dx, sdx);
+        sdy = fmaf(u, dy, sdy);
+        sdz = fmaf(u, dz, sdz);
+      } else {
+        // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
+        const float4 h = H[j];
+        const float hd = fmaf(h.x, dx, fmaf(h.y, dy, h.z * dz));
+        const float hu = 2.0f * beta * hd;
+        const float hg = fmaf(h.x, b.y, fmaf(h.y, b.z, h.z * b.w));
+        const float tt = fmaf(-hu, del, hg);
+        const float alpha = U.x + U.z - hu;
+        const float gam = fmaf(U.x + U.z, del, tt - U.w);
+        const float pa = p * alpha;
+        sc += pa;
+        sgx = fmaf(pa, dx, sgx);
+        sgy = fmaf(pa, dy, sgy);
+        sgz = fmaf(pa, dz, sgz);
+        phx = fmaf(p, h.x, phx);
+        phy = fmaf(p, h.y, phy);
+        phz = fmaf(p, h.z, phz);
+        ss = fmaf(p, fmaf(beta * dd, gam, hu * del), ss);
+        const float pg = p * gam;
+        sdx = fmaf(pg, dx, sdx);
+        sdy = fmaf(pg, dy, sdy);
+        sdz = fmaf(pg, dz, sdz);
+        const float pdel = p * del;
+        pdx = fmaf(pdel, h.x, pdx);
+        pdy = fmaf(pdel, h.y, pdy);
+        pdz = fmaf(pdel, h.z, pdz);
+      }
+    }
+    float dsv, dgx, dgy, dgz;
+    if (!EIK) {
+      dsv = -beta * ss;
+      dgx = sgx; dgy = sgy; dgz = sgz;
+    } else {
+      dsv = -ss;
+      dgx = sgx + phx; dgy = sgy + phy; dgz = sgz + phz;
+    }
+    // padded gradient: node n -> 16 floats {s0,c0,g0x,g0y | g0z,-,-,- | dx,dy,dz,s1 | c1,g1x,g1y,g1z}
+    if (id < n_nodes) {
+      float* gp = gpad + (size_t)id * 16;
+      red_v4(gp, dsv, sc, dgx, dgy);
+      atomicAdd(gp + 4, dgz);
+    } else {
+      float dkx, dky, dkz;
+      if (!EIK) {
         dkx = fmaf(-b.y, sc, 2.0f * beta * sdx);
         dky = fmaf(-b.z, sc, 2.0f * beta * sdy);
         dkz = fmaf(-b.w, sc, 2.0f * beta * sdz);
       } else {
-        dsv = -ss;
-        dgx = sgx + phx; dgy = sgy + phy; dgz = sgz + phz;
         dkx = fmaf(-b.y, sc, 2.0f * beta * (sdx + pdx));
         dky = fmaf(-b.z, sc, 2.0f * beta * (sdy + pdy));
         dkz = fmaf(-b.w, sc, 2.0f * beta * (sdz + pdz));
       }
-      if (id < kv.n_nodes) {
-        float* gp = A.grad + (size_t)id * EF_NCH;
-        atomicAdd(gp + 0, dsv);
-        atomicAdd(gp + 1, sc);
-        atomicAdd(gp + 2, dgx);
-        atomicAdd(gp + 3, dgy);
-        atomicAdd(gp + 4, dgz);
-      } else {
-        float* gp = A.grad + (size_t)(id - kv.n_nodes) * EF_NCH;
-        atomicAdd(gp + 5, dkx);
-        atomicAdd(gp + 6, dky);
-        atomicAdd(gp + 7, dkz);
-        atomicAdd(gp + 8, dsv);
-        atomicAdd(gp + 9, sc);
-        atomicAdd(gp + 10, dgx);
-        atomicAdd(gp + 11, dgy);
-        atomicAdd(gp + 12, dgz);
-      }
+      float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
+      red_v4(gp, dkx, dky, dkz, dsv);
+      red_v4(gp + 4, sc, dgx, dgy, dgz);
     }
   };
-  const uint32_t ln = A.list_n[item];
-  if (ln <= A.list_cap) stage_list(kv, A.lists + (size_t)item * A.list_cap, ln, sm, proc);
-  else traverse<true>(kv, ibox, sm, proc);
+
+  uint32_t head = 0, cnt = 0;  // ring buffer of staged keys
+  enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) {
+      const uint32_t slot = (head + cnt + __popc(bal & lanemask_lt())) % WSLICE;
+      sa[slot] = a;
+      sb[slot] = __ldg(&kv.ks[2 * kp + 1]);
+      sid[slot] = __ldg(&kv.kid[kp]);
+    }
+    cnt += __popc(bal);
+    if (cnt >= 32) {
+      consume(head, 32);
+      head = (head + 32) % WSLICE;
+      cnt -= 32;
+    }
+  });
+  if (cnt) consume(head, cnt);
 }
 
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   if (a.eik) k_backward<true><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
   else k_backward<false><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
+  return 1;
+}
+
+// grad[n][13] += padded gradient (channel map above); zero the padded buffer for the next call
+__global__ void k_fold(float* __restrict__ gpad, float* __restrict__ grad, int n_nodes) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    float4* p = reinterpret_cast<float4*>(gpad + (size_t)n * 16);
+    const float4 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
+    float* g = grad + (size_t)n * EF_NCH;
+    g[0] += v0.x; g[1] += v0.y; g[2] += v0.z; g[3] += v0.w; g[4] += v1.x;
+    g[5] += v2.x; g[6] += v2.y; g[7] += v2.z; g[8] += v2.w;
+    g[9] += v3.x; g[10] += v3.y; g[11] += v3.z; g[12] += v3.w;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    p[0] = z; p[1] = z; p[2] = z; p[3] = z;
+  }
+}
+
+int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s) {
+  int blocks = (n_nodes + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_fold<<<blocks, 256, 0, s>>>(gpad, grad, n_nodes);
   return 1;
 }
 
