@@ -102,6 +102,9 @@ typedef struct {
   int32_t overflow_items;    /* items that took the exact-shift slow path */
   double kept_pairs_offset;  /* kept pairs whose key is in the offset bank (counting mode) */
   int64_t launches;          /* kernels launched by this handle since creation */
+  int64_t list_builds;       /* brick candidate-list builds since creation (Verlet skin) */
+  int64_t list_entries;      /* entries of the current brick lists */
+  int64_t list_overflow;     /* bricks whose list overflowed (their items enumerate directly) */
 } efunc_stats;
 
 /* efunc_create — allocate a handle on cfg->device and upload theta.

@@ -60,18 +60,28 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
-int query_bits(int64_t J) {
-  // target ~4 queries per Morton bin
-  double t = std::log2(std::fmax((double)J / 4.0, 1.0)) / 3.0;
-  int b = (int)std::ceil(t);
-  if (b < 1) b = 1;
-  if (b > MAX_QBITS) b = MAX_QBITS;
-  return b;
-}
-
 float cutoff_log2(const efunc_config& c) {
   if (!(c.cutoff_T > 0.0f) || std::isinf(c.cutoff_T)) return INFINITY;
   return c.cutoff_T * EF_LOG2E;
+}
+
+// Brick edge (in lattice cells) ~ half the search radius at the paper's init (beta = e^7,
+// PAPER.md:L908): rho^2 = 3h^2/4 + T/beta. Dense mode (T = inf): one brick for everything.
+BrickGeom brick_geom(const efunc_config& cfg, int NC, float h) {
+  BrickGeom g;
+  if (!(cfg.cutoff_T > 0.0f) || std::isinf(cfg.cutoff_T)) {
+    g.B = NC;
+  } else {
+    const double rho = std::sqrt(0.75 * h * h + cfg.cutoff_T / std::exp(7.0));
+    int B = 1;
+    while (2 * B * h <= 0.5 * rho && 2 * B <= NC) B *= 2;  // largest power of 2 with B h <= rho / 2
+    g.B = B;
+  }
+  g.nb = (NC + g.B - 1) / g.B;
+  g.bits = 0;
+  while ((1 << g.bits) < g.nb) ++g.bits;
+  g.n_codes = 1u << (3 * g.bits);
+  return g;
 }
 
 KeysView keys_view(efunc_t* h) {
@@ -84,7 +94,11 @@ KeysView keys_view(efunc_t* h) {
   kv.R = h->R;
   kv.NC = h->NC;
   kv.inv_h = h->inv_h;
+  kv.h = h->h;
   kv.n_nodes = h->n_nodes;
+  kv.bl_pool = h->bl_pool;
+  kv.bl_off = h->bl_off;
+  kv.bl_n = h->bl_n;
   return kv;
 }
 
@@ -97,54 +111,34 @@ efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
   return EFUNC_OK;
 }
 
-efunc_status rebuild_keys(efunc_t* h, cudaStream_t s) {
+// S0 + key binning + brick lists. force = 1: theta was replaced wholesale, rebuild the lists
+// regardless of the Verlet skin.
+efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(h->cell_fill, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
-  h->launches += launch_prep_keys(h->theta, h->R, h->key_raw, h->key_cell, h->cell_count, h->ds, s);
+  if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
+  const float skin = SKIN_H * h->h;
+  h->launches += launch_prep_keys(h->theta, h->R, h->key_raw, h->key_cell, h->cell_count, h->key_ref,
+                                  skin * skin, SKIN_MU, h->ds, s);
   h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s);
   h->launches += launch_counting_sort(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_tmp, h->key_order, s);
   h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
+  // per-brick candidate lists for the next forward/backward (query independent)
+  h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
+                                    h->bl_off, h->bl_n, h->ds, s);
+  h->launches += launch_list_snapshot(h->key_raw, h->key_ref, h->n_keys, h->ds, s);
+  CK(cudaMemsetAsync(&h->ds->lists_invalid, 0, sizeof(uint32_t), s));
   CK(cudaGetLastError());
   h->have_fwd = 0;
   return EFUNC_OK;
 }
 
-// Morton bits per axis of the coarse cells that work items may not straddle (edge ~4h).
-int coarse_bits(const efunc_t* h, int bits) {
-  int c = (int)std::lround(std::log2(std::fmax((h->R - 1) / 4.0, 1.0)));
-  if (c < 0) c = 0;
-  if (c > bits) c = bits;
-  return c;
-}
-
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
-  const int bits = query_bits(J);
-  const uint32_t nbins = 1u << (3 * bits);
-  if (nbins + 1 > h->nbins_cap) {
-    dfree(h->bin_count);
-    dfree(h->bin_start);
-    dfree(h->bin_fill);
-    CK(dalloc(&h->bin_count, nbins + 1));
-    CK(dalloc(&h->bin_start, nbins + 1));
-    CK(dalloc(&h->bin_fill, nbins + 1));
-    h->nbins_cap = nbins + 1;
-    RET(ensure_scan_tmp(h, nbins + 1));
-  }
-  const int cb = coarse_bits(h, bits);
-  const uint32_t n_coarse = 1u << (3 * cb);
-  if (n_coarse + 1 > h->coarse_cap) {
-    dfree(h->item_cnt);
-    dfree(h->item_off);
-    CK(dalloc(&h->item_cnt, n_coarse + 1));
-    CK(dalloc(&h->item_off, n_coarse + 1));
-    h->coarse_cap = n_coarse + 1;
-  }
-  const int64_t bound = (J + QITEM - 1) / QITEM + n_coarse;
+  const int64_t bound = (J + QW - 1) / QW + h->bg.n_codes + 1;
   if (bound > h->items_cap) {
-    dfree(h->boxes); dfree(h->loss_part); dfree(h->items);
-    CK(dalloc(&h->boxes, bound));
-    CK(dalloc(&h->loss_part, 4 * bound));
+    dfree(h->loss_part); dfree(h->items);
+    CK(dalloc(&h->loss_part, bound));
     CK(dalloc(&h->items, bound));
     h->items_cap = bound;
   }
@@ -172,8 +166,9 @@ void free_all(efunc_t* h) {
   dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad);
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
-  dfree(h->boxes); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
+  dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
+  dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -195,27 +190,24 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
     return EFUNC_OK;
   }
   RET(ensure_queries(h, J));
-  const int bits = query_bits(J);
-  const uint32_t nbins = 1u << (3 * bits);
+  const uint32_t nb = h->bg.n_codes;             // bricks
+  const uint32_t nbins = nb * QSUB + 1;          // octant bins + the out-of-domain bin
   CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
-  CK(cudaMemsetAsync(reinterpret_cast<char*>(h->ds) + 8, 0, sizeof(DevScalars) - 8, s));
+  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
   const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
-  h->launches += launch_query_bins(q, o_used, J, bits, h->q_bin, h->bin_count, h->ds, s);
+  h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
   h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
   h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
-  // work items: balanced runs of <= QITEM sorted queries inside each coarse Morton cell
-  const int cb = coarse_bits(h, bits);
-  const uint32_t n_coarse = 1u << (3 * cb);
-  const int shift = 3 * (bits - cb);
-  h->launches += launch_items_count(h->bin_start, shift, n_coarse, h->item_cnt, s);
-  h->launches += launch_scan_u32(h->item_cnt, h->item_off, n_coarse + 1, h->scan_tmp, s);
-  h->launches += launch_items_write(h->bin_start, shift, n_coarse, h->item_off, h->items, s);
-  const int64_t items = (J + QITEM - 1) / QITEM + n_coarse;  // launch bound; kernels read the count
-  const uint32_t* n_items = h->item_off + n_coarse;
+  // work items: balanced runs of <= QW sorted queries of one brick
+  h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
+  h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
+  h->launches += launch_items_write(h->bin_start, nb, h->item_off, h->items, s);
+  const int64_t items = (J + QW - 1) / QW + nb + 1;  // launch bound; kernels read the count
+  const uint32_t* n_items = h->item_off + (nb + 1);
   h->fwd_items_bound = items;
-  h->fwd_n_coarse = n_coarse;
   FwdArgs a;
   a.kv = keys_view(h);
   a.qs = h->qs;
@@ -234,12 +226,11 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   a.gs = h->gs;
   a.us = h->us;
   a.hs = h->hs;
-  a.boxes = h->boxes;
   a.loss_part = h->loss_part;
   a.ds = h->ds;
   a.count_kept = h->count_kept;
   h->launches += launch_forward(a, want_g, items, s);
-  if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, 4, loss_out, s);
+  if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, 1, loss_out, s);
   else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   CK(cudaGetLastError());
   if (h->cfg.sync_checks) {
@@ -272,7 +263,7 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.perm = h->perm;
   b.J = h->fwd_J;
   b.items = h->items;
-  b.n_items = h->item_off + h->fwd_n_coarse;
+  b.n_items = h->item_off + (h->bg.n_codes + 1);
   b.T_l = cutoff_log2(h->cfg);
   b.gpad = h->gpad;
   b.rec = h->rec;
@@ -281,7 +272,6 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.hs = h->hs;
   b.dL_dO = dL_dO;
   b.dL_dG = dL_dG;
-  b.boxes = h->boxes;
   b.grad = grad;
   b.eik = eik;
   h->launches += launch_backward(b, h->fwd_items_bound, s);
@@ -355,6 +345,19 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->cell_start, h->n_cells + 1));
     CK(dalloc(&h->cell_fill, h->n_cells + 1));
     CK(dalloc(&h->ds, 1));
+    h->bg = brick_geom(h->cfg, h->NC, h->h);
+    const size_t nbins = (size_t)h->bg.n_codes * QSUB + 1;
+    CK(dalloc(&h->bl_off, h->bg.n_codes));
+    CK(dalloc(&h->bl_n, h->bg.n_codes));
+    const double pool = (double)h->n_keys * POOL_PER_KEY;
+    h->bl_pool_cap = (uint32_t)std::fmin(pool, 4.0e9);
+    CK(dalloc(&h->bl_pool, h->bl_pool_cap));
+    CK(dalloc(&h->bin_count, nbins + 1));
+    CK(dalloc(&h->bin_start, nbins + 1));
+    CK(dalloc(&h->bin_fill, nbins + 1));
+    CK(dalloc(&h->item_cnt, nbins + 1));
+    CK(dalloc(&h->item_off, nbins + 1));
+    RET(ensure_scan_tmp(h, nbins + 1));
     CK(dalloc(&h->gpad, (size_t)h->n_nodes * 16));
     CK(cudaMemset(h->gpad, 0, sizeof(float) * (size_t)h->n_nodes * 16));
     CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
@@ -363,7 +366,9 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     else CK(cudaMemset(h->theta, 0, np * sizeof(float)));
     CK(cudaMemset(h->m, 0, np * sizeof(float)));
     CK(cudaMemset(h->v, 0, np * sizeof(float)));
-    RET(rebuild_keys(h, 0));
+    CK(dalloc(&h->key_ref, h->n_keys));
+    CK(cudaMemset(h->key_ref, 0, sizeof(float4) * (size_t)h->n_keys));
+    RET(rebuild_keys(h, 0, 1));
     CK(cudaDeviceSynchronize());
     return EFUNC_OK;
   }();
@@ -461,7 +466,7 @@ efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, flo
   cudaStream_t s = (cudaStream_t)stream;
   h->launches += launch_mean_shift(h->theta, h->R, surf, N, bandwidth, s);
   CK(cudaGetLastError());
-  return rebuild_keys(h, s);
+  return rebuild_keys(h, s, 1);
 }
 
 efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream) {
@@ -480,7 +485,7 @@ efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, v
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
   CK(cudaMemcpyAsync(h->theta, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-  RET(rebuild_keys(h, s));
+  RET(rebuild_keys(h, s, 1));
   CK(cudaStreamSynchronize(s));
   return EFUNC_OK;
 }
@@ -524,7 +529,7 @@ efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
   CK(cudaMemcpy(&d, h->ds, sizeof(d), cudaMemcpyDeviceToHost));
   out->J = h->fwd_J;
   uint32_t ni = 0;
-  if (h->fwd_J > 0) CK(cudaMemcpy(&ni, h->item_off + h->fwd_n_coarse, sizeof(ni), cudaMemcpyDeviceToHost));
+  if (h->fwd_J > 0) CK(cudaMemcpy(&ni, h->item_off + (h->bg.n_codes + 1), sizeof(ni), cudaMemcpyDeviceToHost));
   out->items = ni;
   out->candidate_pairs = (double)d.cand_pairs;
   out->kept_pairs = (double)d.kept_pairs;
@@ -533,6 +538,9 @@ efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
   out->overflow_items = (int32_t)d.overflow_items;
   out->kept_pairs_offset = (double)d.kept_pairs_offset;
   out->launches = h->launches;
+  out->list_builds = d.list_builds;
+  out->list_entries = d.pool_used;
+  out->list_overflow = d.ovf_last;
   return EFUNC_OK;
 }
 

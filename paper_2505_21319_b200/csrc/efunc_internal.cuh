@@ -2,15 +2,18 @@
 //
 // Data layout in HBM:
 //   theta / m / v / grad : float [R^3][13]  (ABI layout, node-major)
+//   gpad                 : float [R^3][16]  padded gradient accumulator (red.v4 targets)
 //   key record (32 B)    : float4 a = {x, y, z, bl}, float4 b = {c, gx, gy, gz},
 //                          bl = beta * log2(e)  (exponents are evaluated in base 2)
 //                          key id i < R^3: grid bank node i; i >= R^3: offset bank node i-R^3
 //   key_raw              : [2R^3] records in key-id order (grid bank = lattice order)
 //   key_sorted           : [2R^3] records sorted by lattice cell (x fastest), stable by key id
 //   cell_start           : [(R-1)^3 + 1] exclusive prefix of keys per cell
-//   queries (per forward): qs float4 {x,y,z,o} Morton-sorted, perm[sorted] = user index,
-//                          rec float4 {-lambda_j*log2e, dL/dO_j, O_j, 0} (sorted order)
-//   work item            : QITEM consecutive sorted queries; box = AABB + max shift bound
+//   brick lists          : per brick (B^3 lattice cells, Morton-coded) the sorted-key positions
+//                          of every key that can reach a query inside the brick (pool + off/n)
+//   queries (per forward): qs float4 {x,y,z,o} sorted by brick (Morton), stable by index;
+//                          perm[sorted] = user index; rec float4 {-lambda_j log2e, dL/dO_j, O_j, 0}
+//   work item            : <= QW consecutive sorted queries of one brick (one warp)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,10 +27,15 @@
 
 namespace ef {
 
-constexpr int QITEM = 128;        // queries per work item == forward/backward CTA size
-constexpr int NTHREADS = 128;
-constexpr int LCAP = 512;         // candidate keys staged in shared memory per chunk
-constexpr int MAX_QBITS = 7;      // Morton bits per axis for query binning
+constexpr int QW = 32;              // queries per work item (one warp)
+constexpr int NTHREADS = 128;       // 4 independent warps per CTA
+constexpr int NWARP = NTHREADS / 32;
+constexpr int BL_CAP = 4096;        // max staged list length per brick (longer: fallback)
+constexpr uint32_t BL_OVERFLOW = 0xffffffffu;
+constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
+constexpr uint32_t QSUB = 8;        // query bins per brick (octants)
+constexpr float SKIN_H = 0.25f;     // Verlet skin of the brick lists, in lattice spacings
+constexpr float SKIN_MU = 0.05f;    // allowed relative drift of beta between list builds
 
 struct KeysView {
   const float4* ks;        // sorted records, 2 float4 per key (a at 2k, b at 2k+1)
@@ -37,19 +45,25 @@ struct KeysView {
   const float* bl_min;     // device scalar: min bl over all keys
   int R, NC;               // NC = R-1 cells per axis
   float inv_h;             // 1/h, h = 2/(R-1)
+  float h;
   int n_nodes;
-};
-
-struct ItemBox {
-  float4 lo;   // x,y,z, thr (log2-units threshold mh_max + T_l; +inf = dense)
-  float4 hi;   // x,y,z, unused
+  // brick lists
+  const uint32_t* bl_pool;
+  const uint32_t* bl_off;
+  const uint32_t* bl_n;    // BL_OVERFLOW: enumerate instead
 };
 
 struct DevScalars {
   float bl_min;            // as float; written via atomicMin on its bits (bl > 0)
   uint32_t nonfinite;
   uint32_t overflow_items;
-  uint32_t pad;
+  uint32_t pool_top;       // brick-list pool allocation cursor
+  uint32_t lists_invalid;  // 1: the brick lists must be rebuilt (skin exceeded / new theta)
+  uint32_t list_builds;    // number of brick-list builds (diagnostics)
+  uint32_t ovf_count;      // bricks overflowed in the running build
+  uint32_t pool_used;      // entries of the last completed build
+  uint32_t ovf_last;       // overflowed bricks of the last completed build
+  uint32_t pad2;
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
@@ -60,7 +74,7 @@ struct FwdArgs {
   const float4* qs;       // sorted queries {x,y,z,o}
   const int* perm;        // sorted -> user index
   int64_t J;
-  const int2* items;      // work items {first sorted query, count}
+  const int4* items;      // work items {first sorted query, count, brick (-1: outside), 0}
   const uint32_t* n_items;  // device count (grid is launched with an upper bound)
   float T_l;              // cutoff in log2 units (inf = dense)
   // loss
@@ -74,7 +88,6 @@ struct FwdArgs {
   float4* gs;             // sorted G (if WANT_G)
   float4* us;             // sorted ubar (if WANT_G)
   float4* hs;             // sorted fused Eikonal upstream h (if loss eikonal)
-  ItemBox* boxes;         // per item
   float* loss_part;       // per item partial loss
   DevScalars* ds;
   int count_kept;
@@ -85,7 +98,7 @@ struct BwdArgs {
   const float4* qs;
   const int* perm;
   int64_t J;
-  const int2* items;
+  const int4* items;
   const uint32_t* n_items;
   float T_l;              // cutoff in log2 units (inf = dense)
   const float4* rec;
@@ -94,38 +107,49 @@ struct BwdArgs {
   const float4* hs;       // fused h (sorted) or null
   const float* dL_dO;     // user order or null (use rec.y)
   const float* dL_dG;     // user order [J*3] or null
-  const ItemBox* boxes;
   float* grad;            // [R^3][13] +=
   int eik;                // 1: add the dL/dG terms
   float* gpad;            // [R^3][16] padded accumulation buffer (zero on entry, zeroed by k_fold)
 };
 
+struct BrickGeom {
+  int B;          // lattice cells per brick edge
+  int nb;         // bricks per axis
+  int bits;       // Morton bits per axis (2^bits >= nb)
+  uint32_t n_codes;  // 2^(3 bits)
+};
+
 // ---------------------------------------------------------------- launchers (host)
-int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell,
-                      uint32_t* cell_count, DevScalars* ds, cudaStream_t s);
+int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+                     const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s);
+int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, DevScalars* ds,
+                         cudaStream_t s);
 int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp,
-                     cudaStream_t s);
+                    cudaStream_t s);
 int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start,
-                          uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s);
+                         uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s);
 int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted,
-                        int* kid, uint32_t n, cudaStream_t s);
-int launch_query_bins(const float* q, const float* o, int64_t J, int bits, uint32_t* bins,
-                       uint32_t* count, DevScalars* ds, cudaStream_t s);
+                       int* kid, uint32_t n, cudaStream_t s);
+int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool,
+                       uint32_t pool_cap, uint32_t* off, uint32_t* n, DevScalars* ds,
+                       cudaStream_t s);
+int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom& bg, int NC,
+                      float inv_h, uint32_t* bins, uint32_t* count, DevScalars* ds,
+                      cudaStream_t s);
 int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
-                           float4* qs, int* perm, cudaStream_t s);
+                          float4* qs, int* perm, cudaStream_t s);
+int launch_items_count(const uint32_t* bin_start, uint32_t nbins, uint32_t* cnt, cudaStream_t s);
+int launch_items_write(const uint32_t* bin_start, uint32_t nbins, const uint32_t* off, int4* items,
+                       cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
-int launch_items_count(const uint32_t* bin_start, int shift, uint32_t n_coarse, uint32_t* cnt,
-                       cudaStream_t s);
-int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, const uint32_t* off,
-                       int2* items, cudaStream_t s);
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay,
                  float omb1, float b2, float omb2, float eps, uint32_t mask, float step_size,
                  float sqrt_bc2, cudaStream_t s);
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
-                       cudaStream_t s);
+                      cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
 
 }  // namespace ef
@@ -135,6 +159,7 @@ struct efunc {
   efunc_config cfg;
   int R = 0, n_nodes = 0, n_keys = 0, NC = 0, n_cells = 0;
   float h = 0.f, inv_h = 0.f;
+  ef::BrickGeom bg{};
   // parameters + optimizer state
   float* theta = nullptr;
   float* m = nullptr;
@@ -154,13 +179,21 @@ struct efunc {
   size_t scan_tmp_cap = 0;
   ef::DevScalars* ds = nullptr;
   float* fit_grad = nullptr;
+  float* gpad = nullptr;            // [R^3][16] padded gradient accumulator (kept zero between calls)
+  // brick lists
+  uint32_t* bl_pool = nullptr;
+  uint32_t bl_pool_cap = 0;
+  uint32_t* bl_off = nullptr;
+  uint32_t* bl_n = nullptr;
+  float4* key_ref = nullptr;        // [2R^3] key {x,y,z,bl} at the last list build
   // queries
   int64_t J_cap = 0;
-  uint32_t nbins_cap = 0;
   uint32_t* q_bin = nullptr;
-  uint32_t* bin_count = nullptr;
+  uint32_t* bin_count = nullptr;    // nbins + 1
   uint32_t* bin_start = nullptr;
   uint32_t* bin_fill = nullptr;
+  uint32_t* item_cnt = nullptr;
+  uint32_t* item_off = nullptr;     // item_off[nbins] = item count
   uint32_t* q_tmp = nullptr;
   uint32_t* q_order = nullptr;
   float4* qs = nullptr;
@@ -169,16 +202,10 @@ struct efunc {
   float4* gs = nullptr;
   float4* us = nullptr;
   float4* hs = nullptr;
-  ef::ItemBox* boxes = nullptr;
   float* loss_part = nullptr;
   int64_t items_cap = 0;
-  int2* items = nullptr;          // [items bound]
-  float* gpad = nullptr;          // [R^3][16] padded gradient accumulator (kept zero between calls)
-  uint32_t* item_cnt = nullptr;   // [coarse cells + 1]
-  uint32_t* item_off = nullptr;   // [coarse cells + 1]; item_off[n_coarse] = item count
-  uint32_t coarse_cap = 0;
+  int4* items = nullptr;            // [items bound]
   int64_t fwd_items_bound = 0;
-  uint32_t fwd_n_coarse = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;
   float* io_loss = nullptr;

@@ -16,13 +16,16 @@ __device__ __forceinline__ int cell_clamp(float p, float inv_h, int NC) {
 }
 
 // ------------------------------------------------------------------------------ S0
+// Also checks the brick lists' Verlet skin: a key that moved more than skin from its position at
+// the last list build, or whose bl left [ref/(1+mu), ref*(1+mu)], invalidates the lists.
 __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __restrict__ key_raw,
                             uint32_t* __restrict__ key_cell, uint32_t* __restrict__ cell_count,
-                            DevScalars* ds) {
+                            const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
   const int N = R * R * R;
   const int NC = R - 1;
   const float inv_h = (float)((R - 1) / 2.0);
   float local_min = INFINITY;
+  bool moved = false;
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int x = n % R, y = (n / R) % R, z = n / (R * R);
     // lattice k(i) = float32(-1 + 2 i/(R-1))  (reading R-2), evaluated in double
@@ -46,19 +49,48 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
     atomicAdd(&cell_count[c0], 1u);
     atomicAdd(&cell_count[c1], 1u);
     local_min = fminf(local_min, fminf(bl0, bl1));
+    const float4 r0 = key_ref[n], r1 = key_ref[N + n];
+    const float ex = px - r1.x, ey = py - r1.y, ez = pz - r1.z;
+    moved |= fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > skin2;
+    moved |= !(bl0 <= r0.w * (1.0f + mu) && bl0 * (1.0f + mu) >= r0.w);
+    moved |= !(bl1 <= r1.w * (1.0f + mu) && bl1 * (1.0f + mu) >= r1.w);
   }
   // bl > 0: the IEEE bit pattern orders like the value
   for (int o = 16; o > 0; o >>= 1) local_min = fminf(local_min, __shfl_xor_sync(~0u, local_min, o));
   if ((threadIdx.x & 31) == 0 && local_min < INFINITY)
     atomicMin(reinterpret_cast<unsigned int*>(&ds->bl_min), __float_as_uint(local_min));
+  if (__any_sync(~0u, moved) && (threadIdx.x & 31) == 0) atomicOr(&ds->lists_invalid, 1u);
 }
 
-int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell,
-                      uint32_t* cell_count, DevScalars* ds, cudaStream_t s) {
+int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+                     const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s) {
   const int N = R * R * R;
   int blocks = (N + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, key_raw, key_cell, cell_count, ds);
+  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, key_raw, key_cell, cell_count, key_ref, skin2, mu, ds);
+  return 1;
+}
+
+// After a list rebuild: remember every key's position and bl (the skin reference).
+// Also closes the build's counters (pool cursor, overflow count) for the next build.
+__global__ void k_list_snapshot(const float4* __restrict__ key_raw, float4* __restrict__ key_ref, int n_keys,
+                                DevScalars* ds) {
+  if (!ds->lists_invalid) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ds->pool_used = ds->pool_top;
+    ds->pool_top = 0;
+    ds->ovf_last = ds->ovf_count;
+    ds->ovf_count = 0;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_keys; i += gridDim.x * blockDim.x)
+    key_ref[i] = key_raw[2 * i];
+}
+
+int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, DevScalars* ds,
+                         cudaStream_t s) {
+  int blocks = (n_keys + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_list_snapshot<<<blocks, 256, 0, s>>>(key_raw, key_ref, n_keys, ds);
   return 1;
 }
 
@@ -218,30 +250,40 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every 3
   return v;
 }
 
-__global__ void k_query_bins(const float* __restrict__ q, const float* __restrict__ o, int64_t J, int bits,
-                             uint32_t* __restrict__ bins, uint32_t* __restrict__ count, DevScalars* ds) {
-  const float scale = (float)(1 << bits) * 0.5f;
-  const int maxc = (1 << bits) - 1;
+// Bin = Morton code of the query's brick (B^3 lattice cells); queries outside [-1,1]^3 (or
+// non-finite) go to the last bin, whose items enumerate keys directly instead of a brick list.
+__global__ void k_query_bins(const float* __restrict__ q, const float* __restrict__ o, int64_t J, BrickGeom bg,
+                             int NC, float inv_h, uint32_t* __restrict__ bins, uint32_t* __restrict__ count,
+                             DevScalars* ds) {
+  const uint32_t outside = bg.n_codes * QSUB;
+  const float sub_scale = 2.0f * inv_h / (float)bg.B;
   bool bad = false;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
     const float x = q[3 * j], y = q[3 * j + 1], z = q[3 * j + 2];
     bool fin = isfinite(x) && isfinite(y) && isfinite(z);
     if (o) fin = fin && isfinite(o[j]);
     bad |= !fin;
-    const int ix = (int)fminf(fmaxf(floorf((x + 1.0f) * scale), 0.0f), (float)maxc);
-    const int iy = (int)fminf(fmaxf(floorf((y + 1.0f) * scale), 0.0f), (float)maxc);
-    const int iz = (int)fminf(fmaxf(floorf((z + 1.0f) * scale), 0.0f), (float)maxc);
-    const uint32_t b = spread3(ix) | (spread3(iy) << 1) | (spread3(iz) << 2);
+    uint32_t b = outside;
+    if (fin && fabsf(x) <= 1.0f && fabsf(y) <= 1.0f && fabsf(z) <= 1.0f) {
+      const int bx = cell_clamp(x, inv_h, NC) / bg.B;
+      const int by = cell_clamp(y, inv_h, NC) / bg.B;
+      const int bz = cell_clamp(z, inv_h, NC) / bg.B;
+      // octant of the query inside its brick: the 8 sub-bins of a brick stay contiguous
+      const int sx = min(max((int)floorf((x + 1.0f) * sub_scale) - 2 * bx, 0), 1);
+      const int sy = min(max((int)floorf((y + 1.0f) * sub_scale) - 2 * by, 0), 1);
+      const int sz = min(max((int)floorf((z + 1.0f) * sub_scale) - 2 * bz, 0), 1);
+      b = (spread3(bx) | (spread3(by) << 1) | (spread3(bz) << 2)) * QSUB + (uint32_t)(sx | (sy << 1) | (sz << 2));
+    }
     bins[j] = b;
     atomicAdd(&count[b], 1u);
   }
   if (__any_sync(~0u, bad) && (threadIdx.x & 31) == 0) atomicOr(&ds->nonfinite, 1u);
 }
 
-int launch_query_bins(const float* q, const float* o, int64_t J, int bits, uint32_t* bins, uint32_t* count,
-                       DevScalars* ds, cudaStream_t s) {
+int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom& bg, int NC, float inv_h,
+                      uint32_t* bins, uint32_t* count, DevScalars* ds, cudaStream_t s) {
   if (J == 0) return 0;
-  k_query_bins<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(q, o, J, bits, bins, count, ds);
+  k_query_bins<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(q, o, J, bg, NC, inv_h, bins, count, ds);
   return 1;
 }
 
@@ -275,43 +317,52 @@ int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------ work items
-// Items never straddle a coarse Morton cell (edge ~4h): a fixed-size run of the Morton-sorted
-// stream can jump across the domain at a Morton boundary and then gets a huge box (and a huge
-// candidate list). Inside a coarse cell the queries are split into ceil(n/QITEM) balanced runs.
-__global__ void k_items_count(const uint32_t* __restrict__ bin_start, int shift, uint32_t n_coarse,
-                              uint32_t* __restrict__ cnt) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= n_coarse; c += gridDim.x * blockDim.x) {
-    if (c == n_coarse) {
+// A work item is a balanced run of <= QW queries of one brick (its QSUB octant bins are
+// contiguous in the sorted stream): ceil(n/QW) items per brick. The brick field is the brick's
+// Morton code, or -1 for the out-of-domain bin (index nb = number of bricks).
+__device__ __forceinline__ void brick_range(const uint32_t* bin_start, uint32_t c, uint32_t nb, uint32_t& s,
+                                            uint32_t& n) {
+  s = bin_start[c * QSUB];
+  const uint32_t e = (c == nb) ? bin_start[nb * QSUB + 1] : bin_start[(c + 1) * QSUB];
+  n = e - s;
+}
+
+__global__ void k_items_count(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t* __restrict__ cnt) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb + 1; c += gridDim.x * blockDim.x) {
+    if (c == nb + 1) {
       cnt[c] = 0;
       continue;
     }
-    const uint32_t n = bin_start[(c + 1) << shift] - bin_start[c << shift];
-    cnt[c] = (n + QITEM - 1) / QITEM;
+    uint32_t s, n;
+    brick_range(bin_start, c, nb, s, n);
+    cnt[c] = (n + QW - 1) / QW;
   }
 }
 
-__global__ void k_items_write(const uint32_t* __restrict__ bin_start, int shift, uint32_t n_coarse,
-                              const uint32_t* __restrict__ off, int2* __restrict__ items) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_coarse; c += gridDim.x * blockDim.x) {
-    const uint32_t s = bin_start[c << shift];
-    const uint32_t n = bin_start[(c + 1) << shift] - s;
-    const uint32_t m = (n + QITEM - 1) / QITEM;
+__global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t nb,
+                              const uint32_t* __restrict__ off, int4* __restrict__ items) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb; c += gridDim.x * blockDim.x) {
+    uint32_t s, n;
+    brick_range(bin_start, c, nb, s, n);
+    if (n == 0) continue;
+    const uint32_t m = (n + QW - 1) / QW;
     const uint32_t o = off[c];
+    const int brick = (c == nb) ? -1 : (int)c;
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t a = (uint32_t)(((uint64_t)i * n) / m), b = (uint32_t)(((uint64_t)(i + 1) * n) / m);
-      items[o + i] = make_int2((int)(s + a), (int)(b - a));
+      items[o + i] = make_int4((int)(s + a), (int)(b - a), brick, 0);
     }
   }
 }
 
-int launch_items_count(const uint32_t* bin_start, int shift, uint32_t n_coarse, uint32_t* cnt, cudaStream_t s) {
-  k_items_count<<<grid_for(n_coarse + 1, 256), 256, 0, s>>>(bin_start, shift, n_coarse, cnt);
+int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t* cnt, cudaStream_t s) {
+  k_items_count<<<grid_for(nb + 2, 256), 256, 0, s>>>(bin_start, nb, cnt);
   return 1;
 }
 
-int launch_items_write(const uint32_t* bin_start, int shift, uint32_t n_coarse, const uint32_t* off, int2* items,
+int launch_items_write(const uint32_t* bin_start, uint32_t nb, const uint32_t* off, int4* items,
                        cudaStream_t s) {
-  k_items_write<<<grid_for(n_coarse, 128), 128, 0, s>>>(bin_start, shift, n_coarse, off, items);
+  k_items_write<<<grid_for(nb + 1, 128), 128, 0, s>>>(bin_start, nb, off, items);
   return 1;
 }
 

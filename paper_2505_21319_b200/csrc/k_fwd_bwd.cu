@@ -21,7 +21,6 @@
 
 namespace ef {
 
-constexpr int NWARP = NTHREADS / 32;
 constexpr int WSLICE = 64;  // staged keys per warp
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -74,15 +73,25 @@ __device__ __forceinline__ Box warp_box(bool act, float x, float y, float z, flo
   return b;
 }
 
-// Warp-level candidate enumeration. Visits the keys of the lattice-cell rows (x-runs) that
-// overlap the box grown by rho in (row, position) order, 32 at a time; calls
-// stage(pass, kp, a) on every lane for each batch (warp-uniform call; a valid iff pass).
+// distance from a lattice cell's extent along one axis to [lo, hi]; boundary cells extend to
+// infinity (out-of-domain keys are clamped into them); the cell is widened by a rounding margin
+__device__ __forceinline__ float cell_gap(int c, int NC, float h, float lo, float hi) {
+  const float m = 1e-3f * h;
+  const float clo = (c == 0) ? -INFINITY : fmaf((float)c, h, -1.0f) - m;
+  const float chi = (c == NC - 1) ? INFINITY : fmaf((float)(c + 1), h, -1.0f) + m;
+  return fmaxf(fmaxf(lo - chi, clo - hi), 0.0f);
+}
+
+// Warp-level candidate enumeration. Visits, in (row, position) order, the keys of the lattice-
+// cell rows (x-runs) that can hold a key within rho = sqrt(thr / bl_min) of the box: rows whose
+// y-z gap exceeds rho are skipped and each row's x-range is cut to the ball's chord. Calls
+// stage(pass, kp, a) on every lane for each batch of 32 (warp-uniform call; a valid iff pass).
 template <class Stage>
 __device__ __forceinline__ void enumerate(const KeysView& kv, const Box& box, Stage&& stage) {
   const int lane = threadIdx.x & 31;
-  const float rho = sqrtf(box.thr / *kv.bl_min);
+  const float rho2 = box.thr / *kv.bl_min;
+  const float rho = sqrtf(rho2);
   const int NC = kv.NC;
-  const int cx0 = cellc(box.lx - rho, kv.inv_h, NC), cx1 = cellc(box.hx + rho, kv.inv_h, NC);
   const int cy0 = cellc(box.ly - rho, kv.inv_h, NC), cy1 = cellc(box.hy + rho, kv.inv_h, NC);
   const int cz0 = cellc(box.lz - rho, kv.inv_h, NC), cz1 = cellc(box.hz + rho, kv.inv_h, NC);
   const int ny = cy1 - cy0 + 1;
@@ -92,9 +101,16 @@ __device__ __forceinline__ void enumerate(const KeysView& kv, const Box& box, St
     uint32_t s = 0, len = 0;
     if (r < nrows) {
       const int cy = cy0 + r % ny, cz = cz0 + r / ny;
-      const int base = (cz * NC + cy) * NC;
-      s = __ldg(&kv.cell_start[base + cx0]);
-      len = __ldg(&kv.cell_start[base + cx1 + 1]) - s;
+      const float gy = cell_gap(cy, NC, kv.h, box.ly, box.hy);
+      const float gz = cell_gap(cz, NC, kv.h, box.lz, box.hz);
+      const float g2 = fmaf(gy, gy, gz * gz);
+      if (!(g2 > rho2)) {
+        const float rx = sqrtf(fmaxf(rho2 - g2, 0.0f));
+        const int cx0 = cellc(box.lx - rx, kv.inv_h, NC), cx1 = cellc(box.hx + rx, kv.inv_h, NC);
+        const int base = (cz * NC + cy) * NC;
+        s = __ldg(&kv.cell_start[base + cx0]);
+        len = __ldg(&kv.cell_start[base + cx1 + 1]) - s;
+      }
     }
     uint32_t incl = len;
 #pragma unroll
@@ -128,9 +144,222 @@ __device__ __forceinline__ void enumerate(const KeysView& kv, const Box& box, St
   }
 }
 
+// Same visit order as enumerate(), but the flattened position -> row map of each 32-row batch
+// is materialised in a per-warp byte array (owner), so every lane resolves its row with one
+// shared-memory load instead of a 5-step shuffle search, and two loads per lane are in flight.
+// Batches longer than cap fall back to the shuffle search.
+constexpr int OWN_CAP = 4096;
+
+template <class Stage>
+__device__ __forceinline__ void enumerate_owned(const KeysView& kv, const Box& box, uint8_t* owner,
+                                                uint32_t* rs, uint32_t* ro, Stage&& stage) {
+  const int lane = threadIdx.x & 31;
+  const float rho2 = box.thr / *kv.bl_min;
+  const float rho = sqrtf(rho2);
+  const int NC = kv.NC;
+  const int cy0 = cellc(box.ly - rho, kv.inv_h, NC), cy1 = cellc(box.hy + rho, kv.inv_h, NC);
+  const int cz0 = cellc(box.lz - rho, kv.inv_h, NC), cz1 = cellc(box.hz + rho, kv.inv_h, NC);
+  const int ny = cy1 - cy0 + 1;
+  const int nrows = ny * (cz1 - cz0 + 1);
+  for (int rb = 0; rb < nrows; rb += 32) {
+    const int r = rb + lane;
+    uint32_t s = 0, len = 0;
+    if (r < nrows) {
+      const int cy = cy0 + r % ny, cz = cz0 + r / ny;
+      const float gy = cell_gap(cy, NC, kv.h, box.ly, box.hy);
+      const float gz = cell_gap(cz, NC, kv.h, box.lz, box.hz);
+      const float g2 = fmaf(gy, gy, gz * gz);
+      if (!(g2 > rho2)) {
+        const float rx = sqrtf(fmaxf(rho2 - g2, 0.0f));
+        const int cx0 = cellc(box.lx - rx, kv.inv_h, NC), cx1 = cellc(box.hx + rx, kv.inv_h, NC);
+        const int base = (cz * NC + cy) * NC;
+        s = __ldg(&kv.cell_start[base + cx0]);
+        len = __ldg(&kv.cell_start[base + cx1 + 1]) - s;
+      }
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(~0u, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(~0u, incl, 31);
+    const uint32_t off = incl - len;
+    if (total > (uint32_t)OWN_CAP) {
+      for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+        const uint32_t f = f0 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const uint32_t o = __shfl_sync(~0u, off, lo + st);
+          if (o <= f) lo += st;
+        }
+        const uint32_t kp = __shfl_sync(~0u, s, lo) + (f - __shfl_sync(~0u, off, lo));
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool pass = false;
+        if (f < total) {
+          a = __ldg(&kv.ks[2 * kp]);
+          pass = within(a, box);
+        }
+        stage(pass, kp, a);
+      }
+      continue;
+    }
+    rs[lane] = s;
+    ro[lane] = off;
+    for (int rr = 0; rr < 32; ++rr) {
+      const uint32_t l = __shfl_sync(~0u, len, rr), o = __shfl_sync(~0u, off, rr);
+      for (uint32_t t = lane; t < l; t += 32) owner[o + t] = (uint8_t)rr;
+    }
+    __syncwarp();
+    for (uint32_t f0 = 0; f0 < total; f0 += 64) {
+      uint32_t kp[2];
+      float4 a[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t f = f0 + 32 * u + lane;
+        kp[u] = 0;
+        a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (f < total) {
+          const int rw = owner[f];
+          kp[u] = rs[rw] + (f - ro[rw]);
+          a[u] = __ldg(&kv.ks[2 * kp[u]]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t f = f0 + 32 * u + lane;
+        if (f0 + 32 * u < total) stage(f < total && within(a[u], box), kp[u], a[u]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Candidate keys of a warp item: stream its brick's precomputed list (k_brick_lists, key ids)
+// through the warp's own test, or enumerate directly for out-of-domain items and overflowed
+// bricks. stage(pass, key id, a) as for enumerate().
+template <class Stage>
+__device__ __forceinline__ void candidates(const KeysView& kv, int brick, const Box& box, Stage&& stage) {
+  uint32_t n = BL_OVERFLOW;
+  if (brick >= 0) n = __ldg(&kv.bl_n[brick]);
+  if (n == BL_OVERFLOW) {
+    enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
+      stage(pass, pass ? (uint32_t)__ldg(&kv.kid[kp]) : 0u, a);
+    });
+    return;
+  }
+  const uint32_t* L = kv.bl_pool + __ldg(&kv.bl_off[brick]);
+  const int lane = threadIdx.x & 31;
+  uint32_t e_next = ((uint32_t)lane < n) ? __ldg(&L[lane]) : 0u;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t k = base + lane;
+    const uint32_t id = e_next;
+    e_next = (k + 32 < n) ? __ldg(&L[k + 32]) : 0u;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool pass = false;
+    if (k < n) {
+      a = __ldg(&kv.grid_raw[2 * id]);
+      pass = within(a, box);
+    }
+    stage(pass, id, a);
+  }
+}
+
+__device__ __forceinline__ uint32_t compact3(uint32_t v) {  // inverse of the Morton spread
+  v &= 0x09249249u;
+  v = (v | (v >> 2)) & 0x030C30C3u;
+  v = (v | (v >> 4)) & 0x0300F00Fu;
+  v = (v | (v >> 8)) & 0x030000FFu;
+  v = (v | (v >> 16)) & 0x000003FFu;
+  return v;
+}
+
+// Per brick (one warp each): every key that can reach some query inside the brick. A query in
+// cell c has mh <= bl_max(c's corners) * 3h^2/4 (its nearest corner is within sqrt(3) h / 2),
+// so thr_brick = bl_max(brick nodes) * 3h^2/4 + T_l bounds every warp threshold of the step.
+constexpr int KB_WARPS = 2;
+__global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv, const BrickGeom bg, float T_l,
+                                                          uint32_t* __restrict__ pool, uint32_t pool_cap,
+                                                          uint32_t* __restrict__ off, uint32_t* __restrict__ nout,
+                                                          DevScalars* ds) {
+  __shared__ uint32_t st[KB_WARPS][BL_CAP];
+  __shared__ uint8_t own[KB_WARPS][OWN_CAP];
+  __shared__ uint32_t rs[KB_WARPS][32], ro[KB_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (!ds->lists_invalid) return;  // the lists of an earlier step are still valid (Verlet skin)
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ds->list_builds, 1u);
+  for (uint32_t code = blockIdx.x * KB_WARPS + w; code < bg.n_codes; code += gridDim.x * KB_WARPS) {
+  const int bx = (int)compact3(code), by = (int)compact3(code >> 1), bz = (int)compact3(code >> 2);
+  if (bx >= bg.nb || by >= bg.nb || bz >= bg.nb) {
+    if (lane == 0) {
+      off[code] = 0;
+      nout[code] = 0;
+    }
+    continue;
+  }
+  const int NC = kv.NC, R = kv.R, B = bg.B;
+  const int c0x = bx * B, c1x = min(NC, c0x + B) - 1;
+  const int c0y = by * B, c1y = min(NC, c0y + B) - 1;
+  const int c0z = bz * B, c1z = min(NC, c0z + B) - 1;
+  const int nx = c1x - c0x + 2, ny = c1y - c0y + 2, nz = c1z - c0z + 2;
+  float blmax = 0.0f;
+  for (int t = lane; t < nx * ny * nz; t += 32) {
+    const int ix = c0x + t % nx, iy = c0y + (t / nx) % ny, iz = c0z + t / (nx * ny);
+    blmax = fmaxf(blmax, __ldg(&kv.grid_raw[2 * (ix + R * (iy + R * iz))]).w);
+  }
+  for (int o = 16; o > 0; o >>= 1) blmax = fmaxf(blmax, __shfl_xor_sync(~0u, blmax, o));
+  // Verlet skin: valid while every key stays within skin of its build position and its bl within a
+  // factor (1+mu): grow the box by skin and the threshold by (1+mu) for both the key's and the
+  // corner keys' bl drift.
+  const float h = kv.h, m = 1e-3f * h + SKIN_H * h;
+  const float mu1 = 1.0f + SKIN_MU;
+  Box box;
+  box.lx = fmaf((float)c0x, h, -1.0f) - m; box.hx = fmaf((float)(c1x + 1), h, -1.0f) + m;
+  box.ly = fmaf((float)c0y, h, -1.0f) - m; box.hy = fmaf((float)(c1y + 1), h, -1.0f) + m;
+  box.lz = fmaf((float)c0z, h, -1.0f) - m; box.hz = fmaf((float)(c1z + 1), h, -1.0f) + m;
+  box.thr = mu1 * (mu1 * blmax * 0.75f * h * h * 1.001f + T_l) + 1e-3f;
+  uint32_t cnt = 0;
+  enumerate_owned(kv, box, own[w], rs[w], ro[w], [&](bool pass, uint32_t kp, float4 a) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) {
+      const uint32_t slot = cnt + __popc(bal & lanemask_lt());
+      if (slot < (uint32_t)BL_CAP) st[w][slot] = (uint32_t)__ldg(&kv.kid[kp]);  // key id
+    }
+    cnt += __popc(bal);
+  });
+  uint32_t base = 0;
+  if (lane == 0 && cnt <= (uint32_t)BL_CAP) base = atomicAdd(&ds->pool_top, cnt);
+  base = __shfl_sync(~0u, base, 0);
+  if (cnt > (uint32_t)BL_CAP || base + cnt > pool_cap) {
+    if (lane == 0) {
+      off[code] = 0;
+      nout[code] = BL_OVERFLOW;
+      atomicAdd(&ds->ovf_count, 1u);
+    }
+    continue;
+  }
+  __syncwarp();
+  for (uint32_t i = lane; i < cnt; i += 32) pool[base + i] = st[w][i];
+  if (lane == 0) {
+    off[code] = base;
+    nout[code] = cnt;
+  }
+  __syncwarp();
+  }
+}
+
+int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool, uint32_t pool_cap,
+                       uint32_t* off, uint32_t* n, DevScalars* ds, cudaStream_t s) {
+  uint32_t blocks = (bg.n_codes + KB_WARPS - 1) / KB_WARPS;
+  if (blocks > 148u * 16u) blocks = 148u * 16u;
+  k_brick_lists<<<blocks, 32 * KB_WARPS, 0, s>>>(kv, bg, T_l, pool, pool_cap, off, n, ds);
+  return 1;
+}
+
 // Shift bound mh_j >= m_j (log2 units): best of the 8 lattice-corner grid keys and of (up to 32)
 // keys in the query's own cell; f0 = f of that key at q (accuracy shift of SURVEY App. D).
-__device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, float& mh, float& f0) {
+__device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, float& mh, float& f0, float3& g0) {
   const int R = kv.R, NC = kv.NC;
   const int cx = cellc(q.x, kv.inv_h, NC), cy = cellc(q.y, kv.inv_h, NC), cz = cellc(q.z, kv.inv_h, NC);
   mh = INFINITY;
@@ -145,6 +374,7 @@ __device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, 
       mh = e;
       const float4 kb = __ldg(&kv.grid_raw[2 * n + 1]);
       f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
+      g0 = make_float3(kb.y, kb.z, kb.w);
     }
   }
   const int cid = (cz * NC + cy) * NC + cx;
@@ -158,6 +388,7 @@ __device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, 
       mh = e;
       const float4 kb = __ldg(&kv.ks[2 * k + 1]);
       f0 = fmaf(kb.w, dz, fmaf(kb.z, dy, fmaf(kb.y, dx, kb.x)));
+      g0 = make_float3(kb.y, kb.z, kb.w);
     }
   }
 }
@@ -174,16 +405,16 @@ struct FwdAcc {
 
 template <bool WANT_G>
 __device__ __forceinline__ void fwd_pair(const float4 q, const float4 a, const float4 b, float shift, float f0,
-                                         FwdAcc& s) {
+                                         const float3 g0, FwdAcc& s) {
   const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
   const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
   const float wgt = ex2f(fmaf(-a.w, dd, shift));
   s.Z += wgt;
   if (WANT_G) {
     const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x - f0)));
-    s.sgx = fmaf(wgt, b.y, s.sgx);
-    s.sgy = fmaf(wgt, b.z, s.sgy);
-    s.sgz = fmaf(wgt, b.w, s.sgz);
+    s.sgx = fmaf(wgt, b.y - g0.x, s.sgx);  // relative to the shift key's g (accuracy)
+    s.sgy = fmaf(wgt, b.z - g0.y, s.sgy);
+    s.sgz = fmaf(wgt, b.w - g0.z, s.sgz);
     const float wbl = wgt * a.w;
     s.sux = fmaf(wbl, dx, s.sux);
     s.suy = fmaf(wbl, dy, s.suy);
@@ -206,21 +437,18 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   __shared__ int ws_id[NWARP][WSLICE];
   const KeysView& kv = A.kv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t item = blockIdx.x;
+  const uint32_t item = blockIdx.x * NWARP + w;
   if (item >= *A.n_items) return;
-  const int2 it = A.items[item];
-  const int nact = min(32, it.y - 32 * w);  // queries of this warp's group
-  if (nact <= 0) {                           // (warps are independent: no block barrier below)
-    if (lane == 0 && A.loss_kind >= EFUNC_LOSS_MSE) A.loss_part[item * NWARP + w] = 0.0f;
-    return;
-  }
+  const int4 it = A.items[item];
+  const int nact = it.y;  // queries of this warp's item (warps are independent: no block barrier)
   const bool act = lane < nact;
-  const int64_t js = (int64_t)it.x + 32 * w + lane;
+  const int64_t js = (int64_t)it.x + lane;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
   float mh = INFINITY, f0 = 0.f;
+  float3 g0 = make_float3(0.f, 0.f, 0.f);
   if (act) {
     q = A.qs[js];
-    shift_bound(kv, q, mh, f0);
+    shift_bound(kv, q, mh, f0, g0);
   }
   Box box = warp_box(act, q.x, q.y, q.z, mh);
   box.thr += A.T_l;
@@ -240,7 +468,7 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       if (act) {
         if (mode == 0) {
 #pragma unroll 4
-          for (uint32_t i = 0; i < cnt; ++i) fwd_pair<WANT_G>(q, sa[i], sb[i], shift, f0, s);
+          for (uint32_t i = 0; i < cnt; ++i) fwd_pair<WANT_G>(q, sa[i], sb[i], shift, f0, g0, s);
         } else if (mode == 1) {
           for (uint32_t i = 0; i < cnt; ++i) mexact = fminf(mexact, exponent(q, sa[i]));
         } else {
@@ -254,13 +482,13 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       __syncwarp();
       cnt = 0;
     };
-    enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
+    candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a) {
       const uint32_t bal = __ballot_sync(~0u, pass);
       if (pass) {
         const uint32_t slot = cnt + __popc(bal & lanemask_lt());
         sa[slot] = a;
-        if (mode == 0) sb[slot] = __ldg(&kv.ks[2 * kp + 1]);
-        if (mode == 2) sid[slot] = __ldg(&kv.kid[kp]);
+        if (mode == 0) sb[slot] = __ldg(&kv.grid_raw[2 * kp + 1]);
+        if (mode == 2) sid[slot] = (int)kp;
       }
       cnt += __popc(bal);
       if (cnt >= WSLICE - 32) consume();
@@ -306,9 +534,9 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
     if (WANT_G) {
       const float c2 = 2.0f * EF_LN2 * iz;
       const float Of = O - f0;
-      Gx = s.sgx * iz + c2 * fmaf(Of, s.sux, -s.sfx);
-      Gy = s.sgy * iz + c2 * fmaf(Of, s.suy, -s.sfy);
-      Gz = s.sgz * iz + c2 * fmaf(Of, s.suz, -s.sfz);
+      Gx = g0.x + (s.sgx * iz + c2 * fmaf(Of, s.sux, -s.sfx));
+      Gy = g0.y + (s.sgy * iz + c2 * fmaf(Of, s.suy, -s.sfy));
+      Gz = g0.z + (s.sgz * iz + c2 * fmaf(Of, s.suz, -s.sfz));
       A.gs[js] = make_float4(Gx, Gy, Gz, 0.f);
       A.us[js] = make_float4(c2 * s.sux, c2 * s.suy, c2 * s.suz, 0.f);
       if (A.G) {
@@ -333,14 +561,15 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   }
   if (A.loss_kind >= EFUNC_LOSS_MSE) {
     for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
-    if (lane == 0) A.loss_part[item * NWARP + w] = lossj;
+    if (lane == 0) A.loss_part[item] = lossj;
   }
 }
 
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
-  if (want_g) k_forward<true><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
-  else k_forward<false><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (want_g) k_forward<true><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_forward<false><<<blocks, NTHREADS, 0, s>>>(a);
   return 1;
 }
 
@@ -355,15 +584,14 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   __shared__ int kid_s[NWARP][WSLICE];
   const KeysView& kv = A.kv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t item = blockIdx.x;
+  const uint32_t item = blockIdx.x * NWARP + w;
   if (item >= *A.n_items) return;
-  const int2 it = A.items[item];
-  const int nact = min(32, it.y - 32 * w);
-  if (nact <= 0) return;
+  const int4 it = A.items[item];
+  const int nact = it.y;
   const bool act = lane < nact;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
   if (act) {
-    const int64_t js = (int64_t)it.x + 32 * w + lane;
+    const int64_t js = (int64_t)it.x + lane;
     q = A.qs[js];
     const float4 rc = A.rec[js];
     const int ju = A.perm[js];
@@ -488,13 +716,13 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   };
 
   uint32_t head = 0, cnt = 0;  // ring buffer of staged keys
-  enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
+  candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a) {
     const uint32_t bal = __ballot_sync(~0u, pass);
     if (pass) {
       const uint32_t slot = (head + cnt + __popc(bal & lanemask_lt())) % WSLICE;
       sa[slot] = a;
-      sb[slot] = __ldg(&kv.ks[2 * kp + 1]);
-      sid[slot] = __ldg(&kv.kid[kp]);
+      sb[slot] = __ldg(&kv.grid_raw[2 * kp + 1]);
+      sid[slot] = (int)kp;
     }
     cnt += __popc(bal);
     if (cnt >= 32) {
@@ -508,8 +736,9 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
 
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
-  if (a.eik) k_backward<true><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
-  else k_backward<false><<<(unsigned)n_items, NTHREADS, 0, s>>>(a);
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (a.eik) k_backward<true><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_backward<false><<<blocks, NTHREADS, 0, s>>>(a);
   return 1;
 }
 

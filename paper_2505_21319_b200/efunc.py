@@ -44,7 +44,8 @@ class AdamWParams(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("J", C.c_int64), ("items", C.c_int64), ("candidate_pairs", C.c_double),
                 ("kept_pairs", C.c_double), ("beta_min", C.c_float), ("nonfinite", C.c_int32),
-                ("overflow_items", C.c_int32), ("kept_pairs_offset", C.c_double), ("launches", C.c_int64)]
+                ("overflow_items", C.c_int32), ("kept_pairs_offset", C.c_double), ("launches", C.c_int64),
+                ("list_builds", C.c_int64), ("list_entries", C.c_int64), ("list_overflow", C.c_int64)]
 
 
 class EfuncError(RuntimeError):
