@@ -28,7 +28,7 @@
 namespace ef {
 
 constexpr int QW = 32;              // queries per work item (one warp)
-constexpr int NTHREADS = 128;       // 4 independent warps per CTA
+constexpr int NTHREADS = 32;        // one warp per CTA: items retire independently
 constexpr int NWARP = NTHREADS / 32;
 constexpr int BL_CAP = 4096;        // max staged list length per brick (longer: fallback)
 constexpr uint32_t BL_OVERFLOW = 0xffffffffu;

@@ -239,30 +239,39 @@ __device__ __forceinline__ void enumerate_owned(const KeysView& kv, const Box& b
 // Candidate keys of a warp item: stream its brick's precomputed list (k_brick_lists, key ids)
 // through the warp's own test, or enumerate directly for out-of-domain items and overflowed
 // bricks. stage(pass, key id, a) as for enumerate().
+// The list stream is software-pipelined: ids two batches ahead, both key records one batch
+// ahead, so the L2 latency of the gathers overlaps the previous batch's compute.
 template <class Stage>
 __device__ __forceinline__ void candidates(const KeysView& kv, int brick, const Box& box, Stage&& stage) {
   uint32_t n = BL_OVERFLOW;
   if (brick >= 0) n = __ldg(&kv.bl_n[brick]);
   if (n == BL_OVERFLOW) {
     enumerate(kv, box, [&](bool pass, uint32_t kp, float4 a) {
-      stage(pass, pass ? (uint32_t)__ldg(&kv.kid[kp]) : 0u, a);
+      const float4 b = pass ? __ldg(&kv.ks[2 * kp + 1]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      stage(pass, pass ? (uint32_t)__ldg(&kv.kid[kp]) : 0u, a, b);
     });
     return;
   }
   const uint32_t* L = kv.bl_pool + __ldg(&kv.bl_off[brick]);
-  const int lane = threadIdx.x & 31;
-  uint32_t e_next = ((uint32_t)lane < n) ? __ldg(&L[lane]) : 0u;
+  const uint32_t lane = threadIdx.x & 31;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t id1 = (lane < n) ? __ldg(&L[lane]) : 0u;            // batch i
+  uint32_t id2 = (lane + 32 < n) ? __ldg(&L[lane + 32]) : 0u;  // batch i+1
+  float4 a1 = (lane < n) ? __ldg(&kv.grid_raw[2 * id1]) : z4;
+  float4 b1 = (lane < n) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t k = base + lane;
-    const uint32_t id = e_next;
-    e_next = (k + 32 < n) ? __ldg(&L[k + 32]) : 0u;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    bool pass = false;
-    if (k < n) {
-      a = __ldg(&kv.grid_raw[2 * id]);
-      pass = within(a, box);
+    const uint32_t id = id1;
+    const float4 a = a1, b = b1;
+    // prefetch
+    id1 = id2;
+    id2 = (k + 64 < n) ? __ldg(&L[k + 64]) : 0u;
+    if (k + 32 < n) {
+      a1 = __ldg(&kv.grid_raw[2 * id1]);
+      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
     }
-    stage(pass, id, a);
+    const bool pass = (k < n) && within(a, box);
+    stage(pass, id, a, b);
   }
 }
 
@@ -467,8 +476,16 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       if (mode == 0) cand += cnt;
       if (act) {
         if (mode == 0) {
+          // register double-buffering of the broadcast key loads hides the LDS latency
+          float4 a0 = sa[0], b0 = sb[0];
 #pragma unroll 4
-          for (uint32_t i = 0; i < cnt; ++i) fwd_pair<WANT_G>(q, sa[i], sb[i], shift, f0, g0, s);
+          for (uint32_t i = 1; i < cnt; ++i) {
+            const float4 a1 = sa[i], b1 = sb[i];
+            fwd_pair<WANT_G>(q, a0, b0, shift, f0, g0, s);
+            a0 = a1;
+            b0 = b1;
+          }
+          fwd_pair<WANT_G>(q, a0, b0, shift, f0, g0, s);
         } else if (mode == 1) {
           for (uint32_t i = 0; i < cnt; ++i) mexact = fminf(mexact, exponent(q, sa[i]));
         } else {
@@ -482,12 +499,12 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       __syncwarp();
       cnt = 0;
     };
-    candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a) {
+    candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
       const uint32_t bal = __ballot_sync(~0u, pass);
       if (pass) {
         const uint32_t slot = cnt + __popc(bal & lanemask_lt());
         sa[slot] = a;
-        if (mode == 0) sb[slot] = __ldg(&kv.grid_raw[2 * kp + 1]);
+        if (mode == 0) sb[slot] = b;
         if (mode == 2) sid[slot] = (int)kp;
       }
       cnt += __popc(bal);
@@ -636,10 +653,7 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
     const float beta = a.w * EF_LN2;
     float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
     float phx = 0.f, phy = 0.f, phz = 0.f, pdx = 0.f, pdy = 0.f, pdz = 0.f;  // EIK only
-#pragma unroll 4
-    for (int j = 0; j < nact; ++j) {
-      const float4 P = Q[j];
-      const float4 U = V[j];
+    auto pair = [&](const float4 P, const float4 U, const float4 h) {
       const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
       const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
       const float p = ex2f(fmaf(-a.w, dd, P.w));
@@ -659,7 +673,6 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
         sdz = fmaf(u, dz, sdz);
       } else {
         // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
-        const float4 h = H[j];
         const float hd = fmaf(h.x, dx, fmaf(h.y, dy, h.z * dz));
         const float hu = 2.0f * beta * hd;
         const float hg = fmaf(h.x, b.y, fmaf(h.y, b.z, h.z * b.w));
@@ -684,7 +697,19 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
         pdy = fmaf(pdel, h.y, pdy);
         pdz = fmaf(pdel, h.z, pdz);
       }
+    };
+    // register double-buffering of the broadcast query loads hides the LDS latency
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 P0 = Q[0], U0 = V[0], H0 = EIK ? H[0] : z4;
+#pragma unroll 4
+    for (int j = 1; j < nact; ++j) {
+      const float4 P1 = Q[j], U1 = V[j], H1 = EIK ? H[j] : z4;
+      pair(P0, U0, H0);
+      P0 = P1;
+      U0 = U1;
+      H0 = H1;
     }
+    pair(P0, U0, H0);
     float dsv, dgx, dgy, dgz;
     if (!EIK) {
       dsv = -beta * ss;
@@ -716,12 +741,12 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   };
 
   uint32_t head = 0, cnt = 0;  // ring buffer of staged keys
-  candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a) {
+  candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
     const uint32_t bal = __ballot_sync(~0u, pass);
     if (pass) {
       const uint32_t slot = (head + cnt + __popc(bal & lanemask_lt())) % WSLICE;
       sa[slot] = a;
-      sb[slot] = __ldg(&kv.grid_raw[2 * kp + 1]);
+      sb[slot] = b;
       sid[slot] = (int)kp;
     }
     cnt += __popc(bal);

