@@ -156,6 +156,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2505_21319_b200 as ef
+    from paper_2505_21319_b200 import dist as edist
     from workloads import synth
 
     R, J, shape_name, loss_kind, label = CONFIGS[args.config]
@@ -163,7 +164,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     shape = synth.make_shape(shape_name)
     loss = ef.LOSS_MSE if loss_kind == "mse" else ef.LOSS_MSE_EIKONAL
-    J_global = J * world
+    J_global = edist.global_batch(J, world)
 
     # model: paper init (s = 7, c ~ N(0, 0.1^2), g = 0) + mean-shift offsets on the GPU
     th0 = synth.init_theta(R, SEED)
@@ -174,7 +175,7 @@ def run_ours(args, rank, world, local_rank):
 
     # input pool (> L2 at C2); each rank draws its own points
     pool = max(2, min(POOL, int(np.ceil(160e6 / (16 * J)))))
-    host = [synth.sample_batch(shape, J, seed=SEED + 1000 * rank + i) for i in range(pool)]
+    host = [synth.sample_batch(shape, J, seed=edist.rank_seed(SEED, rank, i)) for i in range(pool)]
     qd = [torch.as_tensor(q).cuda(dev) for q, _ in host]
     od = [torch.as_tensor(o).cuda(dev) for _, o in host]
     grad = torch.zeros(R ** 3, ef.NCH, dtype=torch.float32, device=f"cuda:{dev}")
@@ -188,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
         if ev is not None:
             ev[1].record()
         if world > 1:
-            dist.all_reduce(grad)
+            edist.allreduce_grad(grad)
         m.adamw_step(grad, hp)
 
     # kept-pair census (algorithmic work per point), outside the timed region
@@ -261,7 +262,7 @@ def run_ours(args, rank, world, local_rank):
                 grad.zero_()
                 _, _, L = m.forward(qbuf, obuf, loss=loss, J_global=J_global, want_O=False)
                 m.backward(grad=grad)
-                dist.all_reduce(grad)
+                edist.allreduce_grad(grad)
                 m.adamw_step(grad, hp)
                 return float(L.item())
             for w in range(3):

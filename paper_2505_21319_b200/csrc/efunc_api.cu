@@ -168,7 +168,7 @@ void free_all(efunc_t* h) {
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
   dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
-  dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref);
+  dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -266,6 +266,9 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.n_items = h->item_off + (h->bg.n_codes + 1);
   b.T_l = cutoff_log2(h->cfg);
   b.gpad = h->gpad;
+  b.gfix = h->gfix;
+  b.umax = &h->ds->umax;
+  b.fix_overflow = &h->ds->fix_overflow;
   b.rec = h->rec;
   b.gs = h->gs;
   b.us = h->us;
@@ -274,8 +277,14 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.dL_dG = dL_dG;
   b.grad = grad;
   b.eik = eik;
-  h->launches += launch_backward(b, h->fwd_items_bound, s);
-  h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+  if (h->cfg.deterministic) {
+    CK(cudaMemsetAsync(&h->ds->umax, 0, sizeof(float), s));
+    h->launches += launch_backward_det(b, h->fwd_items_bound, s);
+    h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);
+  } else {
+    h->launches += launch_backward(b, h->fwd_items_bound, s);
+    h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+  }
   CK(cudaGetLastError());
   return EFUNC_OK;
 }
@@ -360,6 +369,10 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     RET(ensure_scan_tmp(h, nbins + 1));
     CK(dalloc(&h->gpad, (size_t)h->n_nodes * 16));
     CK(cudaMemset(h->gpad, 0, sizeof(float) * (size_t)h->n_nodes * 16));
+    if (h->cfg.deterministic) {
+      CK(dalloc(&h->gfix, (size_t)h->n_nodes * 16));
+      CK(cudaMemset(h->gfix, 0, sizeof(unsigned long long) * (size_t)h->n_nodes * 16));
+    }
     CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
     RET(ensure_scan_tmp(h, h->n_cells + 1));
     if (theta_host) CK(cudaMemcpy(h->theta, theta_host, np * sizeof(float), cudaMemcpyHostToDevice));
@@ -548,11 +561,16 @@ efunc_status efunc_check(efunc_t* h, void* stream) {
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
-  uint32_t nf = 0;
+  uint32_t nf = 0, fo = 0;
   CK(cudaMemcpy(&nf, &h->ds->nonfinite, sizeof(nf), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&fo, &h->ds->fix_overflow, sizeof(fo), cudaMemcpyDeviceToHost));
   if (nf) {
     CK(cudaMemset(&h->ds->nonfinite, 0, sizeof(uint32_t)));
     return fail(h, EFUNC_ENONFINITE, "non-finite query or target");
+  }
+  if (fo) {
+    CK(cudaMemset(&h->ds->fix_overflow, 0, sizeof(uint32_t)));
+    return fail(h, EFUNC_ENONFINITE, "deterministic backward: a partial exceeded the fixed-point range");
   }
   return EFUNC_OK;
 }

@@ -63,7 +63,8 @@ struct DevScalars {
   uint32_t ovf_count;      // bricks overflowed in the running build
   uint32_t pool_used;      // entries of the last completed build
   uint32_t ovf_last;       // overflowed bricks of the last completed build
-  uint32_t pad2;
+  float umax;              // deterministic backward: max_j (|dL/dO_j| + |dL/dG_j|_1) of the call
+  uint32_t fix_overflow;   // deterministic backward: a partial left the fixed-point range
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
@@ -110,7 +111,14 @@ struct BwdArgs {
   float* grad;            // [R^3][13] +=
   int eik;                // 1: add the dL/dG terms
   float* gpad;            // [R^3][16] padded accumulation buffer (zero on entry, zeroed by k_fold)
+  // deterministic mode: 64-bit fixed point, value = int * umax * 2^-FIX_BITS (integer adds are
+  // associative, so the sum is independent of the order the atomics land in)
+  unsigned long long* gfix;  // [R^3][16]
+  const float* umax;
+  uint32_t* fix_overflow;
 };
+
+constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
 
 struct BrickGeom {
   int B;          // lattice cells per brick edge
@@ -145,6 +153,8 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
+int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);
+int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, int n_nodes, cudaStream_t s);
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay,
                  float omb1, float b2, float omb2, float eps, uint32_t mask, float step_size,
                  float sqrt_bc2, cudaStream_t s);
@@ -180,6 +190,7 @@ struct efunc {
   ef::DevScalars* ds = nullptr;
   float* fit_grad = nullptr;
   float* gpad = nullptr;            // [R^3][16] padded gradient accumulator (kept zero between calls)
+  unsigned long long* gfix = nullptr;  // [R^3][16] fixed-point accumulator (deterministic mode)
   // brick lists
   uint32_t* bl_pool = nullptr;
   uint32_t bl_pool_cap = 0;

@@ -591,8 +591,22 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 }
 
 // ------------------------------------------------------------------------------ backward
-template <bool EIK>
+// DET: deterministic mode, 64-bit fixed-point accumulation (see BwdArgs::gfix)
+template <bool EIK, bool DET>
 __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
+  float fix_scale = 0.0f;
+  if (DET) {
+    const float um = *A.umax;
+    fix_scale = um > 0.0f ? (float)(1ull << FIX_BITS) / um : 0.0f;
+  }
+  auto fix_add = [&](unsigned long long* p, float v) {
+    const float qv = v * fix_scale;
+    if (fabsf(qv) < 4.0e18f) {
+      atomicAdd(p, (unsigned long long)(long long)rintf(qv));
+    } else {
+      atomicOr(A.fix_overflow, 1u);
+    }
+  };
   __shared__ float4 sq[NWARP][32];  // x, y, z, -lambda_l
   __shared__ float4 sv[NWARP][32];  // r, O, h.ubar, h.G
   __shared__ float4 sh[EIK ? NWARP : 1][32];
@@ -720,9 +734,15 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
     }
     // padded gradient: node n -> 16 floats {s0,c0,g0x,g0y | g0z,-,-,- | dx,dy,dz,s1 | c1,g1x,g1y,g1z}
     if (id < n_nodes) {
-      float* gp = gpad + (size_t)id * 16;
-      red_v4(gp, dsv, sc, dgx, dgy);
-      atomicAdd(gp + 4, dgz);
+      if (!DET) {
+        float* gp = gpad + (size_t)id * 16;
+        red_v4(gp, dsv, sc, dgx, dgy);
+        atomicAdd(gp + 4, dgz);
+      } else {
+        unsigned long long* gp = A.gfix + (size_t)id * 16;
+        fix_add(gp + 0, dsv); fix_add(gp + 1, sc); fix_add(gp + 2, dgx); fix_add(gp + 3, dgy);
+        fix_add(gp + 4, dgz);
+      }
     } else {
       float dkx, dky, dkz;
       if (!EIK) {
@@ -734,9 +754,15 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
         dky = fmaf(-b.z, sc, 2.0f * beta * (sdy + pdy));
         dkz = fmaf(-b.w, sc, 2.0f * beta * (sdz + pdz));
       }
-      float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
-      red_v4(gp, dkx, dky, dkz, dsv);
-      red_v4(gp + 4, sc, dgx, dgy, dgz);
+      if (!DET) {
+        float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
+        red_v4(gp, dkx, dky, dkz, dsv);
+        red_v4(gp + 4, sc, dgx, dgy, dgz);
+      } else {
+        unsigned long long* gp = A.gfix + (size_t)(id - n_nodes) * 16 + 8;
+        fix_add(gp + 0, dkx); fix_add(gp + 1, dky); fix_add(gp + 2, dkz); fix_add(gp + 3, dsv);
+        fix_add(gp + 4, sc); fix_add(gp + 5, dgx); fix_add(gp + 6, dgy); fix_add(gp + 7, dgz);
+      }
     }
   };
 
@@ -762,8 +788,57 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
-  if (a.eik) k_backward<true><<<blocks, NTHREADS, 0, s>>>(a);
-  else k_backward<false><<<blocks, NTHREADS, 0, s>>>(a);
+  if (a.eik) k_backward<true, false><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_backward<false, false><<<blocks, NTHREADS, 0, s>>>(a);
+  return 1;
+}
+
+// max_j (|dL/dO_j| + |dL/dG_j|_1): the fixed-point unit of the deterministic backward (a max is
+// independent of the order the atomics land in)
+__global__ void k_upstream_max(const BwdArgs A, float* umax) {
+  float m = 0.0f;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.J; j += (int64_t)gridDim.x * blockDim.x) {
+    float v = fabsf(A.dL_dO ? A.dL_dO[j] : A.rec[j].y);
+    if (A.eik) {
+      if (A.dL_dG) v += fabsf(A.dL_dG[3 * j]) + fabsf(A.dL_dG[3 * j + 1]) + fabsf(A.dL_dG[3 * j + 2]);
+      else v += fabsf(A.hs[j].x) + fabsf(A.hs[j].y) + fabsf(A.hs[j].z);
+    }
+    m = fmaxf(m, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(~0u, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(umax), __float_as_uint(m));
+}
+
+int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  long ub = (a.J + 255) / 256;
+  if (ub > 148 * 8) ub = 148 * 8;
+  k_upstream_max<<<(unsigned)(ub < 1 ? 1 : ub), 256, 0, s>>>(a, const_cast<float*>(a.umax));
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (a.eik) k_backward<true, true><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_backward<false, true><<<blocks, NTHREADS, 0, s>>>(a);
+  return 2;
+}
+
+// grad[n][13] += fixed-point sums * umax * 2^-FIX_BITS; zero the accumulator
+__global__ void k_fold_fix(unsigned long long* __restrict__ gfix, const float* __restrict__ umax,
+                           float* __restrict__ grad, int n_nodes) {
+  const double unit = (double)*umax / (double)(1ull << FIX_BITS);
+  const int map[13] = {0, 1, 2, 3, 4, 8, 9, 10, 11, 12, 13, 14, 15};
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    unsigned long long* p = gfix + (size_t)n * 16;
+    float* g = grad + (size_t)n * EF_NCH;
+#pragma unroll
+    for (int c = 0; c < 13; ++c) g[c] += (float)((double)(long long)p[map[c]] * unit);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) p[c] = 0ull;
+  }
+}
+
+int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, int n_nodes, cudaStream_t s) {
+  int blocks = (n_nodes + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_fold_fix<<<blocks, 256, 0, s>>>(gfix, umax, grad, n_nodes);
   return 1;
 }
 

@@ -312,3 +312,42 @@ def test_kept_pair_counter_matches_oracle():
     ref = orc.forward(th, 8, q, cutoff_T=20.0)
     assert abs(st["kept_pairs"] - ref.kept.sum()) <= 0.01 * ref.kept.sum()
     assert st["candidate_pairs"] >= st["kept_pairs"]
+
+
+# ----------------------------------------------------------------------------- deterministic mode
+def test_deterministic_backward_parity_and_bitwise_repeatability():
+    """Deterministic mode (reading R-D): 64-bit fixed-point gradient accumulation; results match
+    the oracle at 1e-4 and repeat bitwise across runs and handles."""
+    th, q, o = c1_case(seed=101)
+    m = ef.EFunc(8, th, deterministic=True)
+    m.forward(dev(q), dev(o), loss=ef.LOSS_MSE)
+    g1 = m.backward().cpu().numpy()
+    f = orc.forward(th, 8, q)
+    _, r = orc.mse_loss(f.O, o)
+    check_grads(g1, orc.backward(th, 8, q, f, r))
+    m.check()
+    m2 = ef.EFunc(8, th, deterministic=True)
+    m2.forward(dev(q), dev(o), loss=ef.LOSS_MSE)
+    g2 = m2.backward().cpu().numpy()
+    assert np.array_equal(g1, g2)
+
+
+def test_deterministic_fit_bitwise_at_scale():
+    """Three full fit steps at 32^3 x 13 with 2^18 torus points: bitwise identical theta twice."""
+    R, J = 32, 1 << 18
+    tor = synth.Torus()
+    th0 = synth.init_theta(R, 7)
+    s = dev(synth.surface_points(tor, 16384, seed=8))
+    batches = [synth.sample_batch(tor, J, seed=200 + k) for k in range(3)]
+    outs = []
+    for _ in range(2):
+        m = ef.EFunc(R, th0, deterministic=True)
+        m.mean_shift_init(s)
+        grad = torch.zeros(R ** 3, 13, device="cuda")
+        for q, o in batches:
+            grad.zero_()
+            m.forward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=False)
+            m.backward(grad=grad)
+            m.adamw_step(grad)
+        outs.append(m.get_params())
+    assert np.array_equal(outs[0], outs[1])
