@@ -137,10 +137,19 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
   const int64_t bound = (J + QW - 1) / QW + h->bg.n_codes + 1;
   if (bound > h->items_cap) {
-    dfree(h->loss_part); dfree(h->items);
+    dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n);
     CK(dalloc(&h->loss_part, bound));
     CK(dalloc(&h->items, bound));
+    CK(dalloc(&h->wl_off, bound));
+    CK(dalloc(&h->wl_n, bound));
     h->items_cap = bound;
+  }
+  // forward -> backward candidate-id pool: reserved per item = its brick list length
+  const double want = std::fmin((double)J * WL_PER_QUERY, 3.9e9);
+  if (want > (double)h->wl_cap) {
+    dfree(h->wl_pool);
+    CK(dalloc(&h->wl_pool, (size_t)want));
+    h->wl_cap = (uint32_t)want;
   }
   if (J > h->J_cap) {
     dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
@@ -169,6 +178,7 @@ void free_all(efunc_t* h) {
   dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
+  dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -195,6 +205,7 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->wl_top, 0, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
   const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
   h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
@@ -227,6 +238,10 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   a.us = h->us;
   a.hs = h->hs;
   a.loss_part = h->loss_part;
+  a.wl_pool = h->wl_pool;
+  a.wl_cap = h->wl_cap;
+  a.wl_off = h->wl_off;
+  a.wl_n = h->wl_n;
   a.ds = h->ds;
   a.count_kept = h->count_kept;
   h->launches += launch_forward(a, want_g, items, s);
@@ -267,6 +282,9 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.T_l = cutoff_log2(h->cfg);
   b.gpad = h->gpad;
   b.gfix = h->gfix;
+  b.wl_pool = h->wl_pool;
+  b.wl_off = h->wl_off;
+  b.wl_n = h->wl_n;
   b.umax = &h->ds->umax;
   b.fix_overflow = &h->ds->fix_overflow;
   b.rec = h->rec;

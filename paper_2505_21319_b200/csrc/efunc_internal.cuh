@@ -27,13 +27,14 @@
 
 namespace ef {
 
-constexpr int QW = 32;              // queries per work item (one warp)
+constexpr int QW = 32;              // queries per work item (one warp; the forward supports 64)
 constexpr int NTHREADS = 32;        // one warp per CTA: items retire independently
 constexpr int NWARP = NTHREADS / 32;
 constexpr int BL_CAP = 4096;        // max staged list length per brick (longer: fallback)
 constexpr uint32_t BL_OVERFLOW = 0xffffffffu;
 constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
 constexpr uint32_t QSUB = 8;        // query bins per brick (octants)
+constexpr int WL_PER_QUERY = 64;    // forward->backward candidate pool capacity per query
 constexpr float SKIN_H = 0.25f;     // Verlet skin of the brick lists, in lattice spacings
 constexpr float SKIN_MU = 0.05f;    // allowed relative drift of beta between list builds
 
@@ -63,6 +64,7 @@ struct DevScalars {
   uint32_t ovf_count;      // bricks overflowed in the running build
   uint32_t pool_used;      // entries of the last completed build
   uint32_t ovf_last;       // overflowed bricks of the last completed build
+  uint32_t wl_top;         // per-item candidate-list pool cursor (reset every forward)
   float umax;              // deterministic backward: max_j (|dL/dO_j| + |dL/dG_j|_1) of the call
   uint32_t fix_overflow;   // deterministic backward: a partial left the fixed-point range
   unsigned long long cand_pairs;
@@ -92,6 +94,11 @@ struct FwdArgs {
   float* loss_part;       // per item partial loss
   DevScalars* ds;
   int count_kept;
+  // per-item candidate key ids handed to the backward (reserved: the brick list length)
+  uint32_t* wl_pool;
+  uint32_t wl_cap;
+  uint32_t* wl_off;
+  uint32_t* wl_n;         // BL_OVERFLOW: the backward streams the brick list itself
 };
 
 struct BwdArgs {
@@ -111,6 +118,9 @@ struct BwdArgs {
   float* grad;            // [R^3][13] +=
   int eik;                // 1: add the dL/dG terms
   float* gpad;            // [R^3][16] padded accumulation buffer (zero on entry, zeroed by k_fold)
+  const uint32_t* wl_pool;  // the forward's per-item candidate lists
+  const uint32_t* wl_off;
+  const uint32_t* wl_n;
   // deterministic mode: 64-bit fixed point, value = int * umax * 2^-FIX_BITS (integer adds are
   // associative, so the sum is independent of the order the atomics land in)
   unsigned long long* gfix;  // [R^3][16]
@@ -216,6 +226,10 @@ struct efunc {
   float* loss_part = nullptr;
   int64_t items_cap = 0;
   int4* items = nullptr;            // [items bound]
+  uint32_t* wl_pool = nullptr;      // forward -> backward candidate ids
+  uint32_t wl_cap = 0;
+  uint32_t* wl_off = nullptr;       // [items bound]
+  uint32_t* wl_n = nullptr;         // [items bound]
   int64_t fwd_items_bound = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;

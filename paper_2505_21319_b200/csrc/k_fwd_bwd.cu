@@ -439,6 +439,8 @@ __device__ __forceinline__ void fwd_pair(const float4 q, const float4 a, const f
   }
 }
 
+// Each lane owns up to two queries of the warp item (j = lane and lane + 32): every broadcast
+// key serves both, halving the shared-memory loads and the list stream per pair.
 template <bool WANT_G>
 __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   __shared__ float4 ws_a[NWARP][WSLICE];
@@ -449,23 +451,43 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
   const uint32_t item = blockIdx.x * NWARP + w;
   if (item >= *A.n_items) return;
   const int4 it = A.items[item];
-  const int nact = it.y;  // queries of this warp's item (warps are independent: no block barrier)
-  const bool act = lane < nact;
-  const int64_t js = (int64_t)it.x + lane;
-  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-  float mh = INFINITY, f0 = 0.f;
-  float3 g0 = make_float3(0.f, 0.f, 0.f);
-  if (act) {
-    q = A.qs[js];
-    shift_bound(kv, q, mh, f0, g0);
+  const int nact = it.y;       // queries of this warp's item, <= QW (warps are independent)
+  const bool two = nact > 32;  // warp-uniform: the second query slot is in use
+  bool act[2];
+  int64_t js[2];
+  float4 q[2];
+  float mh[2], f0[2];
+  float3 g0[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    act[u] = lane + 32 * u < nact;
+    js[u] = (int64_t)it.x + lane + 32 * u;
+    q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mh[u] = INFINITY;
+    f0[u] = 0.f;
+    g0[u] = make_float3(0.f, 0.f, 0.f);
+    if (act[u]) {
+      q[u] = A.qs[js[u]];
+      shift_bound(kv, q[u], mh[u], f0[u], g0[u]);
+    }
   }
-  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  Box box = warp_box(act[0], q[0].x, q[0].y, q[0].z, mh[0]);
+  if (two) {
+    const Box b1 = warp_box(act[1], q[1].x, q[1].y, q[1].z, mh[1]);
+    box.lx = fminf(box.lx, b1.lx); box.ly = fminf(box.ly, b1.ly); box.lz = fminf(box.lz, b1.lz);
+    box.hx = fmaxf(box.hx, b1.hx); box.hy = fmaxf(box.hy, b1.hy); box.hz = fmaxf(box.hz, b1.hz);
+    box.thr = fmaxf(box.thr, b1.thr);
+  }
   box.thr += A.T_l;
 
   // mode 0: accumulate with `shift`; 1: exact min of the exponent; 2: count kept pairs
-  FwdAcc s = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  float shift = mh, mexact = INFINITY;
+  const FwdAcc zero = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  FwdAcc s[2] = {zero, zero};
+  float shift[2] = {mh[0], mh[1]};
+  float mexact[2] = {INFINITY, INFINITY};
   unsigned long long cand = 0, kept = 0, kept_off = 0;
+  bool emit = false;
+  uint32_t wl_cnt = 0, wl_base = 0;
   float4* sa = ws_a[w];
   float4* sb = ws_b[w];
   int* sid = ws_id[w];
@@ -474,25 +496,42 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
     auto consume = [&]() {
       __syncwarp();
       if (mode == 0) cand += cnt;
-      if (act) {
-        if (mode == 0) {
-          // register double-buffering of the broadcast key loads hides the LDS latency
-          float4 a0 = sa[0], b0 = sb[0];
-#pragma unroll 4
+      if (mode == 0) {
+        // register double-buffering of the broadcast key loads hides the LDS latency
+        float4 a0 = sa[0], b0 = sb[0];
+        if (two) {
+#pragma unroll 2
           for (uint32_t i = 1; i < cnt; ++i) {
             const float4 a1 = sa[i], b1 = sb[i];
-            fwd_pair<WANT_G>(q, a0, b0, shift, f0, g0, s);
+            fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+            fwd_pair<WANT_G>(q[1], a0, b0, shift[1], f0[1], g0[1], s[1]);
             a0 = a1;
             b0 = b1;
           }
-          fwd_pair<WANT_G>(q, a0, b0, shift, f0, g0, s);
-        } else if (mode == 1) {
-          for (uint32_t i = 0; i < cnt; ++i) mexact = fminf(mexact, exponent(q, sa[i]));
+          fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+          fwd_pair<WANT_G>(q[1], a0, b0, shift[1], f0[1], g0[1], s[1]);
         } else {
-          for (uint32_t i = 0; i < cnt; ++i) {
-            const bool kp = exponent(q, sa[i]) - mexact <= A.T_l;
-            kept += kp ? 1ull : 0ull;
-            kept_off += (kp && sid[i] >= kv.n_nodes) ? 1ull : 0ull;
+#pragma unroll 4
+          for (uint32_t i = 1; i < cnt; ++i) {
+            const float4 a1 = sa[i], b1 = sb[i];
+            fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+            a0 = a1;
+            b0 = b1;
+          }
+          fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+        }
+      } else {
+        for (uint32_t i = 0; i < cnt; ++i) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float e = exponent(q[u], sa[i]);
+            if (mode == 1) {
+              mexact[u] = fminf(mexact[u], e);
+            } else if (act[u]) {
+              const bool kp = e - mexact[u] <= A.T_l;
+              kept += kp ? 1ull : 0ull;
+              kept_off += (kp && sid[i] >= kv.n_nodes) ? 1ull : 0ull;
+            }
           }
         }
       }
@@ -502,30 +541,48 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
     candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
       const uint32_t bal = __ballot_sync(~0u, pass);
       if (pass) {
-        const uint32_t slot = cnt + __popc(bal & lanemask_lt());
+        const uint32_t rank = __popc(bal & lanemask_lt());
+        const uint32_t slot = cnt + rank;
         sa[slot] = a;
         if (mode == 0) sb[slot] = b;
         if (mode == 2) sid[slot] = (int)kp;
+        if (emit) A.wl_pool[wl_base + wl_cnt + rank] = kp;  // hand the candidate set to the backward
       }
       cnt += __popc(bal);
+      wl_cnt += __popc(bal);
       if (cnt >= WSLICE - 32) consume();
     });
     if (cnt) consume();
   };
 
+  // reserve room for this item's candidate ids (at most its brick list) in the hand-off pool
+  uint32_t nb = BL_OVERFLOW;
+  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (lane == 0 && nb != BL_OVERFLOW) wl_base = atomicAdd(&A.ds->wl_top, nb);
+  wl_base = __shfl_sync(~0u, wl_base, 0);
+  emit = (nb != BL_OVERFLOW) && (wl_base + nb <= A.wl_cap);
   run(0);
-  const bool bad = act && !(isfinite(s.Z) && isfinite(s.M) && s.Z > 0.0f);
+  if (lane == 0) {
+    A.wl_off[item] = wl_base;
+    A.wl_n[item] = emit ? wl_cnt : BL_OVERFLOW;
+  }
+  emit = false;
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) bad |= act[u] && !(isfinite(s[u].Z) && isfinite(s[u].M) && s[u].Z > 0.0f);
   if (__any_sync(~0u, bad)) {
     // exact-shift slow path: the warp's candidate set contains every argmin key
     run(1);
-    shift = mexact;
-    s = FwdAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    shift[0] = mexact[0];
+    shift[1] = mexact[1];
+    s[0] = zero;
+    s[1] = zero;
     cand = 0;
     run(0);
     if (lane == 0) atomicAdd(&A.ds->overflow_items, 1u);
   }
   if (A.count_kept) {
-    mexact = INFINITY;
+    mexact[0] = mexact[1] = INFINITY;
     run(1);
     run(2);
     for (int o = 16; o > 0; o >>= 1) {
@@ -541,21 +598,24 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
 
   // epilogue: O, lambda, G, loss and its upstream
   float lossj = 0.0f;
-  if (act) {
-    const float iz = 1.0f / s.Z;
-    const float O = (WANT_G ? f0 : 0.0f) + s.M * iz;
-    const float nlam = shift - log2f(s.Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
-    const int ju = A.perm[js];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!act[u]) continue;
+    const FwdAcc& t = s[u];
+    const float iz = 1.0f / t.Z;
+    const float O = (WANT_G ? f0[u] : 0.0f) + t.M * iz;
+    const float nlam = shift[u] - log2f(t.Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
+    const int ju = A.perm[js[u]];
     float r = 0.0f;
     float Gx = 0.f, Gy = 0.f, Gz = 0.f;
     if (WANT_G) {
       const float c2 = 2.0f * EF_LN2 * iz;
-      const float Of = O - f0;
-      Gx = g0.x + (s.sgx * iz + c2 * fmaf(Of, s.sux, -s.sfx));
-      Gy = g0.y + (s.sgy * iz + c2 * fmaf(Of, s.suy, -s.sfy));
-      Gz = g0.z + (s.sgz * iz + c2 * fmaf(Of, s.suz, -s.sfz));
-      A.gs[js] = make_float4(Gx, Gy, Gz, 0.f);
-      A.us[js] = make_float4(c2 * s.sux, c2 * s.suy, c2 * s.suz, 0.f);
+      const float Of = O - f0[u];
+      Gx = g0[u].x + (t.sgx * iz + c2 * fmaf(Of, t.sux, -t.sfx));
+      Gy = g0[u].y + (t.sgy * iz + c2 * fmaf(Of, t.suy, -t.sfy));
+      Gz = g0[u].z + (t.sgz * iz + c2 * fmaf(Of, t.suz, -t.sfz));
+      A.gs[js[u]] = make_float4(Gx, Gy, Gz, 0.f);
+      A.us[js[u]] = make_float4(c2 * t.sux, c2 * t.suy, c2 * t.suz, 0.f);
       if (A.G) {
         A.G[3 * (size_t)ju] = Gx;
         A.G[3 * (size_t)ju + 1] = Gy;
@@ -563,17 +623,17 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A) {
       }
     }
     if (A.loss_kind >= EFUNC_LOSS_MSE) {
-      const float diff = O - q.w;
+      const float diff = O - q[u].w;
       r = 2.0f * diff * A.inv_J;
-      lossj = diff * diff * A.inv_J;
+      lossj = fmaf(diff * diff, A.inv_J, lossj);
     }
     if (WANT_G && A.loss_kind == EFUNC_LOSS_MSE_EIKONAL) {
       const float nrm = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
       lossj = fmaf(A.eik_lambda * (nrm - 1.0f) * (nrm - 1.0f), A.inv_J, lossj);
       const float sc = nrm > 0.0f ? 2.0f * A.eik_lambda * (nrm - 1.0f) / nrm * A.inv_J : 0.0f;
-      A.hs[js] = make_float4(sc * Gx, sc * Gy, sc * Gz, 0.f);
+      A.hs[js[u]] = make_float4(sc * Gx, sc * Gy, sc * Gz, 0.f);
     }
-    A.rec[js] = make_float4(nlam, r, O, 0.f);
+    A.rec[js[u]] = make_float4(nlam, r, O, 0.f);
     if (A.O) A.O[ju] = O;
   }
   if (A.loss_kind >= EFUNC_LOSS_MSE) {
@@ -607,9 +667,9 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
       atomicOr(A.fix_overflow, 1u);
     }
   };
-  __shared__ float4 sq[NWARP][32];  // x, y, z, -lambda_l
-  __shared__ float4 sv[NWARP][32];  // r, O, h.ubar, h.G
-  __shared__ float4 sh[EIK ? NWARP : 1][32];
+  __shared__ float4 sq[NWARP][QW];  // x, y, z, -lambda_l
+  __shared__ float4 sv[NWARP][QW];  // r, O, h.ubar, h.G
+  __shared__ float4 sh[EIK ? NWARP : 1][EIK ? QW : 1];
   __shared__ float4 ka_s[NWARP][WSLICE];
   __shared__ float4 kb_s[NWARP][WSLICE];
   __shared__ int kid_s[NWARP][WSLICE];
@@ -619,30 +679,42 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   if (item >= *A.n_items) return;
   const int4 it = A.items[item];
   const int nact = it.y;
-  const bool act = lane < nact;
-  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (act) {
-    const int64_t js = (int64_t)it.x + lane;
-    q = A.qs[js];
-    const float4 rc = A.rec[js];
-    const int ju = A.perm[js];
-    const float r = A.dL_dO ? A.dL_dO[ju] : rc.y;
-    float hub = 0.f, T = 0.f;
-    if (EIK) {
-      float4 hv;
-      if (A.dL_dG) hv = make_float4(A.dL_dG[3 * (size_t)ju], A.dL_dG[3 * (size_t)ju + 1], A.dL_dG[3 * (size_t)ju + 2], 0.f);
-      else hv = A.hs[js];
-      const float4 G = A.gs[js], ub = A.us[js];
-      hub = hv.x * ub.x + hv.y * ub.y + hv.z * ub.z;
-      T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
-      sh[w][lane] = hv;
+  Box box;
+#pragma unroll
+  for (int u = 0; u < QW / 32; ++u) {
+    const int j = lane + 32 * u;
+    const bool act = j < nact;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+      const int64_t js = (int64_t)it.x + j;
+      q = A.qs[js];
+      const float4 rc = A.rec[js];
+      const int ju = A.perm[js];
+      const float r = A.dL_dO ? A.dL_dO[ju] : rc.y;
+      float hub = 0.f, T = 0.f;
+      if (EIK) {
+        float4 hv;
+        if (A.dL_dG) hv = make_float4(A.dL_dG[3 * (size_t)ju], A.dL_dG[3 * (size_t)ju + 1], A.dL_dG[3 * (size_t)ju + 2], 0.f);
+        else hv = A.hs[js];
+        const float4 G = A.gs[js], ub = A.us[js];
+        hub = hv.x * ub.x + hv.y * ub.y + hv.z * ub.z;
+        T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
+        sh[w][j] = hv;
+      }
+      q.w = rc.x;
+      sq[w][j] = q;
+      sv[w][j] = make_float4(r, rc.z, hub, T);
     }
-    q.w = rc.x;
-    sq[w][lane] = q;
-    sv[w][lane] = make_float4(r, rc.z, hub, T);
+    // item box with the exact threshold max_j(-lambda_l) + T_l (fallback path only)
+    const Box b = warp_box(act, q.x, q.y, q.z, q.w);
+    if (u == 0) {
+      box = b;
+    } else {
+      box.lx = fminf(box.lx, b.lx); box.ly = fminf(box.ly, b.ly); box.lz = fminf(box.lz, b.lz);
+      box.hx = fmaxf(box.hx, b.hx); box.hy = fmaxf(box.hy, b.hy); box.hz = fmaxf(box.hz, b.hz);
+      box.thr = fmaxf(box.thr, b.thr);
+    }
   }
-  // group box with the exact threshold max_j(-lambda_l) + T_l
-  Box box = warp_box(act, q.x, q.y, q.z, q.w);
   box.thr += A.T_l;
   __syncwarp();
   const float4* Q = sq[w];
@@ -655,14 +727,8 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
   const int n_nodes = kv.n_nodes;
 
   // lanes = keys: lane i takes staged key head + i, loops over the group's queries
-  auto consume = [&](uint32_t head, uint32_t count) {
-    __syncwarp();
-    const bool has = (uint32_t)lane < count;
-    const uint32_t slot = (head + lane) % WSLICE;
-    const float4 a = has ? sa[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 b = has ? sb[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const int id = has ? sid[slot] : 0;
-    __syncwarp();
+  // one key per lane over the item's queries; register accumulators, reds at the end
+  auto process = [&](const bool has, const float4 a, const float4 b, const int id) {
     if (!has) return;
     const float beta = a.w * EF_LN2;
     float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
@@ -766,6 +832,40 @@ __global__ void __launch_bounds__(NTHREADS) k_backward(const BwdArgs A) {
     }
   };
 
+  const uint32_t wn = A.wl_n[item];
+  if (wn != BL_OVERFLOW) {
+    // the forward's candidate ids of this item: one key per lane, records gathered straight into
+    // registers (prefetched one batch ahead); no test, no staging
+    const uint32_t* L = A.wl_pool + A.wl_off[item];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t id1 = ((uint32_t)lane < wn) ? __ldg(&L[lane]) : 0u;
+    float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : z4;
+    float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
+    for (uint32_t base = 0; base < wn; base += 32) {
+      const uint32_t k = base + lane;
+      const bool has = k < wn;
+      const uint32_t id = id1;
+      const float4 a = a1, b = b1;
+      if (k + 32 < wn) {
+        id1 = __ldg(&L[k + 32]);
+        a1 = __ldg(&kv.grid_raw[2 * id1]);
+        b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+      }
+      process(has, a, b, (int)id);
+    }
+    return;
+  }
+  // fallback: stream the brick list (or enumerate) with this item's own test, stage in a ring
+  auto consume = [&](uint32_t head, uint32_t count) {
+    __syncwarp();
+    const bool has = (uint32_t)lane < count;
+    const uint32_t slot = (head + lane) % WSLICE;
+    const float4 a = has ? sa[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = has ? sb[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int id = has ? sid[slot] : 0;
+    __syncwarp();
+    process(has, a, b, id);
+  };
   uint32_t head = 0, cnt = 0;  // ring buffer of staged keys
   candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
     const uint32_t bal = __ballot_sync(~0u, pass);
