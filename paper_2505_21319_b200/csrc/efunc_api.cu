@@ -1,5 +1,5 @@
 // efunc_api.cu — the C ABI (include/efunc.h): handle lifetime, workspaces, call sequencing.
-// Every step of the path runs in the kernels of k_bin.cu / k_fwd_bwd.cu / k_adamw.cu; this
+// Every step of the path runs in the kernels of k_bin.cu / k_lists.cu / k_forward.cu / k_backward.cu / k_adamw.cu; this
 // file only validates arguments, sizes workspaces and enqueues launches on the caller's stream.
 #include <cmath>
 #include <cstring>
@@ -137,8 +137,9 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
   const int64_t bound = (J + QW - 1) / QW + h->bg.n_codes + 1;
   if (bound > h->items_cap) {
-    dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n);
+    dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
     CK(dalloc(&h->loss_part, bound));
+    CK(dalloc(&h->slow_items, bound));
     CK(dalloc(&h->items, bound));
     CK(dalloc(&h->wl_off, bound));
     CK(dalloc(&h->wl_n, bound));
@@ -153,8 +154,9 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   }
   if (J > h->J_cap) {
     dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
-    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
+    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->qmh);
     CK(dalloc(&h->q_bin, J));
+    CK(dalloc(&h->qmh, J));
     CK(dalloc(&h->q_tmp, J));
     CK(dalloc(&h->q_order, J));
     CK(dalloc(&h->qs, J));
@@ -175,10 +177,10 @@ void free_all(efunc_t* h) {
   dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad);
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
-  dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
+  dfree(h->qmh); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
-  dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n);
+  dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -206,6 +208,7 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->wl_top, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->slow_n, 0, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
   const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
   h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
@@ -238,10 +241,12 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   a.us = h->us;
   a.hs = h->hs;
   a.loss_part = h->loss_part;
+  a.qmh = h->qmh;
   a.wl_pool = h->wl_pool;
   a.wl_cap = h->wl_cap;
   a.wl_off = h->wl_off;
   a.wl_n = h->wl_n;
+  a.slow_items = h->slow_items;
   a.ds = h->ds;
   a.count_kept = h->count_kept;
   h->launches += launch_forward(a, want_g, items, s);

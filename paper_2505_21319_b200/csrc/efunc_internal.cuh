@@ -67,6 +67,8 @@ struct DevScalars {
   uint32_t wl_top;         // per-item candidate-list pool cursor (reset every forward)
   float umax;              // deterministic backward: max_j (|dL/dO_j| + |dL/dG_j|_1) of the call
   uint32_t fix_overflow;   // deterministic backward: a partial left the fixed-point range
+  uint32_t slow_n;         // items k_forward_keys left to the exact-min slow path (reset every forward)
+  uint32_t pad_;
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
@@ -92,6 +94,7 @@ struct FwdArgs {
   float4* us;             // sorted ubar (if WANT_G)
   float4* hs;             // sorted fused Eikonal upstream h (if loss eikonal)
   float* loss_part;       // per item partial loss
+  float* qmh;             // sorted shift bound mh_j (k_item_lists -> k_forward_keys)
   DevScalars* ds;
   int count_kept;
   // per-item candidate key ids handed to the backward (reserved: the brick list length)
@@ -99,6 +102,7 @@ struct FwdArgs {
   uint32_t wl_cap;
   uint32_t* wl_off;
   uint32_t* wl_n;         // BL_OVERFLOW: the backward streams the brick list itself
+  uint32_t* slow_items;   // items whose shift bound overflowed (ds->slow_n of them)
 };
 
 struct BwdArgs {
@@ -224,12 +228,14 @@ struct efunc {
   float4* us = nullptr;
   float4* hs = nullptr;
   float* loss_part = nullptr;
+  float* qmh = nullptr;
   int64_t items_cap = 0;
   int4* items = nullptr;            // [items bound]
   uint32_t* wl_pool = nullptr;      // forward -> backward candidate ids
   uint32_t wl_cap = 0;
   uint32_t* wl_off = nullptr;       // [items bound]
   uint32_t* wl_n = nullptr;         // [items bound]
+  uint32_t* slow_items = nullptr;   // [items bound]
   int64_t fwd_items_bound = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;

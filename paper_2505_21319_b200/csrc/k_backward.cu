@@ -1,0 +1,381 @@
+// k_backward.cu — S4 backward: lanes = the item's candidate keys, the item's queries
+// broadcast from shared memory, register accumulators (Alg. 2); per (key,
+// item) two red.global.add.v4.f32 into a 16-float-per-node padded gradient folded to the ABI
+// layout by k_fold, or 64-bit fixed-point atomics in deterministic mode.
+#include "k_common.cuh"
+
+namespace ef {
+
+// ------------------------------------------------------------------------------ backward
+// DET: deterministic mode, 64-bit fixed-point accumulation (see BwdArgs::gfix)
+#ifndef BK_MIN_BLOCKS
+#define BK_MIN_BLOCKS 28  // <= 72 registers (measured best of 1/28/32)
+#endif
+template <bool EIK, bool DET>
+__global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdArgs A) {
+  float fix_scale = 0.0f;
+  if (DET) {
+    const float um = *A.umax;
+    fix_scale = um > 0.0f ? (float)(1ull << FIX_BITS) / um : 0.0f;
+  }
+  auto fix_add = [&](unsigned long long* p, float v) {
+    const float qv = v * fix_scale;
+    if (fabsf(qv) < 4.0e18f) {
+      atomicAdd(p, (unsigned long long)(long long)rintf(qv));
+    } else {
+      atomicOr(A.fix_overflow, 1u);
+    }
+  };
+  __shared__ float4 sq[NWARP][QW];  // x, y, z, -lambda_l
+  __shared__ float4 sv[NWARP][QW];  // r, O, h.ubar, h.G
+  __shared__ float4 sh[EIK ? NWARP : 1][EIK ? QW : 1];
+  // MSE: the item's queries as packed pairs for f32x2 arithmetic: {x0,x1,y0,y1}, {z0,z1,w0,w1},
+  // {r0,r1,-O0,-O1} (an idle slot has w = -inf and r = 0: it contributes exactly 0)
+  static_assert(NWARP == 1, "packed query pairs assume one warp per CTA");
+  __shared__ float4 pA[EIK ? 1 : QW / 2], pB[EIK ? 1 : QW / 2], pC[EIK ? 1 : QW / 2];
+  __shared__ float4 ka_s[NWARP][WSLICE];
+  __shared__ float4 kb_s[NWARP][WSLICE];
+  __shared__ int kid_s[NWARP][WSLICE];
+  const KeysView& kv = A.kv;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t item = blockIdx.x * NWARP + w;
+  if (item >= *A.n_items) return;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  Box box;
+#pragma unroll
+  for (int u = 0; u < QW / 32; ++u) {
+    const int j = lane + 32 * u;
+    const bool act = j < nact;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+      const int64_t js = (int64_t)it.x + j;
+      q = A.qs[js];
+      const float4 rc = A.rec[js];
+      const int ju = A.perm[js];
+      const float r = A.dL_dO ? A.dL_dO[ju] : rc.y;
+      float hub = 0.f, T = 0.f;
+      if (EIK) {
+        float4 hv;
+        if (A.dL_dG) hv = make_float4(A.dL_dG[3 * (size_t)ju], A.dL_dG[3 * (size_t)ju + 1], A.dL_dG[3 * (size_t)ju + 2], 0.f);
+        else hv = A.hs[js];
+        const float4 G = A.gs[js], ub = A.us[js];
+        hub = hv.x * ub.x + hv.y * ub.y + hv.z * ub.z;
+        T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
+        sh[w][j] = hv;
+      }
+      q.w = rc.x;
+      sq[w][j] = q;
+      sv[w][j] = make_float4(r, rc.z, hub, T);
+    }
+    if (!EIK) {
+      const float x = q.x, y = q.y, z = q.z, wv = act ? q.w : -INFINITY;
+      const float r = act ? sv[w][j].x : 0.f, nO = act ? -sv[w][j].y : 0.f;
+      const float xo = __shfl_xor_sync(~0u, x, 1), yo = __shfl_xor_sync(~0u, y, 1), zo = __shfl_xor_sync(~0u, z, 1);
+      const float wo = __shfl_xor_sync(~0u, wv, 1), ro = __shfl_xor_sync(~0u, r, 1), nOo = __shfl_xor_sync(~0u, nO, 1);
+      if ((lane & 1) == 0) {
+        pA[j >> 1] = make_float4(x, xo, y, yo);
+        pB[j >> 1] = make_float4(z, zo, wv, wo);
+        pC[j >> 1] = make_float4(r, ro, nO, nOo);
+      }
+    }
+    // item box with the exact threshold max_j(-lambda_l) + T_l (fallback path only)
+    const Box b = warp_box(act, q.x, q.y, q.z, q.w);
+    if (u == 0) {
+      box = b;
+    } else {
+      box.lx = fminf(box.lx, b.lx); box.ly = fminf(box.ly, b.ly); box.lz = fminf(box.lz, b.lz);
+      box.hx = fmaxf(box.hx, b.hx); box.hy = fmaxf(box.hy, b.hy); box.hz = fmaxf(box.hz, b.hz);
+      box.thr = fmaxf(box.thr, b.thr);
+    }
+  }
+  box.thr += A.T_l;
+  __syncwarp();
+  const float4* Q = sq[w];
+  const float4* V = sv[w];
+  const float4* H = sh[EIK ? w : 0];
+  float4* sa = ka_s[w];
+  float4* sb = kb_s[w];
+  int* sid = kid_s[w];
+  float* gpad = A.gpad;
+  const int n_nodes = kv.n_nodes;
+
+  // lanes = keys: lane i takes staged key head + i, loops over the group's queries
+  // one key per lane over the item's queries; register accumulators, reds at the end
+  auto process = [&](const bool has, const float4 a, const float4 b, const int id) {
+    if (!has) return;
+    const float beta = a.w * EF_LN2;
+    float sc = 0.f, sgx = 0.f, sgy = 0.f, sgz = 0.f, ss = 0.f, sdx = 0.f, sdy = 0.f, sdz = 0.f;
+    float phx = 0.f, phy = 0.f, phz = 0.f, pdx = 0.f, pdy = 0.f, pdz = 0.f;  // EIK only
+    auto pair = [&](const float4 P, const float4 U, const float4 h) {
+      const float dx = P.x - a.x, dy = P.y - a.y, dz = P.z - a.z;
+      const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float p = ex2f(fmaf(-a.w, dd, P.w));
+      const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+      const float del = f - U.y;
+      if (!EIK) {
+        // Alg. 2: dO/dc = p, dO/dg = p d, dO/ds = -p a (f - O), dO/dk = p(-g + 2 beta d (f - O))
+        const float t = U.x * p;
+        const float u = t * del;
+        sc += t;
+        sgx = fmaf(t, dx, sgx);
+        sgy = fmaf(t, dy, sgy);
+        sgz = fmaf(t, dz, sgz);
+        ss = fmaf(u, dd, ss);
+        sdx = fmaf(u, dx, sdx);
+        sdy = fmaf(u, dy, sdy);
+        sdz = fmaf(u, dz, sdz);
+      } else {
+        // MSE + second-order (dL/dG) terms, DESIGN.md "Eikonal backward"
+        const float hd = fmaf(h.x, dx, fmaf(h.y, dy, h.z * dz));
+        const float hu = 2.0f * beta * hd;
+        const float hg = fmaf(h.x, b.y, fmaf(h.y, b.z, h.z * b.w));
+        const float tt = fmaf(-hu, del, hg);
+        const float alpha = U.x + U.z - hu;
+        const float gam = fmaf(U.x + U.z, del, tt - U.w);
+        const float pa = p * alpha;
+        sc += pa;
+        sgx = fmaf(pa, dx, sgx);
+        sgy = fmaf(pa, dy, sgy);
+        sgz = fmaf(pa, dz, sgz);
+        phx = fmaf(p, h.x, phx);
+        phy = fmaf(p, h.y, phy);
+        phz = fmaf(p, h.z, phz);
+        ss = fmaf(p, fmaf(beta * dd, gam, hu * del), ss);
+        const float pg = p * gam;
+        sdx = fmaf(pg, dx, sdx);
+        sdy = fmaf(pg, dy, sdy);
+        sdz = fmaf(pg, dz, sdz);
+        const float pdel = p * del;
+        pdx = fmaf(pdel, h.x, pdx);
+        pdy = fmaf(pdel, h.y, pdy);
+        pdz = fmaf(pdel, h.z, pdz);
+      }
+    };
+    if (!EIK) {
+      // two queries per f32x2 instruction; the halves are summed at the end
+      const float2 nx = make_float2(-a.x, -a.x), ny = make_float2(-a.y, -a.y), nz = make_float2(-a.z, -a.z);
+      const float2 nbl = make_float2(-a.w, -a.w);
+      const float2 c2 = make_float2(b.x, b.x), gx2 = make_float2(b.y, b.y), gy2 = make_float2(b.z, b.z),
+                   gz2 = make_float2(b.w, b.w);
+      float2 Sc = make_float2(0.f, 0.f), Sgx = Sc, Sgy = Sc, Sgz = Sc, Ss = Sc, Sdx = Sc, Sdy = Sc, Sdz = Sc;
+      const int npairs = (nact + 1) >> 1;
+#pragma unroll 2
+      for (int jp = 0; jp < npairs; ++jp) {
+        const float4 QA = pA[jp], QB = pB[jp], QC = pC[jp];
+        const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), nx);
+        const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), ny);
+        const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), nz);
+        float2 dd = __fmul2_rn(dz, dz);
+        dd = __ffma2_rn(dy, dy, dd);
+        dd = __ffma2_rn(dx, dx, dd);
+        const float2 e = __ffma2_rn(nbl, dd, make_float2(QB.z, QB.w));
+        const float2 p = make_float2(ex2f(e.x), ex2f(e.y));
+        float2 f = __ffma2_rn(gx2, dx, c2);
+        f = __ffma2_rn(gy2, dy, f);
+        f = __ffma2_rn(gz2, dz, f);
+        const float2 del = __fadd2_rn(f, make_float2(QC.z, QC.w));
+        const float2 t = __fmul2_rn(make_float2(QC.x, QC.y), p);
+        const float2 u = __fmul2_rn(t, del);
+        Sc = __fadd2_rn(Sc, t);
+        Sgx = __ffma2_rn(t, dx, Sgx);
+        Sgy = __ffma2_rn(t, dy, Sgy);
+        Sgz = __ffma2_rn(t, dz, Sgz);
+        Ss = __ffma2_rn(u, dd, Ss);
+        Sdx = __ffma2_rn(u, dx, Sdx);
+        Sdy = __ffma2_rn(u, dy, Sdy);
+        Sdz = __ffma2_rn(u, dz, Sdz);
+      }
+      sc = Sc.x + Sc.y; sgx = Sgx.x + Sgx.y; sgy = Sgy.x + Sgy.y; sgz = Sgz.x + Sgz.y;
+      ss = Ss.x + Ss.y; sdx = Sdx.x + Sdx.y; sdy = Sdy.x + Sdy.y; sdz = Sdz.x + Sdz.y;
+    } else {
+      // register double-buffering of the broadcast query loads hides the LDS latency
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 P0 = Q[0], U0 = V[0], H0 = EIK ? H[0] : z4;
+#pragma unroll 4
+      for (int j = 1; j < nact; ++j) {
+        const float4 P1 = Q[j], U1 = V[j], H1 = EIK ? H[j] : z4;
+        pair(P0, U0, H0);
+        P0 = P1;
+        U0 = U1;
+        H0 = H1;
+      }
+      pair(P0, U0, H0);
+    }
+    float dsv, dgx, dgy, dgz;
+    if (!EIK) {
+      dsv = -beta * ss;
+      dgx = sgx; dgy = sgy; dgz = sgz;
+    } else {
+      dsv = -ss;
+      dgx = sgx + phx; dgy = sgy + phy; dgz = sgz + phz;
+    }
+    // padded gradient: node n -> 16 floats {s0,c0,g0x,g0y | g0z,-,-,- | dx,dy,dz,s1 | c1,g1x,g1y,g1z}
+    if (id < n_nodes) {
+      if (!DET) {
+        float* gp = gpad + (size_t)id * 16;
+        red_v4(gp, dsv, sc, dgx, dgy);
+        atomicAdd(gp + 4, dgz);
+      } else {
+        unsigned long long* gp = A.gfix + (size_t)id * 16;
+        fix_add(gp + 0, dsv); fix_add(gp + 1, sc); fix_add(gp + 2, dgx); fix_add(gp + 3, dgy);
+        fix_add(gp + 4, dgz);
+      }
+    } else {
+      float dkx, dky, dkz;
+      if (!EIK) {
+        dkx = fmaf(-b.y, sc, 2.0f * beta * sdx);
+        dky = fmaf(-b.z, sc, 2.0f * beta * sdy);
+        dkz = fmaf(-b.w, sc, 2.0f * beta * sdz);
+      } else {
+        dkx = fmaf(-b.y, sc, 2.0f * beta * (sdx + pdx));
+        dky = fmaf(-b.z, sc, 2.0f * beta * (sdy + pdy));
+        dkz = fmaf(-b.w, sc, 2.0f * beta * (sdz + pdz));
+      }
+      if (!DET) {
+        float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
+        red_v4(gp, dkx, dky, dkz, dsv);
+        red_v4(gp + 4, sc, dgx, dgy, dgz);
+      } else {
+        unsigned long long* gp = A.gfix + (size_t)(id - n_nodes) * 16 + 8;
+        fix_add(gp + 0, dkx); fix_add(gp + 1, dky); fix_add(gp + 2, dkz); fix_add(gp + 3, dsv);
+        fix_add(gp + 4, sc); fix_add(gp + 5, dgx); fix_add(gp + 6, dgy); fix_add(gp + 7, dgz);
+      }
+    }
+  };
+
+  const uint32_t wn = A.wl_n[item];
+  if (wn != BL_OVERFLOW) {
+    // the forward's candidate ids of this item: one key per lane, records gathered straight into
+    // registers; ids prefetched two batches ahead and records one batch ahead, so neither
+    // gather waits on a load issued just before it; no test, no staging
+    const uint32_t* L = A.wl_pool + A.wl_off[item];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t id1 = ((uint32_t)lane < wn) ? __ldg(&L[lane]) : 0u;
+    uint32_t id2 = ((uint32_t)lane + 32 < wn) ? __ldg(&L[lane + 32]) : 0u;
+    float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : z4;
+    float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
+    for (uint32_t base = 0; base < wn; base += 32) {
+      const uint32_t k = base + lane;
+      const bool has = k < wn;
+      const uint32_t id = id1;
+      const float4 a = a1, b = b1;
+      id1 = id2;
+      id2 = (k + 64 < wn) ? __ldg(&L[k + 64]) : 0u;
+      if (k + 32 < wn) {
+        a1 = __ldg(&kv.grid_raw[2 * id1]);
+        b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+      }
+      process(has, a, b, (int)id);
+    }
+    return;
+  }
+  // fallback: stream the brick list (or enumerate) with this item's own test, stage in a ring
+  auto consume = [&](uint32_t head, uint32_t count) {
+    __syncwarp();
+    const bool has = (uint32_t)lane < count;
+    const uint32_t slot = (head + lane) % WSLICE;
+    const float4 a = has ? sa[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = has ? sb[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int id = has ? sid[slot] : 0;
+    __syncwarp();
+    process(has, a, b, id);
+  };
+  uint32_t head = 0, cnt = 0;  // ring buffer of staged keys
+  candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) {
+      const uint32_t slot = (head + cnt + __popc(bal & lanemask_lt())) % WSLICE;
+      sa[slot] = a;
+      sb[slot] = b;
+      sid[slot] = (int)kp;
+    }
+    cnt += __popc(bal);
+    if (cnt >= 32) {
+      consume(head, 32);
+      head = (head + 32) % WSLICE;
+      cnt -= 32;
+    }
+  });
+  if (cnt) consume(head, cnt);
+}
+
+int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (a.eik) k_backward<true, false><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_backward<false, false><<<blocks, NTHREADS, 0, s>>>(a);
+  return 1;
+}
+
+// max_j (|dL/dO_j| + |dL/dG_j|_1): the fixed-point unit of the deterministic backward (a max is
+// independent of the order the atomics land in)
+__global__ void k_upstream_max(const BwdArgs A, float* umax) {
+  float m = 0.0f;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.J; j += (int64_t)gridDim.x * blockDim.x) {
+    float v = fabsf(A.dL_dO ? A.dL_dO[j] : A.rec[j].y);
+    if (A.eik) {
+      if (A.dL_dG) v += fabsf(A.dL_dG[3 * j]) + fabsf(A.dL_dG[3 * j + 1]) + fabsf(A.dL_dG[3 * j + 2]);
+      else v += fabsf(A.hs[j].x) + fabsf(A.hs[j].y) + fabsf(A.hs[j].z);
+    }
+    m = fmaxf(m, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(~0u, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(umax), __float_as_uint(m));
+}
+
+int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  long ub = (a.J + 255) / 256;
+  if (ub > 148 * 8) ub = 148 * 8;
+  k_upstream_max<<<(unsigned)(ub < 1 ? 1 : ub), 256, 0, s>>>(a, const_cast<float*>(a.umax));
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (a.eik) k_backward<true, true><<<blocks, NTHREADS, 0, s>>>(a);
+  else k_backward<false, true><<<blocks, NTHREADS, 0, s>>>(a);
+  return 2;
+}
+
+// grad[n][13] += fixed-point sums * umax * 2^-FIX_BITS; zero the accumulator
+__global__ void k_fold_fix(unsigned long long* __restrict__ gfix, const float* __restrict__ umax,
+                           float* __restrict__ grad, int n_nodes) {
+  const double unit = (double)*umax / (double)(1ull << FIX_BITS);
+  const int map[13] = {0, 1, 2, 3, 4, 8, 9, 10, 11, 12, 13, 14, 15};
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    unsigned long long* p = gfix + (size_t)n * 16;
+    float* g = grad + (size_t)n * EF_NCH;
+#pragma unroll
+    for (int c = 0; c < 13; ++c) g[c] += (float)((double)(long long)p[map[c]] * unit);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) p[c] = 0ull;
+  }
+}
+
+int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, int n_nodes, cudaStream_t s) {
+  int blocks = (n_nodes + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_fold_fix<<<blocks, 256, 0, s>>>(gfix, umax, grad, n_nodes);
+  return 1;
+}
+
+// grad[n][13] += padded gradient (channel map above); zero the padded buffer for the next call
+__global__ void k_fold(float* __restrict__ gpad, float* __restrict__ grad, int n_nodes) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    float4* p = reinterpret_cast<float4*>(gpad + (size_t)n * 16);
+    const float4 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
+    float* g = grad + (size_t)n * EF_NCH;
+    g[0] += v0.x; g[1] += v0.y; g[2] += v0.z; g[3] += v0.w; g[4] += v1.x;
+    g[5] += v2.x; g[6] += v2.y; g[7] += v2.z; g[8] += v2.w;
+    g[9] += v3.x; g[10] += v3.y; g[11] += v3.z; g[12] += v3.w;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    p[0] = z; p[1] = z; p[2] = z; p[3] = z;
+  }
+}
+
+int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s) {
+  int blocks = (n_nodes + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_fold<<<blocks, 256, 0, s>>>(gpad, grad, n_nodes);
+  return 1;
+}
+
+}  // namespace ef

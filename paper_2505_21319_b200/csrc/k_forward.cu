@@ -1,0 +1,512 @@
+// k_forward.cu — S2/S3 forward (+ loss epilogue).
+//
+// A work item is up to QW queries of one brick (sorted by brick and octant). A warp streams the
+// brick's candidate list (k_lists.cu), keeps key k iff bl_k * dist^2(k, item AABB) <= thr with
+// thr = max_j mh_j + T_l, where mh_j >= m_j is the exponent of the best key among the query's 8
+// lattice corners and its own cell (the shift of the paper's "maximum-reduce").
+// Every skipped pair has a - m_j > cutoff_T (reading R-1). The kept ids are handed to
+// the backward (wl lists).
+//   k_forward_keys (value-only forward, the fit step's): lanes = compacted candidate keys, the
+//     item's queries broadcast from shared memory two per packed f32x2 instruction, per-query
+//     partial sums in registers, one transpose-reduction per item (Alg. 1).
+//   k_forward (G forward, exact-min slow path, kept-pair census): lanes = queries, staged keys
+//     broadcast (Alg. 1 and the G sums of Eq. func-normal).
+#include "k_common.cuh"
+
+namespace ef {
+
+// ------------------------------------------------------------------------------ forward
+struct FwdAcc {
+  float Z, M, sgx, sgy, sgz, sux, suy, suz, sfx, sfy, sfz;
+};
+
+template <bool WANT_G>
+__device__ __forceinline__ void fwd_pair(const float4 q, const float4 a, const float4 b, float shift, float f0,
+                                         const float3 g0, FwdAcc& s) {
+  const float dx = q.x - a.x, dy = q.y - a.y, dz = q.z - a.z;
+  const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float wgt = ex2f(fmaf(-a.w, dd, shift));
+  s.Z += wgt;
+  if (WANT_G) {
+    const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x - f0)));
+    s.sgx = fmaf(wgt, b.y - g0.x, s.sgx);  // relative to the shift key's g (accuracy)
+    s.sgy = fmaf(wgt, b.z - g0.y, s.sgy);
+    s.sgz = fmaf(wgt, b.w - g0.z, s.sgz);
+    const float wbl = wgt * a.w;
+    s.sux = fmaf(wbl, dx, s.sux);
+    s.suy = fmaf(wbl, dy, s.suy);
+    s.suz = fmaf(wbl, dz, s.suz);
+    const float wbf = wbl * f;
+    s.sfx = fmaf(wbf, dx, s.sfx);
+    s.sfy = fmaf(wbf, dy, s.sfy);
+    s.sfz = fmaf(wbf, dz, s.sfz);
+    s.M = fmaf(wgt, f, s.M);
+  } else {
+    const float f = fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x)));
+    s.M = fmaf(wgt, f, s.M);
+  }
+}
+
+// Each lane owns up to two queries of the warp item (j = lane and lane + 32): every broadcast
+// key serves both, halving the shared-memory loads and the list stream per pair.
+template <bool WANT_G>
+__device__ __forceinline__ void forward_item(const FwdArgs& A, const uint32_t item) {
+  __shared__ float4 ws_a[NWARP][WSLICE];
+  __shared__ float4 ws_b[NWARP][WSLICE];
+  __shared__ int ws_id[NWARP][WSLICE];
+  const KeysView& kv = A.kv;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int4 it = A.items[item];
+  const int nact = it.y;       // queries of this warp's item, <= QW (warps are independent)
+  const bool two = nact > 32;  // warp-uniform: the second query slot is in use
+  bool act[2];
+  int64_t js[2];
+  float4 q[2];
+  float mh[2], f0[2];
+  float3 g0[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    act[u] = lane + 32 * u < nact;
+    js[u] = (int64_t)it.x + lane + 32 * u;
+    q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mh[u] = INFINITY;
+    f0[u] = 0.f;
+    g0[u] = make_float3(0.f, 0.f, 0.f);
+    if (act[u]) {
+      q[u] = A.qs[js[u]];
+      shift_bound(kv, q[u], mh[u], f0[u], g0[u]);
+    }
+  }
+  Box box = warp_box(act[0], q[0].x, q[0].y, q[0].z, mh[0]);
+  if (two) {
+    const Box b1 = warp_box(act[1], q[1].x, q[1].y, q[1].z, mh[1]);
+    box.lx = fminf(box.lx, b1.lx); box.ly = fminf(box.ly, b1.ly); box.lz = fminf(box.lz, b1.lz);
+    box.hx = fmaxf(box.hx, b1.hx); box.hy = fmaxf(box.hy, b1.hy); box.hz = fmaxf(box.hz, b1.hz);
+    box.thr = fmaxf(box.thr, b1.thr);
+  }
+  box.thr += A.T_l;
+
+  // mode 0: accumulate with `shift`; 1: exact min of the exponent; 2: count kept pairs
+  const FwdAcc zero = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  FwdAcc s[2] = {zero, zero};
+  float shift[2] = {mh[0], mh[1]};
+  float mexact[2] = {INFINITY, INFINITY};
+  unsigned long long cand = 0, kept = 0, kept_off = 0;
+  bool emit = false;
+  uint32_t wl_cnt = 0, wl_base = 0;
+  float4* sa = ws_a[w];
+  float4* sb = ws_b[w];
+  int* sid = ws_id[w];
+  auto run = [&](const int mode) {
+    uint32_t cnt = 0;
+    auto consume = [&]() {
+      __syncwarp();
+      if (mode == 0) cand += cnt;
+      if (mode == 0) {
+        // register double-buffering of the broadcast key loads hides the LDS latency
+        float4 a0 = sa[0], b0 = sb[0];
+        if (two) {
+#pragma unroll 2
+          for (uint32_t i = 1; i < cnt; ++i) {
+            const float4 a1 = sa[i], b1 = sb[i];
+            fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+            fwd_pair<WANT_G>(q[1], a0, b0, shift[1], f0[1], g0[1], s[1]);
+            a0 = a1;
+            b0 = b1;
+          }
+          fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+          fwd_pair<WANT_G>(q[1], a0, b0, shift[1], f0[1], g0[1], s[1]);
+        } else {
+#pragma unroll 4
+          for (uint32_t i = 1; i < cnt; ++i) {
+            const float4 a1 = sa[i], b1 = sb[i];
+            fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+            a0 = a1;
+            b0 = b1;
+          }
+          fwd_pair<WANT_G>(q[0], a0, b0, shift[0], f0[0], g0[0], s[0]);
+        }
+      } else {
+        for (uint32_t i = 0; i < cnt; ++i) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float e = exponent(q[u], sa[i]);
+            if (mode == 1) {
+              mexact[u] = fminf(mexact[u], e);
+            } else if (act[u]) {
+              const bool kp = e - mexact[u] <= A.T_l;
+              kept += kp ? 1ull : 0ull;
+              kept_off += (kp && sid[i] >= kv.n_nodes) ? 1ull : 0ull;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      cnt = 0;
+    };
+    candidates(kv, it.z, box, [&](bool pass, uint32_t kp, float4 a, float4 b) {
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      if (pass) {
+        const uint32_t rank = __popc(bal & lanemask_lt());
+        const uint32_t slot = cnt + rank;
+        sa[slot] = a;
+        if (mode == 0) sb[slot] = b;
+        if (mode == 2) sid[slot] = (int)kp;
+        if (emit) A.wl_pool[wl_base + wl_cnt + rank] = kp;  // hand the candidate set to the backward
+      }
+      cnt += __popc(bal);
+      wl_cnt += __popc(bal);
+      if (cnt >= WSLICE - 32) consume();
+    });
+    if (cnt) consume();
+  };
+
+  // reserve room for this item's candidate ids (at most its brick list) in the hand-off pool
+  uint32_t nb = BL_OVERFLOW;
+  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (lane == 0 && nb != BL_OVERFLOW) wl_base = atomicAdd(&A.ds->wl_top, nb);
+  wl_base = __shfl_sync(~0u, wl_base, 0);
+  emit = (nb != BL_OVERFLOW) && (wl_base + nb <= A.wl_cap);
+  run(0);
+  if (lane == 0) {
+    A.wl_off[item] = wl_base;
+    A.wl_n[item] = emit ? wl_cnt : BL_OVERFLOW;
+  }
+  emit = false;
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) bad |= act[u] && !(isfinite(s[u].Z) && isfinite(s[u].M) && s[u].Z > 0.0f);
+  if (__any_sync(~0u, bad)) {
+    // exact-shift slow path: the warp's candidate set contains every argmin key
+    run(1);
+    shift[0] = mexact[0];
+    shift[1] = mexact[1];
+    s[0] = zero;
+    s[1] = zero;
+    cand = 0;
+    run(0);
+    if (lane == 0) atomicAdd(&A.ds->overflow_items, 1u);
+  }
+  if (A.count_kept) {
+    mexact[0] = mexact[1] = INFINITY;
+    run(1);
+    run(2);
+    for (int o = 16; o > 0; o >>= 1) {
+      kept += __shfl_xor_sync(~0u, kept, o);
+      kept_off += __shfl_xor_sync(~0u, kept_off, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&A.ds->kept_pairs, kept);
+      atomicAdd(&A.ds->kept_pairs_offset, kept_off);
+    }
+  }
+  if (lane == 0) atomicAdd(&A.ds->cand_pairs, cand * (unsigned long long)nact);
+
+  // epilogue: O, lambda, G, loss and its upstream
+  float lossj = 0.0f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!act[u]) continue;
+    const FwdAcc& t = s[u];
+    const float iz = 1.0f / t.Z;
+    const float O = (WANT_G ? f0[u] : 0.0f) + t.M * iz;
+    const float nlam = shift[u] - log2f(t.Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
+    const int ju = A.perm[js[u]];
+    float r = 0.0f;
+    float Gx = 0.f, Gy = 0.f, Gz = 0.f;
+    if (WANT_G) {
+      const float c2 = 2.0f * EF_LN2 * iz;
+      const float Of = O - f0[u];
+      Gx = g0[u].x + (t.sgx * iz + c2 * fmaf(Of, t.sux, -t.sfx));
+      Gy = g0[u].y + (t.sgy * iz + c2 * fmaf(Of, t.suy, -t.sfy));
+      Gz = g0[u].z + (t.sgz * iz + c2 * fmaf(Of, t.suz, -t.sfz));
+      A.gs[js[u]] = make_float4(Gx, Gy, Gz, 0.f);
+      A.us[js[u]] = make_float4(c2 * t.sux, c2 * t.suy, c2 * t.suz, 0.f);
+      if (A.G) {
+        A.G[3 * (size_t)ju] = Gx;
+        A.G[3 * (size_t)ju + 1] = Gy;
+        A.G[3 * (size_t)ju + 2] = Gz;
+      }
+    }
+    if (A.loss_kind >= EFUNC_LOSS_MSE) {
+      const float diff = O - q[u].w;
+      r = 2.0f * diff * A.inv_J;
+      lossj = fmaf(diff * diff, A.inv_J, lossj);
+    }
+    if (WANT_G && A.loss_kind == EFUNC_LOSS_MSE_EIKONAL) {
+      const float nrm = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
+      lossj = fmaf(A.eik_lambda * (nrm - 1.0f) * (nrm - 1.0f), A.inv_J, lossj);
+      const float sc = nrm > 0.0f ? 2.0f * A.eik_lambda * (nrm - 1.0f) / nrm * A.inv_J : 0.0f;
+      A.hs[js[u]] = make_float4(sc * Gx, sc * Gy, sc * Gz, 0.f);
+    }
+    A.rec[js[u]] = make_float4(nlam, r, O, 0.f);
+    if (A.O) A.O[ju] = O;
+  }
+  if (A.loss_kind >= EFUNC_LOSS_MSE) {
+    for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
+    if (lane == 0) A.loss_part[item] = lossj;
+  }
+}
+
+// from_list: the items flagged by k_forward_keys (ds->slow_n of them in A.slow_items), grid-strided
+template <bool WANT_G>
+__global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A, const int from_list) {
+  if (!from_list) {
+    const uint32_t item = blockIdx.x * NWARP + (threadIdx.x >> 5);
+    if (item < *A.n_items) forward_item<WANT_G>(A, item);
+    return;
+  }
+  const uint32_t n = *(volatile uint32_t*)&A.ds->slow_n;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) forward_item<WANT_G>(A, A.slow_items[i]);
+}
+
+// ------------------------------------------------------------------ forward, lanes = keys
+// Reduce-scatter of N per-lane values over the warp: afterwards lane l holds in v[0 .. N/32) the
+// warp totals of values [l N/32, (l+1) N/32) (N = 32 or 64). 31 (N=32) / 62 (N=64) shuffles.
+template <int N>
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[N], const int lane) {
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int o = 16 >> st;
+    const int c = N >> (st + 1);  // values kept after this step (compile-time once unrolled)
+    if (c >= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < c; ++i) {
+        const float send = up ? v[i] : v[i + c];
+        const float keep = up ? v[i + c] : v[i];
+        v[i] = keep + __shfl_xor_sync(~0u, send, o);
+      }
+    } else {
+      v[0] += __shfl_xor_sync(~0u, v[0], o);
+    }
+  }
+}
+
+// S2a (value-only forward, part 1): per item, the shift bounds mh_j and the compacted candidate
+// ids (the item's warp-box test over its brick list) written to the item's slice of wl_pool.
+// Latency-bound gathers: few registers and 4 independent warps per CTA for occupancy.
+constexpr int IL_WARPS = 4;
+__global__ void __launch_bounds__(32 * IL_WARPS) k_item_lists(const FwdArgs A) {
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const uint32_t item = blockIdx.x * IL_WARPS + (threadIdx.x >> 5);
+  if (item >= *A.n_items) return;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY, f0 = 0.f;
+  float3 g0 = make_float3(0.f, 0.f, 0.f);
+  if (act) {
+    q = A.qs[js];
+    shift_bound(kv, q, mh, f0, g0);
+    A.qmh[js] = mh;
+  }
+  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  box.thr += A.T_l;
+  // reserve room for this item's candidate ids (at most its brick list)
+  uint32_t nb = BL_OVERFLOW, wl_base = 0;
+  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (lane == 0 && nb != BL_OVERFLOW) wl_base = atomicAdd(&A.ds->wl_top, nb);
+  wl_base = __shfl_sync(~0u, wl_base, 0);
+  if (nb == BL_OVERFLOW || wl_base + nb > A.wl_cap) {
+    if (lane == 0) {  // no list: k_forward (slow list) and the backward's fallback stream handle it
+      A.wl_off[item] = 0;
+      A.wl_n[item] = BL_OVERFLOW;
+    }
+    return;
+  }
+  uint32_t cnt = 0;
+  uint32_t* out = A.wl_pool + wl_base;
+  stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t kp) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) out[cnt + __popc(bal & lanemask_lt())] = kp;
+    cnt += __popc(bal);
+  });
+  if (lane == 0) {
+    A.wl_off[item] = wl_base;
+    A.wl_n[item] = cnt;
+    atomicAdd(&A.ds->cand_pairs, (unsigned long long)cnt * (unsigned long long)nact);
+  }
+}
+
+// S2b (value-only forward, part 2): lanes = the item's candidate keys (its wl list, ids two
+// rounds ahead, records one round ahead), the item's queries broadcast from shared memory as
+// packed pairs (f32x2: two queries per instruction), per-query partial sums Z_j, M_j in
+// registers, one transpose-reduction per item (Alg. 1).
+// NPM = max query pairs (8: <= 16 queries, 16: <= 32). Returns Z_j, M_j to lane j.
+#define FK_PAIR(pp) \
+  { \
+    const float4 QA = sQA[pp], QB = sQB[pp]; /* {x0,x1,y0,y1}, {z0,z1,mh0,mh1} */ \
+    const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), nx); \
+    const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), ny); \
+    const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), nz); \
+    float2 dd = __fmul2_rn(dz, dz); \
+    dd = __ffma2_rn(dy, dy, dd); \
+    dd = __ffma2_rn(dx, dx, dd); \
+    const float2 e = __ffma2_rn(nbl, dd, make_float2(QB.z, QB.w)); \
+    const float2 wv = make_float2(ex2f(e.x), ex2f(e.y)); \
+    float2 f = __ffma2_rn(gx, dx, c); \
+    f = __ffma2_rn(gy, dy, f); \
+    f = __ffma2_rn(gz, dz, f); \
+    Z[pp] = __fadd2_rn(Z[pp], wv); \
+    M[pp] = __ffma2_rn(wv, f, M[pp]); \
+  }
+template <int NPM>
+__device__ __forceinline__ void fwd_keys_sums(const KeysView& kv, const uint32_t* L, const uint32_t wn,
+                                              const int nact, const float4* sQA, const float4* sQB,
+                                              float& Zj, float& Mj) {
+  const int lane = threadIdx.x & 31;
+  const int npairs = (nact + 1) >> 1;
+  float2 Z[NPM], M[NPM];
+#pragma unroll
+  for (int pp = 0; pp < NPM; ++pp) {
+    Z[pp] = make_float2(0.f, 0.f);
+    M[pp] = make_float2(0.f, 0.f);
+  }
+  // one round: lane = one key, loop over the item's query pairs
+  auto round = [&](const float4 ka, const float4 kb) {
+    const float2 nx = make_float2(-ka.x, -ka.x), ny = make_float2(-ka.y, -ka.y), nz = make_float2(-ka.z, -ka.z);
+    const float2 nbl = make_float2(-ka.w, -ka.w);
+    const float2 c = make_float2(kb.x, kb.x), gx = make_float2(kb.y, kb.y), gy = make_float2(kb.z, kb.z),
+                 gz = make_float2(kb.w, kb.w);
+    // groups of 4 pairs without a branch inside, so the scheduler can interleave their chains;
+    // the last 1-3 pairs one by one (an odd query count pads one slot with shift -inf: weight 0)
+#pragma unroll
+    for (int pg = 0; pg < NPM; pg += 4) {
+      const int rem = npairs - pg;
+      if (rem >= 4) {
+        FK_PAIR(pg) FK_PAIR(pg + 1) FK_PAIR(pg + 2) FK_PAIR(pg + 3)
+      } else if (rem > 0) {
+        FK_PAIR(pg)
+        if (rem >= 2) FK_PAIR(pg + 1)
+        if (rem >= 3) FK_PAIR(pg + 2)
+      }
+    }
+  };
+  // idle lanes of the last round get a far-away zero key: weight exactly 0
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
+  uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : far_a;
+  float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
+  for (uint32_t base = 0; base < wn; base += 32) {
+    const uint32_t k = base + lane;
+    const float4 ka = a1, kb = b1;
+    id1 = id2;
+    id2 = (k + 64 < wn) ? L[k + 64] : 0u;
+    a1 = far_a;
+    b1 = z4;
+    if (k + 32 < wn) {
+      a1 = __ldg(&kv.grid_raw[2 * id1]);
+      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+    }
+    round(ka, kb);
+  }
+  // transpose-reduce {Zx, Zy, Mx, My} of every pair; lane j then fetches its query's totals
+  if (NPM == 8) {
+    float v[32];
+#pragma unroll
+    for (int pp = 0; pp < 8; ++pp) {
+      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
+    }
+    warp_reduce_scatter<32>(v, lane);  // lane l holds value l
+    const int j = lane & 15;
+    Zj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + (j & 1));
+    Mj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + 2 + (j & 1));
+  } else {
+    float v[64];
+#pragma unroll
+    for (int pp = 0; pp < NPM; ++pp) {
+      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
+    }
+    warp_reduce_scatter<64>(v, lane);  // lane l holds values 2l, 2l+1
+    const int src = lane & ~1;
+    const float z0 = __shfl_sync(~0u, v[0], src), z1 = __shfl_sync(~0u, v[1], src);
+    const float m0 = __shfl_sync(~0u, v[0], src + 1), m1 = __shfl_sync(~0u, v[1], src + 1);
+    Zj = (lane & 1) ? z1 : z0;
+    Mj = (lane & 1) ? m1 : m0;
+  }
+}
+
+#ifndef FK_MIN_BLOCKS
+#define FK_MIN_BLOCKS 16  // <= 128 registers (measured: 1/16/20/24; half-item warps were slower)
+#endif
+__global__ void __launch_bounds__(NTHREADS, FK_MIN_BLOCKS) k_forward_keys(const FwdArgs A) {
+  static_assert(NWARP == 1 && QW == 32, "k_forward_keys: one warp per CTA, <= 32 queries per item");
+  __shared__ float4 sQA[QW / 2], sQB[QW / 2];
+  const int lane = threadIdx.x & 31;
+  const uint32_t item = blockIdx.x;
+  if (item >= *A.n_items) return;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const uint32_t wn = A.wl_n[item];
+  if (wn == BL_OVERFLOW) {  // no candidate list: the lanes = queries kernel streams this item
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = -INFINITY;  // an idle slot has shift -inf (weight 0)
+  if (act) {
+    q = A.qs[js];
+    mh = A.qmh[js];
+  }
+  {
+    const float xo = __shfl_xor_sync(~0u, q.x, 1), yo = __shfl_xor_sync(~0u, q.y, 1);
+    const float zo = __shfl_xor_sync(~0u, q.z, 1), mo = __shfl_xor_sync(~0u, mh, 1);
+    if ((lane & 1) == 0) {
+      sQA[lane >> 1] = make_float4(q.x, xo, q.y, yo);
+      sQB[lane >> 1] = make_float4(q.z, zo, mh, mo);
+    }
+  }
+  __syncwarp();
+  const uint32_t* L = A.wl_pool + A.wl_off[item];
+  float Z, M;
+  if (nact <= 16) fwd_keys_sums<8>(A.kv, L, wn, nact, sQA, sQB, Z, M);
+  else fwd_keys_sums<16>(A.kv, L, wn, nact, sQA, sQB, Z, M);
+  const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
+  if (__any_sync(~0u, bad)) {
+    // the shift bound overflowed: k_forward redoes the item with the exact-min shift
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  // epilogue: O, lambda, loss and its upstream (value-only forward)
+  float lossj = 0.0f;
+  if (act) {
+    const float O = M * (1.0f / Z);
+    const float nlam = mh - log2f(Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
+    const int ju = A.perm[js];
+    float r = 0.0f;
+    if (A.loss_kind >= EFUNC_LOSS_MSE) {
+      const float diff = O - q.w;
+      r = 2.0f * diff * A.inv_J;
+      lossj = diff * diff * A.inv_J;
+    }
+    A.rec[js] = make_float4(nlam, r, O, 0.f);
+    if (A.O) A.O[ju] = O;
+  }
+  if (A.loss_kind >= EFUNC_LOSS_MSE) {
+    for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
+    if (lane == 0) A.loss_part[item] = lossj;
+  }
+}
+
+int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
+  if (want_g || a.count_kept) {
+    if (want_g) k_forward<true><<<blocks, NTHREADS, 0, s>>>(a, 0);
+    else k_forward<false><<<blocks, NTHREADS, 0, s>>>(a, 0);
+    return 1;
+  }
+  k_item_lists<<<(unsigned)((n_items + IL_WARPS - 1) / IL_WARPS), 32 * IL_WARPS, 0, s>>>(a);
+  k_forward_keys<<<blocks, NTHREADS, 0, s>>>(a);
+  k_forward<false><<<148 * 4, NTHREADS, 0, s>>>(a, 1);  // slow-path items (usually none)
+  return 3;
+}
+
+}  // namespace ef

@@ -12,7 +12,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libefunc.so")
+# EFUNC_LIB_PATH: an alternative in-tree build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("EFUNC_LIB_PATH") or os.path.join(_PKG, "lib", "libefunc.so")
 
 NCH = 13
 OK, EINVAL, ESTATE, ENONFINITE, ECUDA, ENOMEM = range(6)
