@@ -75,7 +75,10 @@ typedef struct {
   int32_t deterministic;  /* 1: gradients bitwise reproducible run to run (no float atomics) */
   int32_t device;         /* CUDA device ordinal */
   int32_t sync_checks;    /* 1: forward synchronises and returns EFUNC_ENONFINITE at once */
-  int32_t reserved[5];    /* must be 0 */
+  int32_t fit_graph;      /* 1: efunc_fit_step replays a CUDA graph of its device work, captured on
+                             the second call with the same J, pointers, loss and hyper-parameters
+                             (any workspace reallocation drops it); 0: plain launches */
+  int32_t reserved[4];    /* must be 0 */
 } efunc_config;
 
 typedef enum { EFUNC_LOSS_NONE = 0, EFUNC_LOSS_MSE = 1, EFUNC_LOSS_MSE_EIKONAL = 2 } efunc_loss_kind;

@@ -102,9 +102,16 @@ KeysView keys_view(efunc_t* h) {
   return kv;
 }
 
+void drop_fit_graph(efunc_t* h) {
+  if (h->fit_exec) cudaGraphExecDestroy(h->fit_exec);
+  h->fit_exec = nullptr;
+  h->fit_seen = 0;
+}
+
 efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
   size_t tiles = (n_elems + 4095) / 4096 + 1;
   if (tiles <= h->scan_tmp_cap) return EFUNC_OK;
+  drop_fit_graph(h);
   dfree(h->scan_tmp);
   CK(dalloc(&h->scan_tmp, tiles));
   h->scan_tmp_cap = tiles;
@@ -118,11 +125,15 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   CK(cudaMemsetAsync(h->cell_fill, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
   if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->keys_resort, force ? 1 : 0, sizeof(uint32_t), s));
   const float skin = SKIN_H * h->h;
   h->launches += launch_prep_keys(h->theta, h->R, h->key_raw, h->key_cell, h->cell_count, h->key_ref,
                                   skin * skin, SKIN_MU, h->ds, s);
-  h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s);
-  h->launches += launch_counting_sort(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_tmp, h->key_order, s);
+  // the cell sort only when some offset key changed cell (k_prep_keys sets keys_resort)
+  const uint32_t* gate = &h->ds->keys_resort;
+  h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s, gate);
+  h->launches += launch_counting_sort(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_tmp,
+                                      h->key_order, s, gate);
   h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
   // per-brick candidate lists for the next forward/backward (query independent)
   h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
@@ -136,6 +147,7 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
 
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
   const int64_t bound = (J + QW - 1) / QW + h->bg.n_codes + 1;
+  if (bound > h->items_cap || J > h->J_cap) drop_fit_graph(h);
   if (bound > h->items_cap) {
     dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
     CK(dalloc(&h->loss_part, bound));
@@ -148,6 +160,7 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   // forward -> backward candidate-id pool: reserved per item = its brick list length
   const double want = std::fmin((double)J * WL_PER_QUERY, 3.9e9);
   if (want > (double)h->wl_cap) {
+    drop_fit_graph(h);
     dfree(h->wl_pool);
     CK(dalloc(&h->wl_pool, (size_t)want));
     h->wl_cap = (uint32_t)want;
@@ -181,6 +194,9 @@ void free_all(efunc_t* h) {
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
+  drop_fit_graph(h);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  h->cap_stream = nullptr;
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -314,17 +330,15 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
 
 efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cudaStream_t s) {
   if (!grad || !hp) return fail(h, EFUNC_EINVAL, "NULL argument");
-  h->step += 1;
-  // hyper-parameters are doubles (like torch's python floats); derived constants are rounded
-  // to fp32 once, here
-  const double b1 = hp->beta1, b2 = hp->beta2;
-  const double bc1 = 1.0 - std::pow(b1, (double)h->step);
-  const double bc2 = 1.0 - std::pow(b2, (double)h->step);
-  const float step_size = (float)(hp->lr / bc1);
-  const float sqrt_bc2 = (float)std::sqrt(bc2);
-  const float decay = (float)(1.0 - hp->lr * hp->weight_decay);
-  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, decay, (float)(1.0 - b1),
-                              (float)b2, (float)(1.0 - b2), (float)hp->eps, hp->decay_mask, step_size, sqrt_bc2, s);
+  // the step counter and the bias corrections live on the device (k_adamw)
+  AdamWConst hc;
+  hc.lr = hp->lr;
+  hc.beta1 = hp->beta1;
+  hc.beta2 = hp->beta2;
+  hc.eps = hp->eps;
+  hc.weight_decay = hp->weight_decay;
+  hc.decay_mask = hp->decay_mask;
+  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
   CK(cudaGetLastError());
   return rebuild_keys(h, s);
 }
@@ -467,6 +481,7 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
   float* lossd = loss_out;
   if (host_io) {
     if (J > h->io_cap || !h->io_q) {
+      drop_fit_graph(h);
       dfree(h->io_q);
       dfree(h->io_o);
       CK(dalloc(&h->io_q, 3 * (size_t)J));
@@ -483,10 +498,47 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
     lossd = h->io_loss;
   }
   float* g = grad_ws ? grad_ws : h->fit_grad;
-  CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, s));
-  RET(do_forward(h, qd, od, J, loss, nullptr, nullptr, lossd, 1, s));
-  RET(do_backward(h, nullptr, nullptr, g, s));
-  RET(do_adamw(h, g, hp, s));
+  auto device_work = [&](cudaStream_t st) -> efunc_status {
+    CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, st));
+    RET(do_forward(h, qd, od, J, loss, nullptr, nullptr, lossd, 1, st));
+    RET(do_backward(h, nullptr, nullptr, g, st));
+    return do_adamw(h, g, hp, st);
+  };
+  efunc_t::FitKey key{};
+  key.q = qd; key.o = od; key.g = g; key.lossd = lossd;
+  key.J = J; key.J_global = loss->J_global; key.kind = loss->kind; key.eik = loss->eikonal_lambda;
+  key.lr = hp->lr; key.b1 = hp->beta1; key.b2 = hp->beta2; key.eps = hp->eps; key.wd = hp->weight_decay;
+  key.mask = hp->decay_mask; key.count_kept = h->count_kept;
+  const bool same = h->fit_seen && std::memcmp(&key, &h->fit_key, sizeof(key)) == 0;
+  if (h->cfg.fit_graph && !h->cfg.sync_checks && same) {
+    if (!h->fit_exec) {
+      // second identical call: capture the device work once (nothing reallocates: the first,
+      // eager call sized every workspace) and replay it from now on
+      if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      const int64_t l0 = h->launches;
+      CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const efunc_status st = device_work(h->cap_stream);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(h->cap_stream, &graph);
+      if (st != EFUNC_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      CK(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&h->fit_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(ie);
+      h->fit_launches = h->launches - l0;
+      h->launches = l0;
+    }
+    CK(cudaGraphLaunch(h->fit_exec, s));
+    h->launches += h->fit_launches;
+  } else {
+    drop_fit_graph(h);
+    RET(device_work(s));
+    h->fit_key = key;
+    h->fit_seen = 1;
+  }
   if (host_io) {
     if (loss_out) CK(cudaMemcpyAsync(loss_out, lossd, sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -533,7 +585,11 @@ efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int6
   CK(cudaDeviceSynchronize());
   if (m_host) CK(cudaMemcpy(m_host, h->m, bytes, cudaMemcpyDeviceToHost));
   if (v_host) CK(cudaMemcpy(v_host, h->v, bytes, cudaMemcpyDeviceToHost));
-  if (step) *step = h->step;
+  if (step) {
+    unsigned long long t = 0;
+    CK(cudaMemcpy(&t, &h->ds->adam_t, sizeof(t), cudaMemcpyDeviceToHost));
+    *step = (int64_t)t;
+  }
   return EFUNC_OK;
 }
 
@@ -547,7 +603,8 @@ efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* 
   else CK(cudaMemset(h->m, 0, bytes));
   if (v_host) CK(cudaMemcpy(h->v, v_host, bytes, cudaMemcpyHostToDevice));
   else CK(cudaMemset(h->v, 0, bytes));
-  h->step = step;
+  const unsigned long long t = (unsigned long long)step;
+  CK(cudaMemcpy(&h->ds->adam_t, &t, sizeof(t), cudaMemcpyHostToDevice));
   return EFUNC_OK;
 }
 

@@ -68,7 +68,10 @@ struct DevScalars {
   float umax;              // deterministic backward: max_j (|dL/dO_j| + |dL/dG_j|_1) of the call
   uint32_t fix_overflow;   // deterministic backward: a partial left the fixed-point range
   uint32_t slow_n;         // items k_forward_keys left to the exact-min slow path (reset every forward)
-  uint32_t pad_;
+  uint32_t adam_done;      // k_adamw blocks finished (the last one advances adam_t and resets this)
+  uint32_t keys_resort;    // an offset key changed lattice cell: re-sort the keys (else only regather)
+  uint32_t pad1_;
+  unsigned long long adam_t;  // AdamW step counter (device-side so CUDA graphs replay it correctly)
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
@@ -147,9 +150,10 @@ int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_c
 int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, DevScalars* ds,
                          cudaStream_t s);
 int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp,
-                    cudaStream_t s);
+                    cudaStream_t s, const uint32_t* gate = nullptr);
 int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start,
-                         uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s);
+                         uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s,
+                         const uint32_t* gate = nullptr);
 int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted,
                        int* kid, uint32_t n, cudaStream_t s);
 int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool,
@@ -169,9 +173,12 @@ int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* o
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
 int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, int n_nodes, cudaStream_t s);
-int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay,
-                 float omb1, float b2, float omb2, float eps, uint32_t mask, float step_size,
-                 float sqrt_bc2, cudaStream_t s);
+struct AdamWConst {  // the efunc_adamw hyper-parameters (doubles, like torch's python floats)
+  double lr, beta1, beta2, eps, weight_decay;
+  uint32_t decay_mask;
+};
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,
+                 DevScalars* ds, cudaStream_t s);
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
@@ -188,7 +195,6 @@ struct efunc {
   float* theta = nullptr;
   float* m = nullptr;
   float* v = nullptr;
-  int64_t step = 0;
   // keys
   float4* key_raw = nullptr;
   float4* key_sorted = nullptr;
@@ -248,5 +254,19 @@ struct efunc {
   int fwd_loss_kind = 0;
   int count_kept = 0;
   int64_t launches = 0;
+  // efunc_fit_step CUDA graph (cfg.fit_graph): the key of the last call, the captured executable
+  struct FitKey {
+    const float* q; const float* o; float* g; float* lossd;
+    int64_t J, J_global;
+    int kind;
+    float eik;
+    double lr, b1, b2, eps, wd;
+    uint32_t mask;
+    int count_kept;
+  } fit_key{};
+  int fit_seen = 0;                  // fit_key holds the last (eager) call
+  cudaGraphExec_t fit_exec = nullptr;
+  int64_t fit_launches = 0;          // kernels inside the captured graph
+  cudaStream_t cap_stream = nullptr;
   std::string err;
 };

@@ -7,10 +7,29 @@ namespace ef {
 // Elementwise over theta [R^3][13]; op order follows torch's single-tensor AdamW:
 //   p *= 1 - lr*wd (masked channels);  m += (1-b1)(g - m);  v = v*b2 + (1-b2) g*g;
 //   p += -step_size * m / (sqrt(v) / sqrt(bc2) + eps),  step_size = lr / bc1
-// All scalar constants are computed in double on the host and rounded to fp32 once.
+// The step counter t lives on the device (ds->adam_t): every block derives the scalar constants
+// for t + 1 in double (rounded to fp32 once), and the last block to finish stores t + 1. So a
+// captured CUDA graph replays correct bias corrections.
 __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
-                        float* __restrict__ v, int64_t n, float decay, float omb1, float b2, float omb2,
-                        float eps, uint32_t mask, float step_size, float sqrt_bc2) {
+                        float* __restrict__ v, int64_t n, const AdamWConst hc, DevScalars* ds) {
+  __shared__ float c[8];
+  __shared__ unsigned long long t_next;
+  if (threadIdx.x == 0) {
+    const unsigned long long t = ds->adam_t + 1;
+    const double bc1 = 1.0 - pow(hc.beta1, (double)t);
+    const double bc2 = 1.0 - pow(hc.beta2, (double)t);
+    c[0] = (float)(1.0 - hc.lr * hc.weight_decay);  // decay
+    c[1] = (float)(1.0 - hc.beta1);                  // 1 - b1
+    c[2] = (float)hc.beta2;
+    c[3] = (float)(1.0 - hc.beta2);                  // 1 - b2
+    c[4] = (float)hc.eps;
+    c[5] = (float)(hc.lr / bc1);                     // step_size
+    c[6] = (float)sqrt(bc2);
+    t_next = t;
+  }
+  __syncthreads();
+  const float decay = c[0], omb1 = c[1], b2 = c[2], omb2 = c[3], eps = c[4], step_size = c[5], sqrt_bc2 = c[6];
+  const uint32_t mask = hc.decay_mask;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % EF_NCH);
     float p = theta[i];
@@ -26,16 +45,24 @@ __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ gra
     m[i] = mi;
     v[i] = vi;
   }
+  // every block has read adam_t (above) before it arrives here: the last one advances it
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ds->adam_done, 1u) == gridDim.x - 1) {
+      ds->adam_t = t_next;
+      ds->adam_done = 0;
+    }
+  }
 }
 
-int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, float decay, float omb1,
-                 float b2, float omb2, float eps, uint32_t mask, float step_size, float sqrt_bc2,
-                 cudaStream_t s) {
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,
+                 DevScalars* ds, cudaStream_t s) {
+  // few fat blocks: each block derives the step constants once (a double pow on one thread)
   long blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 2) blocks = 148 * 2;
   if (blocks < 1) blocks = 1;
-  k_adamw<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, decay, omb1, b2, omb2, eps, mask, step_size,
-                                            sqrt_bc2);
+  k_adamw<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, hc, ds);
   return 1;
 }
 

@@ -25,7 +25,7 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
   const int NC = R - 1;
   const float inv_h = (float)((R - 1) / 2.0);
   float local_min = INFINITY;
-  bool moved = false;
+  bool moved = false, resort = false;
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int x = n % R, y = (n / R) % R, z = n / (R * R);
     // lattice k(i) = float32(-1 + 2 i/(R-1))  (reading R-2), evaluated in double
@@ -44,6 +44,7 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
                                    cell_clamp(kx, inv_h, NC));
     const uint32_t c1 = (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
                                    cell_clamp(px, inv_h, NC));
+    resort |= key_cell[N + n] != c1;  // grid-bank cells never change
     key_cell[n] = c0;
     key_cell[N + n] = c1;
     atomicAdd(&cell_count[c0], 1u);
@@ -60,6 +61,7 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
   if ((threadIdx.x & 31) == 0 && local_min < INFINITY)
     atomicMin(reinterpret_cast<unsigned int*>(&ds->bl_min), __float_as_uint(local_min));
   if (__any_sync(~0u, moved) && (threadIdx.x & 31) == 0) atomicOr(&ds->lists_invalid, 1u);
+  if (__any_sync(~0u, resort) && (threadIdx.x & 31) == 0) atomicOr(&ds->keys_resort, 1u);
 }
 
 int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
@@ -123,8 +125,12 @@ __device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s
   return incl - v + s_w[w];
 }
 
+// gate (nullable): the kernels of a scan / counting sort do nothing when *gate == 0
+#define GATED if (gate && *gate == 0u) return
+
 __global__ void k_scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n,
-                             uint32_t* __restrict__ tile_sums) {
+                             uint32_t* __restrict__ tile_sums, const uint32_t* gate) {
+  GATED;
   __shared__ uint32_t s_w[33];
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER;
   uint32_t v[SCAN_PER];
@@ -144,7 +150,8 @@ __global__ void k_scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restri
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
 }
 
-__global__ void k_scan_tile_sums(uint32_t* __restrict__ tile_sums, uint32_t nt) {
+__global__ void k_scan_tile_sums(uint32_t* __restrict__ tile_sums, uint32_t nt, const uint32_t* gate) {
+  GATED;
   __shared__ uint32_t s_w[33];
   uint32_t carry = 0;
   for (uint32_t b0 = 0; b0 < nt; b0 += SCAN_TILE) {
@@ -168,7 +175,9 @@ __global__ void k_scan_tile_sums(uint32_t* __restrict__ tile_sums, uint32_t nt) 
   }
 }
 
-__global__ void k_scan_add(uint32_t* __restrict__ out, uint32_t n, const uint32_t* __restrict__ tile_sums) {
+__global__ void k_scan_add(uint32_t* __restrict__ out, uint32_t n, const uint32_t* __restrict__ tile_sums,
+                           const uint32_t* gate) {
+  GATED;
   const uint32_t add = tile_sums[blockIdx.x];
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER;
 #pragma unroll
@@ -176,12 +185,13 @@ __global__ void k_scan_add(uint32_t* __restrict__ out, uint32_t n, const uint32_
     if (base + i < n) out[base + i] += add;
 }
 
-int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp, cudaStream_t s) {
+int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp, cudaStream_t s,
+                    const uint32_t* gate) {
   const uint32_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
-  k_scan_tiles<<<nt, SCAN_T, 0, s>>>(in, out, n, block_tmp);
+  k_scan_tiles<<<nt, SCAN_T, 0, s>>>(in, out, n, block_tmp, gate);
   if (nt > 1) {
-    k_scan_tile_sums<<<1, SCAN_T, 0, s>>>(block_tmp, nt);
-    k_scan_add<<<nt, SCAN_T, 0, s>>>(out, n, block_tmp);
+    k_scan_tile_sums<<<1, SCAN_T, 0, s>>>(block_tmp, nt, gate);
+    k_scan_add<<<nt, SCAN_T, 0, s>>>(out, n, block_tmp, gate);
     return 3;
   }
   return 1;
@@ -189,7 +199,8 @@ int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* blo
 
 // ------------------------------------------------------------------------------ counting sort
 __global__ void k_scatter(const uint32_t* __restrict__ bin, uint32_t n, const uint32_t* __restrict__ bin_start,
-                          uint32_t* __restrict__ fill, uint32_t* __restrict__ tmp_idx) {
+                          uint32_t* __restrict__ fill, uint32_t* __restrict__ tmp_idx, const uint32_t* gate) {
+  GATED;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t b = bin[i];
     tmp_idx[bin_start[b] + atomicAdd(&fill[b], 1u)] = i;
@@ -198,7 +209,9 @@ __global__ void k_scatter(const uint32_t* __restrict__ bin, uint32_t n, const ui
 
 // Rank of each element inside its bin = number of same-bin elements with a smaller index.
 __global__ void k_stable_rank(const uint32_t* __restrict__ bin, uint32_t n, const uint32_t* __restrict__ bin_start,
-                              const uint32_t* __restrict__ tmp_idx, uint32_t* __restrict__ out_idx) {
+                              const uint32_t* __restrict__ tmp_idx, uint32_t* __restrict__ out_idx,
+                              const uint32_t* gate) {
+  GATED;
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     const uint32_t i = tmp_idx[p];
     const uint32_t b = bin[i];
@@ -217,10 +230,10 @@ static int grid_for(uint32_t n, int threads) {
 }
 
 int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
-                          uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s) {
+                          uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s, const uint32_t* gate) {
   if (n == 0) return 0;
-  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, tmp_idx);
-  k_stable_rank<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, tmp_idx, out_idx);
+  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, tmp_idx, gate);
+  k_stable_rank<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, tmp_idx, out_idx, gate);
   return 2;
 }
 

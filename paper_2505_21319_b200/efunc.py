@@ -30,7 +30,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
 class Config(C.Structure):
     _fields_ = [("R", C.c_int32), ("degree", C.c_int32), ("variant", C.c_int32), ("cutoff_T", C.c_float),
                 ("deterministic", C.c_int32), ("device", C.c_int32), ("sync_checks", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("fit_graph", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class Loss(C.Structure):
@@ -130,13 +130,14 @@ class EFunc:
     """One efunc grid (O^{+Delta}, degree 1, R^3 x 13) on one CUDA device."""
 
     def __init__(self, R: int, theta=None, cutoff_T: float = 20.0, device: int = 0,
-                 deterministic: bool = False, sync_checks: bool = False):
+                 deterministic: bool = False, sync_checks: bool = False, fit_graph: bool = True):
         import torch
         self.lib = load_library()
         self.R = int(R)
         self.device = int(device)
         self.n_params = self.R ** 3 * NCH
-        cfg = Config(self.R, 1, 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks))
+        cfg = Config(self.R, 1, 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks),
+                     int(fit_graph))
         th = None
         if theta is not None:
             if isinstance(theta, torch.Tensor):

@@ -351,3 +351,39 @@ def test_deterministic_fit_bitwise_at_scale():
             m.adamw_step(grad)
         outs.append(m.get_params())
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_fit_step_graph_replay_bitwise_equals_eager():
+    """efunc_fit_step with cfg.fit_graph (captured on the 2nd call, replayed after) gives bitwise the
+    same theta, moments and loss trajectory as plain launches (deterministic mode), and the device-
+    side AdamW step counter advances once per replay."""
+    R, J = 16, 1 << 15
+    tor = synth.Torus()
+    th0 = synth.init_theta(R, 31)
+    s = dev(synth.surface_points(tor, 4096, seed=32))
+    batches = [synth.sample_batch(tor, J, seed=300 + k) for k in range(2)]
+    qd = [dev(q) for q, _ in batches]
+    od = [dev(o) for _, o in batches]
+    # device-pointer fit_step: one q/o buffer pair per handle (the graph key includes the pointers)
+    res = []
+    for graph in (False, True):
+        m = ef.EFunc(R, th0, deterministic=True, fit_graph=graph)
+        m.mean_shift_init(s)
+        qb, ob = torch.empty_like(qd[0]), torch.empty_like(od[0])
+        lo = torch.zeros(1, device="cuda")
+        losses = []
+        for k in range(6):
+            qb.copy_(qd[k % 2]); ob.copy_(od[k % 2])
+            m.fit_step(qb, ob, ef.AdamW(), loss=ef.LOSS_MSE, loss_out=lo)
+            losses.append(float(lo.item()))
+        mm, vv, st = m.get_adam_state()
+        res.append((m.get_params(), mm, vv, st, losses))
+    (p0, m0, v0, s0, l0), (p1, m1, v1, s1, l1) = res
+    assert s0 == s1 == 6
+    assert np.array_equal(p0, p1) and np.array_equal(m0, m1) and np.array_equal(v0, v1)
+    assert l0 == l1
+    # host-io fit_step (pinned buffers, graph inside) also advances the step
+    m = ef.EFunc(R, th0, fit_graph=True)
+    for k in range(3):
+        m.fit_step(torch.as_tensor(batches[k % 2][0]).pin_memory(), torch.as_tensor(batches[k % 2][1]).pin_memory())
+    assert m.get_adam_state()[2] == 3
