@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--eager", action="store_true", help="N=1: plain launches instead of a CUDA graph per step")
+    p.add_argument("--split", action="store_true", help="efunc_forward + efunc_backward instead of the fused call")
     return p.parse_args()
 
 
@@ -181,23 +182,26 @@ def run_ours(args, rank, world, local_rank):
     od = [torch.as_tensor(o).cuda(dev) for _, o in host]
     grad = torch.zeros(R ** 3, ef.NCH, dtype=torch.float32, device=f"cuda:{dev}")
 
-    def step_calls(i, ev=None):
+    # fused path (default): efunc_forward_backward runs the fused fit kernel k_fit for the MSE loss;
+    # --split: efunc_forward + efunc_backward (k_item_lists, k_forward_keys, k_backward)
+    def step_calls(i):
         grad.zero_()
-        m.forward(qd[i], od[i], loss=loss, J_global=J_global, want_O=False, want_loss=False)
-        if ev is not None:
-            ev[0].record()
-        m.backward(grad=grad)
-        if ev is not None:
-            ev[1].record()
+        if args.split:
+            m.forward(qd[i], od[i], loss=loss, J_global=J_global, want_O=False, want_loss=False)
+            m.backward(grad=grad)
+        else:
+            m.forward_backward(qd[i], od[i], loss=loss, J_global=J_global, grad=grad, want_loss=False)
         if world > 1:
             edist.allreduce_grad(grad)
         m.adamw_step(grad, hp)
 
     # N=1: the step is replayed from a CUDA graph per input batch (the same ABI calls, captured once;
-    # the AdamW step counter is device-side), with external timing events around the backward.
+    # the AdamW step counter is device-side). The library records CUDA events around the dominant
+    # kernel (k_fit, or k_backward on the split path) of every step: slot = batch index.
     # N>1 (NCCL all-reduce inside the step): plain launches.
     use_graph = world == 1 and not args.eager
-    graphs, gev, launches_per_step = [], [], None
+    graphs, launches_per_step = [], None
+    m.set_timing(pool)
     if use_graph:
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(torch.cuda.current_stream(dev))
@@ -207,20 +211,17 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         l0 = m.stats()["launches"]
         for i in range(pool):
-            ev = (torch.cuda.Event(enable_timing=True, external=True),
-                  torch.cuda.Event(enable_timing=True, external=True))
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=cap):
-                step_calls(i, ev)
+                step_calls(i)
             graphs.append(g)
-            gev.append(ev)
         launches_per_step = (m.stats()["launches"] - l0) / pool
 
-    def step(i, ev=None):
+    def step(i):
         if use_graph:
             graphs[i].replay()
         else:
-            step_calls(i, ev)
+            step_calls(i)
 
     # kept-pair census (algorithmic work per point), outside the timed region
     m.set_counting(True)
@@ -243,7 +244,6 @@ def run_ours(args, rank, world, local_rank):
         step(0)
     torch.cuda.synchronize()
     launches0 = m.stats()["launches"]
-    bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -252,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
     clk.active = True
     t0.record()
     for k in range(args.steps):
-        step((args.warmup + k) % pool, None if use_graph else bev[k])
+        step((args.warmup + k) % pool)
     t1.record()
     torch.cuda.synchronize()
     clk.active = False
@@ -261,11 +261,9 @@ def run_ours(args, rank, world, local_rank):
     launches = m.stats()["launches"] - launches0
     sec = t0.elapsed_time(t1) / 1e3
     if use_graph:
-        # the last replay of each batch's graph: the final `pool` steps of the timed region
         launches = launches_per_step * args.steps
-        bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in gev]))
-    else:
-        bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in bev]))
+    # the dominant kernel's CUDA-event time in the last `pool` steps of the timed region
+    bwd_ms = float(np.nanmean(m.kernel_ms(pool)))
     if world > 1:
         tt = torch.tensor([sec, bwd_ms], dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -295,8 +293,7 @@ def run_ours(args, rank, world, local_rank):
                 qbuf.copy_(hq[i], non_blocking=True)
                 obuf.copy_(ho[i], non_blocking=True)
                 grad.zero_()
-                _, _, L = m.forward(qbuf, obuf, loss=loss, J_global=J_global, want_O=False)
-                m.backward(grad=grad)
+                _, _, L = m.forward_backward(qbuf, obuf, loss=loss, J_global=J_global, grad=grad)
                 edist.allreduce_grad(grad)
                 m.adamw_step(grad, hp)
                 return float(L.item())
@@ -315,26 +312,31 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (k_backward): algorithmic lane-ops per launch / its time
+    # roofline of the dominant kernel: algorithmic lane-ops per launch / its time. k_fit (fused,
+    # MSE) does the forward and the backward of every kept pair; k_backward only the backward.
+    fused = loss_kind == "mse" and not args.split
+    kname = "k_fit" if fused else "k_backward"
     if loss_kind == "mse":
         ops = OPS_BWD_GRID * (kept - kept_off) + OPS_BWD_OFF * kept_off
     else:
         ops = OPS_BWD_EIK_GRID * (kept - kept_off) + OPS_BWD_EIK_OFF * kept_off
+    if fused:
+        ops += OPS_FWD * kept
     peak = SM_COUNT * FP32_LANES * SM_MAX_MHZ * 1e6 / 1e12
     achieved = ops / (bwd_ms * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"{args.config}:k_backward")
+            traffic = json.load(open(tp)).get(f"{args.config}:{kname}")
         except Exception:
             traffic = None
-    roof = {"bound": "alu", "kernel": "k_backward", "achieved": achieved, "peak": peak,
+    roof = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": peak,
             "unit": "T fp32 lane-op/s", "frac": achieved / peak, "traffic": traffic,
             "ops_per_launch": ops, "launch_ms": bwd_ms,
-            "launch_ms_source": ("CUDA events (external nodes) around k_backward in each batch's step graph, "
-                                 "last replay of each: the final steps of the timed region") if use_graph else
-                                ("CUDA events around k_backward in every timed step"),
+            "launch_ms_source": (f"CUDA events the library records around {kname} on the launch stream "
+                                 "(efunc_set_timing; external event nodes inside each batch's step graph), "
+                                 "mean over the final steps of the timed region"),
             "share_of_step": bwd_ms * 1e-3 / (sec / args.steps),
             "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz max clock (guide unit counts)",
             "kept_pairs_per_point": kept / J, "candidate_pairs_per_point": cand / J}
@@ -346,6 +348,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": label, "R": R, "points_per_step_per_gpu": J, "global_batch": J_global,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}",
                        "launch": "cuda-graph per step" if use_graph else "eager",
+                       "path": "split forward/backward" if args.split else "efunc_forward_backward (fused k_fit for MSE)",
                        "l2": f"inputs larger than L2: pool of {pool} batches x {J * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:

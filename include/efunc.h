@@ -142,6 +142,21 @@ EFUNC_API efunc_status efunc_forward(efunc_t* h, const float* q, const float* o,
 EFUNC_API efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad,
                             void* stream);
 
+/* efunc_forward_backward — efunc_forward followed by efunc_backward(dL_dO = NULL, dL_dG = NULL):
+ * the fit step's forward, fused loss upstream and backward (Alg. 1 + Eq. loss + Alg. 2,
+ * PAPER.md:L486-490, L505-568) in one call.
+ *   q, o  dev float[J*3], float[J]; loss must be MSE or MSE_EIKONAL (NULL/NONE: EFUNC_EINVAL)
+ *   O     dev float[J] output values or NULL
+ *   grad  dev float[R^3*13], accumulated into (+=)
+ *   loss_out dev float[1] or NULL
+ * For the MSE loss (non-deterministic mode, counting off) it runs one fused kernel per work
+ * item: the MSE upstream of a query depends on that query alone, so each item's forward and
+ * backward share one candidate-key pass. Otherwise it is exactly forward + backward. Leaves
+ * no saved forward state (a following efunc_backward returns EFUNC_ESTATE). */
+EFUNC_API efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J,
+                                    const efunc_loss* loss, float* O, float* grad, float* loss_out,
+                                    void* stream);
+
 /* efunc_adamw_step — one AdamW update of theta with torch.optim.AdamW semantics
  * (decoupled decay first, bias-corrected moments; reading R-10). grad: dev float[R^3*13],
  * already summed over data-parallel ranks. Increments the handle's step counter, then
@@ -179,6 +194,13 @@ EFUNC_API efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, con
 /* efunc_set_counting — 1: the forward also counts kept pairs (a - m <= T) for
  * efunc_get_stats (slower; diagnostics only). */
 EFUNC_API efunc_status efunc_set_counting(efunc_t* h, int32_t on);
+/* efunc_set_timing — slots > 0: every efunc_backward / efunc_forward_backward call records a
+ * CUDA event pair around its dominant kernel (k_backward, or k_fit when fused) on the call's
+ * stream, into slot (call index mod slots); the records also work inside CUDA-graph capture
+ * (external event nodes). slots = 0 turns timing off. efunc_get_kernel_ms synchronises and
+ * writes the elapsed milliseconds of slots 0..n-1 (NaN for a slot never recorded). */
+EFUNC_API efunc_status efunc_set_timing(efunc_t* h, int32_t slots);
+EFUNC_API efunc_status efunc_get_kernel_ms(efunc_t* h, float* ms_host, int32_t n);
 /* efunc_get_stats — synchronises `stream` and reports counters of the last forward. */
 EFUNC_API efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream);
 /* efunc_check — synchronises; EFUNC_ENONFINITE if a non-finite input was seen since the

@@ -183,6 +183,34 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   return EFUNC_OK;
 }
 
+// Kernel timing: record an event pair around the call's dominant kernel (capture-safe).
+void record_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
+
+int timing_begin(efunc_t* h, cudaStream_t s) {
+  if (h->tev.empty()) return -1;
+  const int slot = (int)(h->tseq++ % (int64_t)(h->tev.size() / 2));
+  record_event(h->tev[2 * slot], s);
+  return slot;
+}
+
+void timing_end(efunc_t* h, int slot, cudaStream_t s) {
+  if (slot < 0) return;
+  record_event(h->tev[2 * slot + 1], s);
+  h->tev_used[slot] = 1;
+}
+
+void free_timing(efunc_t* h) {
+  for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+  h->tev.clear();
+  h->tev_used.clear();
+  h->tseq = 0;
+}
+
 void free_all(efunc_t* h) {
   dfree(h->theta); dfree(h->m); dfree(h->v);
   dfree(h->key_raw); dfree(h->key_sorted); dfree(h->kid); dfree(h->key_cell);
@@ -194,9 +222,64 @@ void free_all(efunc_t* h) {
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
+  dfree(h->fit_scratch);
   drop_fit_graph(h);
+  free_timing(h);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   h->cap_stream = nullptr;
+}
+
+// S1 for one forward: query bins, stable counting sort, gather, work items; then the forward
+// arguments (everything but the outputs).
+efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64_t J, const efunc_loss* loss,
+                          FwdArgs& a, cudaStream_t s) {
+  const int kind = loss ? loss->kind : EFUNC_LOSS_NONE;
+  RET(ensure_queries(h, J));
+  const uint32_t nb = h->bg.n_codes;             // bricks
+  const uint32_t nbins = nb * QSUB + 1;          // octant bins + the out-of-domain bin
+  CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
+  CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
+  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->wl_top, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->slow_n, 0, sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&h->ds->fwd_next, 0, 3 * sizeof(uint32_t), s));  // fwd_next, bwd_next, fit_next
+  h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
+  h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
+  h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
+  h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
+  // work items: balanced runs of <= QW sorted queries of one brick
+  h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
+  h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
+  h->launches += launch_items_write(h->bin_start, nb, h->item_off, h->items, s);
+  const int64_t items = (J + QW - 1) / QW + nb + 1;  // launch bound; kernels read the count
+  h->fwd_items_bound = items;
+  a = FwdArgs{};
+  a.kv = keys_view(h);
+  a.qs = h->qs;
+  a.perm = h->perm;
+  a.J = J;
+  a.items = h->items;
+  a.n_items = h->item_off + (nb + 1);
+  a.T_l = cutoff_log2(h->cfg);
+  a.loss_kind = kind;
+  const int64_t Jg = (loss && loss->J_global > 0) ? loss->J_global : J;
+  a.inv_J = (float)(1.0 / (double)Jg);
+  a.eik_lambda = loss ? loss->eikonal_lambda : 0.0f;
+  a.rec = h->rec;
+  a.gs = h->gs;
+  a.us = h->us;
+  a.hs = h->hs;
+  a.loss_part = h->loss_part;
+  a.qmh = h->qmh;
+  a.wl_pool = h->wl_pool;
+  a.wl_cap = h->wl_cap;
+  a.wl_off = h->wl_off;
+  a.wl_n = h->wl_n;
+  a.slow_items = h->slow_items;
+  a.ds = h->ds;
+  a.count_kept = h->count_kept;
+  return EFUNC_OK;
 }
 
 efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -217,54 +300,13 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
     h->fwd_loss_kind = kind;
     return EFUNC_OK;
   }
-  RET(ensure_queries(h, J));
-  const uint32_t nb = h->bg.n_codes;             // bricks
-  const uint32_t nbins = nb * QSUB + 1;          // octant bins + the out-of-domain bin
-  CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
-  CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
-  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->wl_top, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->slow_n, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
   const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
-  h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
-  h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
-  h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
-  h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
-  // work items: balanced runs of <= QW sorted queries of one brick
-  h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
-  h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
-  h->launches += launch_items_write(h->bin_start, nb, h->item_off, h->items, s);
-  const int64_t items = (J + QW - 1) / QW + nb + 1;  // launch bound; kernels read the count
-  const uint32_t* n_items = h->item_off + (nb + 1);
-  h->fwd_items_bound = items;
   FwdArgs a;
-  a.kv = keys_view(h);
-  a.qs = h->qs;
-  a.perm = h->perm;
-  a.J = J;
-  a.items = h->items;
-  a.n_items = n_items;
-  a.T_l = cutoff_log2(h->cfg);
-  a.loss_kind = kind;
-  const int64_t Jg = (loss && loss->J_global > 0) ? loss->J_global : J;
-  a.inv_J = (float)(1.0 / (double)Jg);
-  a.eik_lambda = loss ? loss->eikonal_lambda : 0.0f;
+  RET(prep_queries(h, q, o_used, J, loss, a, s));
+  const int64_t items = h->fwd_items_bound;
+  const uint32_t* n_items = a.n_items;
   a.O = O;
   a.G = G;
-  a.rec = h->rec;
-  a.gs = h->gs;
-  a.us = h->us;
-  a.hs = h->hs;
-  a.loss_part = h->loss_part;
-  a.qmh = h->qmh;
-  a.wl_pool = h->wl_pool;
-  a.wl_cap = h->wl_cap;
-  a.wl_off = h->wl_off;
-  a.wl_n = h->wl_n;
-  a.slow_items = h->slow_items;
-  a.ds = h->ds;
-  a.count_kept = h->count_kept;
   h->launches += launch_forward(a, want_g, items, s);
   if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, 1, loss_out, s);
   else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
@@ -285,15 +327,8 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
   return EFUNC_OK;
 }
 
-efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, cudaStream_t s) {
-  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
-  if (!h->have_fwd) return fail(h, EFUNC_ESTATE, "backward without a valid forward (saved e_j missing)");
-  if (h->fwd_J == 0) return EFUNC_OK;
-  if (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_NONE)
-    return fail(h, EFUNC_EINVAL, "dL_dO is NULL and the forward had no fused loss");
-  const int eik = (dL_dG != nullptr) || (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_MSE_EIKONAL);
-  if (eik && !h->fwd_has_g) return fail(h, EFUNC_ESTATE, "dL_dG needs a forward that computed G");
-  BwdArgs b;
+BwdArgs bwd_args(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, int eik) {
+  BwdArgs b{};
   b.kv = keys_view(h);
   b.qs = h->qs;
   b.perm = h->perm;
@@ -316,15 +351,88 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   b.dL_dG = dL_dG;
   b.grad = grad;
   b.eik = eik;
+  b.next = &h->ds->bwd_next;
+  b.list = nullptr;
+  b.list_n = nullptr;
+  return b;
+}
+
+efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, cudaStream_t s) {
+  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
+  if (!h->have_fwd) return fail(h, EFUNC_ESTATE, "backward without a valid forward (saved e_j missing)");
+  if (h->fwd_J == 0) return EFUNC_OK;
+  if (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_NONE)
+    return fail(h, EFUNC_EINVAL, "dL_dO is NULL and the forward had no fused loss");
+  const int eik = (dL_dG != nullptr) || (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_MSE_EIKONAL);
+  if (eik && !h->fwd_has_g) return fail(h, EFUNC_ESTATE, "dL_dG needs a forward that computed G");
+  BwdArgs b = bwd_args(h, dL_dO, dL_dG, grad, eik);
+  CK(cudaMemsetAsync(&h->ds->bwd_next, 0, sizeof(uint32_t), s));
   if (h->cfg.deterministic) {
     CK(cudaMemsetAsync(&h->ds->umax, 0, sizeof(float), s));
     h->launches += launch_backward_det(b, h->fwd_items_bound, s);
     h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);
   } else {
+    const int slot = timing_begin(h, s);
     h->launches += launch_backward(b, h->fwd_items_bound, s);
+    timing_end(h, slot, s);
     h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
   }
   CK(cudaGetLastError());
+  return EFUNC_OK;
+}
+
+// efunc_forward_backward: the fused fit kernel for the MSE loss (k_fit.cu), the split kernels for
+// its leftover items; forward + backward otherwise.
+efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                                 float* O, float* grad, float* loss_out, cudaStream_t s) {
+  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
+  if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "forward_backward needs a loss");
+  const int fused = loss->kind == EFUNC_LOSS_MSE && !h->cfg.deterministic && !h->count_kept;
+  if (!fused || J == 0) {
+    RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
+    RET(do_backward(h, nullptr, nullptr, grad, s));
+    h->have_fwd = 0;
+    return EFUNC_OK;
+  }
+  if (J < 0) return fail(h, EFUNC_EINVAL, "J < 0");
+  if (loss->kind < EFUNC_LOSS_NONE || loss->kind > EFUNC_LOSS_MSE_EIKONAL) return fail(h, EFUNC_EINVAL, "bad loss kind");
+  if (!q || !o) return fail(h, EFUNC_EINVAL, "q or o is NULL");
+  if (J > (int64_t)0x7fffffff) return fail(h, EFUNC_EINVAL, "J > 2^31-1 per call");
+  h->have_fwd = 0;
+  if (!h->fit_scratch) {
+    drop_fit_graph(h);
+    CK(dalloc(&h->fit_scratch, fit_scratch_entries()));
+  }
+  FwdArgs a;
+  RET(prep_queries(h, q, o, J, loss, a, s));
+  a.O = O;
+  a.G = nullptr;
+  FitArgs f;
+  f.f = a;
+  f.gpad = h->gpad;
+  f.scratch = h->fit_scratch;
+  const int slot = timing_begin(h, s);
+  h->launches += launch_fit(f, h->fwd_items_bound, s);
+  timing_end(h, slot, s);
+  // items the fused kernel left (no brick list / shift-bound overflow): the split kernels
+  h->fwd_J = J;
+  h->launches += launch_forward_slow(a, s);
+  BwdArgs b = bwd_args(h, nullptr, nullptr, grad, 0);
+  b.list = h->slow_items;
+  b.list_n = &h->ds->slow_n;
+  h->launches += launch_backward(b, h->fwd_items_bound, s);
+  h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+  if (loss_out) h->launches += launch_sum_partials(h->loss_part, a.n_items, 1, loss_out, s);
+  CK(cudaGetLastError());
+  if (h->cfg.sync_checks) {
+    CK(cudaStreamSynchronize(s));
+    uint32_t nf = 0;
+    CK(cudaMemcpy(&nf, &h->ds->nonfinite, sizeof(nf), cudaMemcpyDeviceToHost));
+    if (nf) {
+      CK(cudaMemset(&h->ds->nonfinite, 0, sizeof(uint32_t)));
+      return fail(h, EFUNC_ENONFINITE, "non-finite query or target");
+    }
+  }
   return EFUNC_OK;
 }
 
@@ -456,6 +564,13 @@ efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, 
   return do_backward(h, dL_dO, dL_dG, grad, (cudaStream_t)stream);
 }
 
+efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                                    float* O, float* grad, float* loss_out, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  return do_forward_backward(h, q, o, J, loss, O, grad, loss_out, (cudaStream_t)stream);
+}
+
 efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream) {
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
@@ -500,8 +615,7 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
   float* g = grad_ws ? grad_ws : h->fit_grad;
   auto device_work = [&](cudaStream_t st) -> efunc_status {
     CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, st));
-    RET(do_forward(h, qd, od, J, loss, nullptr, nullptr, lossd, 1, st));
-    RET(do_backward(h, nullptr, nullptr, g, st));
+    RET(do_forward_backward(h, qd, od, J, loss, nullptr, g, lossd, st));
     return do_adamw(h, g, hp, st);
   };
   efunc_t::FitKey key{};
@@ -611,6 +725,35 @@ efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* 
 efunc_status efunc_set_counting(efunc_t* h, int32_t on) {
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   h->count_kept = on ? 1 : 0;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_set_timing(efunc_t* h, int32_t slots) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (slots < 0 || slots > 4096) return fail(h, EFUNC_EINVAL, "slots must be in [0, 4096]");
+  DeviceGuard dg(h->cfg.device);
+  CK(cudaDeviceSynchronize());
+  free_timing(h);
+  for (int i = 0; i < 2 * slots; ++i) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreate(&e));
+    h->tev.push_back(e);
+  }
+  h->tev_used.assign(slots, 0);
+  return EFUNC_OK;
+}
+
+efunc_status efunc_get_kernel_ms(efunc_t* h, float* ms_host, int32_t n) {
+  if (!h || !ms_host) return fail(h, EFUNC_EINVAL, "NULL argument");
+  DeviceGuard dg(h->cfg.device);
+  const int slots = (int)(h->tev.size() / 2);
+  for (int i = 0; i < n; ++i) {
+    ms_host[i] = NAN;
+    if (i >= slots || !h->tev_used[i]) continue;
+    CK(cudaEventSynchronize(h->tev[2 * i + 1]));
+    float ms = NAN;
+    if (cudaEventElapsedTime(&ms, h->tev[2 * i], h->tev[2 * i + 1]) == cudaSuccess) ms_host[i] = ms;
+  }
   return EFUNC_OK;
 }
 

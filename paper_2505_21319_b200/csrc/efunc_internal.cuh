@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "../../include/efunc.h"
 
@@ -75,7 +76,11 @@ struct DevScalars {
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
+  uint32_t fwd_next;       // persistent fetch cursors (reset before each launch)
+  uint32_t bwd_next;
+  uint32_t fit_next;
 };
+
 
 struct FwdArgs {
   KeysView kv;
@@ -133,6 +138,16 @@ struct BwdArgs {
   unsigned long long* gfix;  // [R^3][16]
   const float* umax;
   uint32_t* fix_overflow;
+  uint32_t* next;            // persistent fetch cursor (zeroed before the launch)
+  const uint32_t* list;      // null: every item; else the items list[0 .. *list_n)
+  const uint32_t* list_n;
+};
+
+// Fused fit item kernel (k_fit.cu): value-only forward + MSE upstream + backward per work item.
+struct FitArgs {
+  FwdArgs f;
+  float* gpad;            // [R^3][16] padded gradient accumulator
+  uint32_t* scratch;      // per-warp candidate-id scratch, fit_scratch_entries() ids
 };
 
 constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
@@ -168,7 +183,10 @@ int launch_items_count(const uint32_t* bin_start, uint32_t nbins, uint32_t* cnt,
 int launch_items_write(const uint32_t* bin_start, uint32_t nbins, const uint32_t* off, int4* items,
                        cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
+int launch_forward_slow(const FwdArgs& a, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
+int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
+size_t fit_scratch_entries();
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
 int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);
@@ -242,6 +260,7 @@ struct efunc {
   uint32_t* wl_off = nullptr;       // [items bound]
   uint32_t* wl_n = nullptr;         // [items bound]
   uint32_t* slow_items = nullptr;   // [items bound]
+  uint32_t* fit_scratch = nullptr;  // fused fit kernel: per-warp candidate ids
   int64_t fwd_items_bound = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;
@@ -268,5 +287,9 @@ struct efunc {
   cudaGraphExec_t fit_exec = nullptr;
   int64_t fit_launches = 0;          // kernels inside the captured graph
   cudaStream_t cap_stream = nullptr;
+  // kernel timing (efunc_set_timing): event pairs, slot = call index mod slots
+  std::vector<cudaEvent_t> tev;
+  std::vector<int> tev_used;
+  int64_t tseq = 0;
   std::string err;
 };

@@ -2,22 +2,36 @@
 // broadcast from shared memory, register accumulators (Alg. 2); per (key,
 // item) two red.global.add.v4.f32 into a 16-float-per-node padded gradient folded to the ABI
 // layout by k_fold, or 64-bit fixed-point atomics in deterministic mode.
-#include "k_common.cuh"
+#include <algorithm>
+
+#include "k_pair.cuh"
 
 namespace ef {
 
 // ------------------------------------------------------------------------------ backward
 // DET: deterministic mode, 64-bit fixed-point accumulation (see BwdArgs::gfix)
 #ifndef BK_MIN_BLOCKS
-#define BK_MIN_BLOCKS 28  // <= 72 registers (measured best of 1/28/32)
+#define BK_MIN_BLOCKS 28  // warps per SM: <= 72 registers (measured best of 1/28/32)
 #endif
+constexpr int BW_WARPS = 4;  // persistent: warps per CTA, each fetching items heaviest-first
+
+// per-warp shared memory of the backward
+template <bool EIK>
+struct BwdSmem {
+  float4 sq[QW];  // x, y, z, -lambda_l
+  float4 sv[QW];  // r, O, h.ubar, h.G
+  float4 sh[EIK ? QW : 1];
+  // MSE: the item's queries as packed pairs for f32x2 arithmetic: {x0,x1,y0,y1}, {z0,z1,w0,w1},
+  // {r0,r1,-O0,-O1} (an idle slot has w = -inf and r = 0: it contributes exactly 0)
+  float4 pA[EIK ? 1 : QW / 2], pB[EIK ? 1 : QW / 2], pC[EIK ? 1 : QW / 2];
+  float4 ka[WSLICE];  // fallback staging ring
+  float4 kb[WSLICE];
+  int kid[WSLICE];
+};
+
 template <bool EIK, bool DET>
-__global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdArgs A) {
-  float fix_scale = 0.0f;
-  if (DET) {
-    const float um = *A.umax;
-    fix_scale = um > 0.0f ? (float)(1ull << FIX_BITS) / um : 0.0f;
-  }
+__device__ __forceinline__ void backward_item(const BwdArgs& A, const uint32_t item, BwdSmem<EIK>& S,
+                                              const float fix_scale) {
   auto fix_add = [&](unsigned long long* p, float v) {
     const float qv = v * fix_scale;
     if (fabsf(qv) < 4.0e18f) {
@@ -26,20 +40,11 @@ __global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdA
       atomicOr(A.fix_overflow, 1u);
     }
   };
-  __shared__ float4 sq[NWARP][QW];  // x, y, z, -lambda_l
-  __shared__ float4 sv[NWARP][QW];  // r, O, h.ubar, h.G
-  __shared__ float4 sh[EIK ? NWARP : 1][EIK ? QW : 1];
-  // MSE: the item's queries as packed pairs for f32x2 arithmetic: {x0,x1,y0,y1}, {z0,z1,w0,w1},
-  // {r0,r1,-O0,-O1} (an idle slot has w = -inf and r = 0: it contributes exactly 0)
-  static_assert(NWARP == 1, "packed query pairs assume one warp per CTA");
-  __shared__ float4 pA[EIK ? 1 : QW / 2], pB[EIK ? 1 : QW / 2], pC[EIK ? 1 : QW / 2];
-  __shared__ float4 ka_s[NWARP][WSLICE];
-  __shared__ float4 kb_s[NWARP][WSLICE];
-  __shared__ int kid_s[NWARP][WSLICE];
+  float4* const pA = S.pA;
+  float4* const pB = S.pB;
+  float4* const pC = S.pC;
   const KeysView& kv = A.kv;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t item = blockIdx.x * NWARP + w;
-  if (item >= *A.n_items) return;
+  const int lane = threadIdx.x & 31;
   const int4 it = A.items[item];
   const int nact = it.y;
   Box box;
@@ -62,15 +67,15 @@ __global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdA
         const float4 G = A.gs[js], ub = A.us[js];
         hub = hv.x * ub.x + hv.y * ub.y + hv.z * ub.z;
         T = hv.x * G.x + hv.y * G.y + hv.z * G.z;
-        sh[w][j] = hv;
+        S.sh[j] = hv;
       }
       q.w = rc.x;
-      sq[w][j] = q;
-      sv[w][j] = make_float4(r, rc.z, hub, T);
+      S.sq[j] = q;
+      S.sv[j] = make_float4(r, rc.z, hub, T);
     }
     if (!EIK) {
       const float x = q.x, y = q.y, z = q.z, wv = act ? q.w : -INFINITY;
-      const float r = act ? sv[w][j].x : 0.f, nO = act ? -sv[w][j].y : 0.f;
+      const float r = act ? S.sv[j].x : 0.f, nO = act ? -S.sv[j].y : 0.f;
       const float xo = __shfl_xor_sync(~0u, x, 1), yo = __shfl_xor_sync(~0u, y, 1), zo = __shfl_xor_sync(~0u, z, 1);
       const float wo = __shfl_xor_sync(~0u, wv, 1), ro = __shfl_xor_sync(~0u, r, 1), nOo = __shfl_xor_sync(~0u, nO, 1);
       if ((lane & 1) == 0) {
@@ -91,12 +96,12 @@ __global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdA
   }
   box.thr += A.T_l;
   __syncwarp();
-  const float4* Q = sq[w];
-  const float4* V = sv[w];
-  const float4* H = sh[EIK ? w : 0];
-  float4* sa = ka_s[w];
-  float4* sb = kb_s[w];
-  int* sid = kid_s[w];
+  const float4* Q = S.sq;
+  const float4* V = S.sv;
+  const float4* H = S.sh;
+  float4* sa = S.ka;
+  float4* sb = S.kb;
+  int* sid = S.kid;
   float* gpad = A.gpad;
   const int n_nodes = kv.n_nodes;
 
@@ -153,41 +158,10 @@ __global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdA
       }
     };
     if (!EIK) {
-      // two queries per f32x2 instruction; the halves are summed at the end
-      const float2 nx = make_float2(-a.x, -a.x), ny = make_float2(-a.y, -a.y), nz = make_float2(-a.z, -a.z);
-      const float2 nbl = make_float2(-a.w, -a.w);
-      const float2 c2 = make_float2(b.x, b.x), gx2 = make_float2(b.y, b.y), gy2 = make_float2(b.z, b.z),
-                   gz2 = make_float2(b.w, b.w);
-      float2 Sc = make_float2(0.f, 0.f), Sgx = Sc, Sgy = Sc, Sgz = Sc, Ss = Sc, Sdx = Sc, Sdy = Sc, Sdz = Sc;
-      const int npairs = (nact + 1) >> 1;
-#pragma unroll 2
-      for (int jp = 0; jp < npairs; ++jp) {
-        const float4 QA = pA[jp], QB = pB[jp], QC = pC[jp];
-        const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), nx);
-        const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), ny);
-        const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), nz);
-        float2 dd = __fmul2_rn(dz, dz);
-        dd = __ffma2_rn(dy, dy, dd);
-        dd = __ffma2_rn(dx, dx, dd);
-        const float2 e = __ffma2_rn(nbl, dd, make_float2(QB.z, QB.w));
-        const float2 p = make_float2(ex2f(e.x), ex2f(e.y));
-        float2 f = __ffma2_rn(gx2, dx, c2);
-        f = __ffma2_rn(gy2, dy, f);
-        f = __ffma2_rn(gz2, dz, f);
-        const float2 del = __fadd2_rn(f, make_float2(QC.z, QC.w));
-        const float2 t = __fmul2_rn(make_float2(QC.x, QC.y), p);
-        const float2 u = __fmul2_rn(t, del);
-        Sc = __fadd2_rn(Sc, t);
-        Sgx = __ffma2_rn(t, dx, Sgx);
-        Sgy = __ffma2_rn(t, dy, Sgy);
-        Sgz = __ffma2_rn(t, dz, Sgz);
-        Ss = __ffma2_rn(u, dd, Ss);
-        Sdx = __ffma2_rn(u, dx, Sdx);
-        Sdy = __ffma2_rn(u, dy, Sdy);
-        Sdz = __ffma2_rn(u, dz, Sdz);
-      }
-      sc = Sc.x + Sc.y; sgx = Sgx.x + Sgx.y; sgy = Sgy.x + Sgy.y; sgz = Sgz.x + Sgz.y;
-      ss = Ss.x + Ss.y; sdx = Sdx.x + Sdx.y; sdy = Sdy.x + Sdy.y; sdz = Sdz.x + Sdz.y;
+      // two queries per f32x2 instruction (k_pair.cuh)
+      const MseSums ms = bwd_mse_sums(a, b, (nact + 1) >> 1, pA, pB, pC);
+      sc = ms.sc; sgx = ms.sgx; sgy = ms.sgy; sgz = ms.sgz;
+      ss = ms.ss; sdx = ms.sdx; sdy = ms.sdy; sdz = ms.sdz;
     } else {
       // register double-buffering of the broadcast query loads hides the LDS latency
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -300,11 +274,32 @@ __global__ void __launch_bounds__(NTHREADS, BK_MIN_BLOCKS) k_backward(const BwdA
   if (cnt) consume(head, cnt);
 }
 
+template <bool EIK, bool DET>
+__global__ void __launch_bounds__(32 * BW_WARPS, BK_MIN_BLOCKS / BW_WARPS) k_backward(const BwdArgs A) {
+  __shared__ BwdSmem<EIK> smem[BW_WARPS];
+  float fix_scale = 0.0f;
+  if (DET) {
+    const float um = *A.umax;
+    fix_scale = um > 0.0f ? (float)(1ull << FIX_BITS) / um : 0.0f;
+  }
+  BwdSmem<EIK>& S = smem[threadIdx.x >> 5];
+  for (;;) {
+    const int64_t item = fetch_item(A.next, A.n_items, A.list, A.list_n);
+    if (item < 0) break;
+    __syncwarp();  // the previous item's readers of S are done
+    backward_item<EIK, DET>(A, (uint32_t)item, S, fix_scale);
+  }
+}
+
+static unsigned bwd_blocks(int64_t n_items) {
+  return (unsigned)std::min<int64_t>((n_items + BW_WARPS - 1) / BW_WARPS, 148 * (BK_MIN_BLOCKS / BW_WARPS));
+}
+
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
-  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
-  if (a.eik) k_backward<true, false><<<blocks, NTHREADS, 0, s>>>(a);
-  else k_backward<false, false><<<blocks, NTHREADS, 0, s>>>(a);
+  const unsigned blocks = bwd_blocks(n_items);
+  if (a.eik) k_backward<true, false><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
+  else k_backward<false, false><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
   return 1;
 }
 
@@ -329,9 +324,9 @@ int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   long ub = (a.J + 255) / 256;
   if (ub > 148 * 8) ub = 148 * 8;
   k_upstream_max<<<(unsigned)(ub < 1 ? 1 : ub), 256, 0, s>>>(a, const_cast<float*>(a.umax));
-  const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
-  if (a.eik) k_backward<true, true><<<blocks, NTHREADS, 0, s>>>(a);
-  else k_backward<false, true><<<blocks, NTHREADS, 0, s>>>(a);
+  const unsigned blocks = bwd_blocks(n_items);
+  if (a.eik) k_backward<true, true><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
+  else k_backward<false, true><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
   return 2;
 }
 

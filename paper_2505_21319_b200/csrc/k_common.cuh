@@ -320,6 +320,9 @@ __device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, 
       g0 = make_float3(kb.y, kb.z, kb.w);
     }
   }
+#ifdef EF_CORNERS_ONLY
+  return;
+#endif
   const int cid = (cz * NC + cy) * NC + cx;
   const uint32_t s = __ldg(&kv.cell_start[cid]);
   const uint32_t e_ = min(__ldg(&kv.cell_start[cid + 1]), s + 32u);
@@ -334,6 +337,18 @@ __device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, 
       g0 = make_float3(kb.y, kb.z, kb.w);
     }
   }
+}
+
+// Persistent-kernel work fetch (warp-uniform): the next item in index order (Morton order keeps
+// the co-resident warps of an SM on neighbouring items, which share key records in L1/L2), or
+// -1 when all are taken. With a list, the g-th item is list[g] of *list_n.
+__device__ __forceinline__ int64_t fetch_item(uint32_t* next, const uint32_t* n_items, const uint32_t* list,
+                                              const uint32_t* list_n) {
+  uint32_t g = 0;
+  if ((threadIdx.x & 31) == 0) g = atomicAdd(next, 1u);
+  g = __shfl_sync(~0u, g, 0);
+  if (list) return g < __ldcg(list_n) ? (int64_t)__ldcg(&list[g]) : -1;
+  return g < *n_items ? (int64_t)g : -1;
 }
 
 __device__ __forceinline__ float exponent(const float4 q, const float4 a) {

@@ -11,7 +11,9 @@
 //     partial sums in registers, one transpose-reduction per item (Alg. 1).
 //   k_forward (G forward, exact-min slow path, kept-pair census): lanes = queries, staged keys
 //     broadcast (Alg. 1 and the G sums of Eq. func-normal).
-#include "k_common.cuh"
+#include <algorithm>
+
+#include "k_pair.cuh"
 
 namespace ef {
 
@@ -261,28 +263,6 @@ __global__ void __launch_bounds__(NTHREADS) k_forward(const FwdArgs A, const int
 }
 
 // ------------------------------------------------------------------ forward, lanes = keys
-// Reduce-scatter of N per-lane values over the warp: afterwards lane l holds in v[0 .. N/32) the
-// warp totals of values [l N/32, (l+1) N/32) (N = 32 or 64). 31 (N=32) / 62 (N=64) shuffles.
-template <int N>
-__device__ __forceinline__ void warp_reduce_scatter(float (&v)[N], const int lane) {
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int o = 16 >> st;
-    const int c = N >> (st + 1);  // values kept after this step (compile-time once unrolled)
-    if (c >= 1) {
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < c; ++i) {
-        const float send = up ? v[i] : v[i + c];
-        const float keep = up ? v[i + c] : v[i];
-        v[i] = keep + __shfl_xor_sync(~0u, send, o);
-      }
-    } else {
-      v[0] += __shfl_xor_sync(~0u, v[0], o);
-    }
-  }
-}
-
 // S2a (value-only forward, part 1): per item, the shift bounds mh_j and the compacted candidate
 // ids (the item's warp-box test over its brick list) written to the item's slice of wl_pool.
 // Latency-bound gathers: few registers and 4 independent warps per CTA for occupancy.
@@ -332,114 +312,13 @@ __global__ void __launch_bounds__(32 * IL_WARPS) k_item_lists(const FwdArgs A) {
   }
 }
 
-// S2b (value-only forward, part 2): lanes = the item's candidate keys (its wl list, ids two
-// rounds ahead, records one round ahead), the item's queries broadcast from shared memory as
-// packed pairs (f32x2: two queries per instruction), per-query partial sums Z_j, M_j in
-// registers, one transpose-reduction per item (Alg. 1).
-// NPM = max query pairs (8: <= 16 queries, 16: <= 32). Returns Z_j, M_j to lane j.
-#define FK_PAIR(pp) \
-  { \
-    const float4 QA = sQA[pp], QB = sQB[pp]; /* {x0,x1,y0,y1}, {z0,z1,mh0,mh1} */ \
-    const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), nx); \
-    const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), ny); \
-    const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), nz); \
-    float2 dd = __fmul2_rn(dz, dz); \
-    dd = __ffma2_rn(dy, dy, dd); \
-    dd = __ffma2_rn(dx, dx, dd); \
-    const float2 e = __ffma2_rn(nbl, dd, make_float2(QB.z, QB.w)); \
-    const float2 wv = make_float2(ex2f(e.x), ex2f(e.y)); \
-    float2 f = __ffma2_rn(gx, dx, c); \
-    f = __ffma2_rn(gy, dy, f); \
-    f = __ffma2_rn(gz, dz, f); \
-    Z[pp] = __fadd2_rn(Z[pp], wv); \
-    M[pp] = __ffma2_rn(wv, f, M[pp]); \
-  }
-template <int NPM>
-__device__ __forceinline__ void fwd_keys_sums(const KeysView& kv, const uint32_t* L, const uint32_t wn,
-                                              const int nact, const float4* sQA, const float4* sQB,
-                                              float& Zj, float& Mj) {
-  const int lane = threadIdx.x & 31;
-  const int npairs = (nact + 1) >> 1;
-  float2 Z[NPM], M[NPM];
-#pragma unroll
-  for (int pp = 0; pp < NPM; ++pp) {
-    Z[pp] = make_float2(0.f, 0.f);
-    M[pp] = make_float2(0.f, 0.f);
-  }
-  // one round: lane = one key, loop over the item's query pairs
-  auto round = [&](const float4 ka, const float4 kb) {
-    const float2 nx = make_float2(-ka.x, -ka.x), ny = make_float2(-ka.y, -ka.y), nz = make_float2(-ka.z, -ka.z);
-    const float2 nbl = make_float2(-ka.w, -ka.w);
-    const float2 c = make_float2(kb.x, kb.x), gx = make_float2(kb.y, kb.y), gy = make_float2(kb.z, kb.z),
-                 gz = make_float2(kb.w, kb.w);
-    // groups of 4 pairs without a branch inside, so the scheduler can interleave their chains;
-    // the last 1-3 pairs one by one (an odd query count pads one slot with shift -inf: weight 0)
-#pragma unroll
-    for (int pg = 0; pg < NPM; pg += 4) {
-      const int rem = npairs - pg;
-      if (rem >= 4) {
-        FK_PAIR(pg) FK_PAIR(pg + 1) FK_PAIR(pg + 2) FK_PAIR(pg + 3)
-      } else if (rem > 0) {
-        FK_PAIR(pg)
-        if (rem >= 2) FK_PAIR(pg + 1)
-        if (rem >= 3) FK_PAIR(pg + 2)
-      }
-    }
-  };
-  // idle lanes of the last round get a far-away zero key: weight exactly 0
-  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
-  uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
-  float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : far_a;
-  float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
-  for (uint32_t base = 0; base < wn; base += 32) {
-    const uint32_t k = base + lane;
-    const float4 ka = a1, kb = b1;
-    id1 = id2;
-    id2 = (k + 64 < wn) ? L[k + 64] : 0u;
-    a1 = far_a;
-    b1 = z4;
-    if (k + 32 < wn) {
-      a1 = __ldg(&kv.grid_raw[2 * id1]);
-      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
-    }
-    round(ka, kb);
-  }
-  // transpose-reduce {Zx, Zy, Mx, My} of every pair; lane j then fetches its query's totals
-  if (NPM == 8) {
-    float v[32];
-#pragma unroll
-    for (int pp = 0; pp < 8; ++pp) {
-      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
-    }
-    warp_reduce_scatter<32>(v, lane);  // lane l holds value l
-    const int j = lane & 15;
-    Zj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + (j & 1));
-    Mj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + 2 + (j & 1));
-  } else {
-    float v[64];
-#pragma unroll
-    for (int pp = 0; pp < NPM; ++pp) {
-      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
-    }
-    warp_reduce_scatter<64>(v, lane);  // lane l holds values 2l, 2l+1
-    const int src = lane & ~1;
-    const float z0 = __shfl_sync(~0u, v[0], src), z1 = __shfl_sync(~0u, v[1], src);
-    const float m0 = __shfl_sync(~0u, v[0], src + 1), m1 = __shfl_sync(~0u, v[1], src + 1);
-    Zj = (lane & 1) ? z1 : z0;
-    Mj = (lane & 1) ? m1 : m0;
-  }
-}
-
 #ifndef FK_MIN_BLOCKS
-#define FK_MIN_BLOCKS 16  // <= 128 registers (measured: 1/16/20/24; half-item warps were slower)
+#define FK_MIN_BLOCKS 16  // warps per SM: <= 128 registers (measured: 1/16/20/24; half-item warps were slower)
 #endif
-__global__ void __launch_bounds__(NTHREADS, FK_MIN_BLOCKS) k_forward_keys(const FwdArgs A) {
-  static_assert(NWARP == 1 && QW == 32, "k_forward_keys: one warp per CTA, <= 32 queries per item");
-  __shared__ float4 sQA[QW / 2], sQB[QW / 2];
+constexpr int FK_WARPS = 4;  // persistent: warps per CTA, each fetching items heaviest-first
+__device__ __forceinline__ void forward_keys_item(const FwdArgs& A, const uint32_t item, float4* sQA, float4* sQB) {
+  static_assert(QW == 32, "k_forward_keys: <= 32 queries per item");
   const int lane = threadIdx.x & 31;
-  const uint32_t item = blockIdx.x;
-  if (item >= *A.n_items) return;
   const int4 it = A.items[item];
   const int nact = it.y;
   const uint32_t wn = A.wl_n[item];
@@ -455,6 +334,7 @@ __global__ void __launch_bounds__(NTHREADS, FK_MIN_BLOCKS) k_forward_keys(const 
     q = A.qs[js];
     mh = A.qmh[js];
   }
+  __syncwarp();  // the previous item's readers of sQA/sQB are done
   {
     const float xo = __shfl_xor_sync(~0u, q.x, 1), yo = __shfl_xor_sync(~0u, q.y, 1);
     const float zo = __shfl_xor_sync(~0u, q.z, 1), mo = __shfl_xor_sync(~0u, mh, 1);
@@ -495,6 +375,21 @@ __global__ void __launch_bounds__(NTHREADS, FK_MIN_BLOCKS) k_forward_keys(const 
   }
 }
 
+__global__ void __launch_bounds__(32 * FK_WARPS, FK_MIN_BLOCKS / FK_WARPS) k_forward_keys(const FwdArgs A) {
+  __shared__ float4 sQA[FK_WARPS][QW / 2], sQB[FK_WARPS][QW / 2];
+  const int w = threadIdx.x >> 5;
+  for (;;) {
+    const int64_t item = fetch_item(&A.ds->fwd_next, A.n_items, nullptr, nullptr);
+    if (item < 0) break;
+    forward_keys_item(A, (uint32_t)item, sQA[w], sQB[w]);
+  }
+}
+
+int launch_forward_slow(const FwdArgs& a, cudaStream_t s) {
+  k_forward<false><<<148 * 4, NTHREADS, 0, s>>>(a, 1);  // the items in a.slow_items (usually none)
+  return 1;
+}
+
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);
@@ -504,7 +399,9 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
     return 1;
   }
   k_item_lists<<<(unsigned)((n_items + IL_WARPS - 1) / IL_WARPS), 32 * IL_WARPS, 0, s>>>(a);
-  k_forward_keys<<<blocks, NTHREADS, 0, s>>>(a);
+  const unsigned pblocks =
+      (unsigned)std::min<int64_t>((n_items + FK_WARPS - 1) / FK_WARPS, 148 * (FK_MIN_BLOCKS / FK_WARPS));
+  k_forward_keys<<<pblocks, 32 * FK_WARPS, 0, s>>>(a);
   k_forward<false><<<148 * 4, NTHREADS, 0, s>>>(a, 1);  // slow-path items (usually none)
   return 3;
 }

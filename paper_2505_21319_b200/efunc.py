@@ -21,10 +21,12 @@ LOSS_NONE, LOSS_MSE, LOSS_MSE_EIKONAL = 0, 1, 2
 # default decay mask (reading R-10 / SPEC D15): polynomial coefficients c, g of both banks
 DEFAULT_DECAY_MASK = (1 << 1) | (0b111 << 2) | (1 << 9) | (0b111 << 10)
 
-EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", "efunc_adamw_step",
+EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", "efunc_forward_backward",
+            "efunc_adamw_step",
             "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
-            "efunc_get_stats", "efunc_check", "efunc_last_error", "efunc_abi_version"]
+            "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_last_error",
+            "efunc_abi_version"]
 
 
 class Config(C.Structure):
@@ -73,6 +75,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_destroy": [P],
         "efunc_forward": [P, P, P, i64, C.POINTER(Loss), P, P, P, P],
         "efunc_backward": [P, P, P, P, P],
+        "efunc_forward_backward": [P, P, P, i64, C.POINTER(Loss), P, P, P, P],
         "efunc_adamw_step": [P, P, C.POINTER(AdamWParams), P],
         "efunc_eval_grad": [P, P, i64, P, P, P],
         "efunc_fit_step": [P, P, P, i64, C.POINTER(Loss), C.POINTER(AdamWParams), P, P, i32, P],
@@ -84,6 +87,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_set_counting": [P, i32],
         "efunc_get_stats": [P, C.POINTER(Stats), P],
         "efunc_check": [P, P],
+        "efunc_set_timing": [P, i32],
+        "efunc_get_kernel_ms": [P, P, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -198,6 +203,23 @@ class EFunc:
         self._ok(self.lib.efunc_backward(self.h, _ptr(dL_dO), _ptr(dL_dG), _ptr(grad), self._stream()))
         return grad
 
+    def forward_backward(self, q, o, loss: int = LOSS_MSE, eikonal_lambda: float = 0.1, J_global: int = 0,
+                         grad=None, want_O: bool = False, want_loss: bool = True):
+        """forward + fused loss upstream + backward in one call (the fused fit kernel for MSE).
+        Returns (grad, O, loss); grad is accumulated into (+=) when given."""
+        J = q.shape[0] if q.dim() == 2 else q.numel() // 3
+        _check_dev(q, "q", 3 * J, self.device)
+        _check_dev(o, "o", J, self.device)
+        if grad is None:
+            grad = self._torch.zeros(self.R ** 3, NCH, dtype=self._torch.float32, device=f"cuda:{self.device}")
+        _check_dev(grad, "grad", self.n_params, self.device)
+        O = self._empty(J) if want_O else None
+        L = self._empty(1) if want_loss else None
+        lc = Loss(loss, eikonal_lambda, J_global)
+        self._ok(self.lib.efunc_forward_backward(self.h, _ptr(q), _ptr(o), J, C.byref(lc), _ptr(O), _ptr(grad),
+                                                 _ptr(L), self._stream()))
+        return grad, O, L
+
     def adamw_step(self, grad, hp: AdamW | None = None):
         hp = hp or AdamW()
         _check_dev(grad, "grad", self.n_params, self.device)
@@ -261,6 +283,15 @@ class EFunc:
 
     def set_counting(self, on: bool):
         self._ok(self.lib.efunc_set_counting(self.h, int(on)))
+
+    def set_timing(self, slots: int):
+        """Record CUDA events around the dominant kernel of each backward/forward_backward call."""
+        self._ok(self.lib.efunc_set_timing(self.h, int(slots)))
+
+    def kernel_ms(self, n: int) -> list:
+        buf = (C.c_float * n)()
+        self._ok(self.lib.efunc_get_kernel_ms(self.h, C.addressof(buf), int(n)))
+        return [float(x) for x in buf]
 
     def stats(self) -> dict:
         s = Stats()
