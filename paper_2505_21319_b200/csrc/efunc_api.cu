@@ -232,7 +232,7 @@ void free_all(efunc_t* h) {
 // S1 for one forward: query bins, stable counting sort, gather, work items; then the forward
 // arguments (everything but the outputs).
 efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64_t J, const efunc_loss* loss,
-                          FwdArgs& a, cudaStream_t s) {
+                          FwdArgs& a, cudaStream_t s, int with_mh = 0) {
   const int kind = loss ? loss->kind : EFUNC_LOSS_NONE;
   RET(ensure_queries(h, J));
   const uint32_t nb = h->bg.n_codes;             // bricks
@@ -247,7 +247,10 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
   h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
-  h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
+  if (with_mh)  // + the per-query shift bound (fused path)
+    h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh, s);
+  else
+    h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
   // work items: balanced runs of <= QW sorted queries of one brick
   h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
   h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
@@ -404,7 +407,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
     CK(dalloc(&h->fit_scratch, fit_scratch_entries()));
   }
   FwdArgs a;
-  RET(prep_queries(h, q, o, J, loss, a, s));
+  RET(prep_queries(h, q, o, J, loss, a, s, 1));
   a.O = O;
   a.G = nullptr;
   FitArgs f;

@@ -179,6 +179,8 @@ int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom
                       cudaStream_t s);
 int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
                           float4* qs, int* perm, cudaStream_t s);
+int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
+                             float4* qs, int* perm, float* qmh, cudaStream_t s);
 int launch_items_count(const uint32_t* bin_start, uint32_t nbins, uint32_t* cnt, cudaStream_t s);
 int launch_items_write(const uint32_t* bin_start, uint32_t nbins, const uint32_t* off, int4* items,
                        cudaStream_t s);

@@ -2,18 +2,28 @@
 // work item).
 //
 // Per work item (<= 32 sorted queries of one brick, one warp, persistent warps in Morton order):
-//   1. shift bounds mh_j >= m_j (the "maximum-reduce" of PAPER.md:L501) and the warp's box test
-//      over the brick's candidate list -> the item's candidate key ids in the warp's scratch;
-//   2. forward, lanes = candidate keys, queries broadcast as packed pairs: Z_j, M_j (Alg. 1,
-//      PAPER.md:L505-518), O_j = M_j / Z_j, lambda_j, the MSE loss and r_j = 2(O_j - o_j)/J
-//      (Eq. loss);
+//   1. the queries' shift bounds mh_j >= m_j (computed by k_gather_queries_mh) and the warp's box
+//      test over the brick's candidate list -> the item's candidate key ids in the warp's scratch
+//      (every skipped pair has a_ij - m_j > cutoff_T, reading R-1);
+//   2. forward, lanes = candidate keys, queries broadcast as packed pairs: Z_j = sum_i e^-a_ij,
+//      M_j = sum_i e^-a_ij f_i(q_j) (Alg. 1), O_j = M_j / Z_j, the MSE loss and
+//      r_j = 2(O_j - o_j)/J (Eq. loss);
 //   3. backward over the same candidate ids, lanes = keys (Alg. 2), two
 //      red.global.add.v4 per (key, item) into the padded gradient.
-// The MSE upstream of a query depends on that query alone, so nothing crosses items: the split
-// path's k_item_lists / k_forward_keys / k_backward launches, their candidate-id hand-off through
-// HBM and two of the three passes over the queries collapse into one kernel whose latency-bound
-// list phase overlaps other warps' FP32 phases. Items without a brick list, or whose shift bound
-// overflowed, are left to the split kernels (ds->slow_items).
+// The MSE upstream of a query depends on that query alone, so nothing crosses items.
+//
+// Item-local expansion. With o the centre of the item's box, q' = q - o and k' = k - o,
+//   a_ij log2(e) = bl_i |q'_j - k'_i|^2 = bl_i qq_j - A_i . q'_j - C_i,
+//   qq_j = |q'_j|^2, A_i = 2 bl_i k'_i, C_i = -bl_i |k'_i|^2,
+// so the exponent of a pair is 4 FMAs (instead of 3 subtractions, 3 for |d|^2 and the scale), and
+//   f_i(q_j) = c_i + g_i . (q_j - k_i) = c'_i + g_i . q'_j,  c'_i = c_i - g_i . k'_i.
+// Both are exact rewrites; rounding stays at the level of the direct form because |q'|, |k'| are
+// small (a cell and the cutoff radius). The forward is unshifted: Z_j = sum 2^(-a_ij log2 e)
+// needs m_j < ~100 log2 units, else the item goes to the split kernels (exact shift). The
+// backward sums are taken in q' and mapped to d = q' - k' per key at the end:
+//   sum t d = sum t q' - k' sum t,   sum u |d|^2 = sum u qq - 2 k' . sum u q' + |k'|^2 sum u,
+// with t_ij = r_j p_ij = (r_j / Z_j) 2^(-a_ij log2 e) and u_ij = t_ij (f_i(q_j) - O_j).
+// Items without a brick list, or whose Z underflowed, are left to the split kernels.
 #include <algorithm>
 
 #include "k_pair.cuh"
@@ -21,18 +31,175 @@
 namespace ef {
 
 #ifndef FT_MIN_WARPS
-#define FT_MIN_WARPS 16  // warps per SM (measured 16/20/24/28 with FT_NPM 8 and 16: 16 + 16 best)
-#endif
-#ifndef FT_NPM
-#define FT_NPM 16  // forward: query pairs per accumulator set (8: two passes for > 16 queries)
+#define FT_MIN_WARPS 16  // warps per SM (measured 16..28; the 16-pair forward needs 128 registers)
 #endif
 constexpr int FT_WARPS = 4;
 constexpr int FT_BLOCKS = 148 * (FT_MIN_WARPS / FT_WARPS);
+constexpr float FT_ZMIN = 7.8886e-31f;  // 2^-100: smaller Z_j -> exact-shift split path
 
 struct FitSmem {
-  float4 qa[QW / 2], qb[QW / 2];            // forward: {x0,x1,y0,y1}, {z0,z1,mh0,mh1}
-  float4 pa[QW / 2], pb[QW / 2], pc[QW / 2];  // backward: {x,y}, {z,w}, {r,-O} pairs
+  float4 qa[QW / 2], qb[QW / 2];              // {x'0,x'1,y'0,y'1}, {z'0,z'1,qq0,qq1}
+  float4 pc[QW / 2];                          // backward: {rho0,rho1,-O0,-O1}
 };
+
+// per-key constants of the expansion
+struct KeyX {
+  float nbl, C, Ax, Ay, Az, c, gx, gy, gz, kx, ky, kz, kk;
+};
+
+__device__ __forceinline__ KeyX key_x(const float4 a, const float4 b, const float3 o) {
+  KeyX k;
+  k.kx = a.x - o.x;
+  k.ky = a.y - o.y;
+  k.kz = a.z - o.z;
+  k.kk = fmaf(k.kx, k.kx, fmaf(k.ky, k.ky, k.kz * k.kz));
+  k.nbl = -a.w;
+  k.C = -a.w * k.kk;
+  const float bl2 = 2.0f * a.w;
+  k.Ax = bl2 * k.kx;
+  k.Ay = bl2 * k.ky;
+  k.Az = bl2 * k.kz;
+  k.c = fmaf(-b.w, k.kz, fmaf(-b.z, k.ky, fmaf(-b.y, k.kx, b.x)));
+  k.gx = b.y;
+  k.gy = b.z;
+  k.gz = b.w;
+  return k;
+}
+
+// exponent (log2 units, <= 0) and polynomial value of one key at a packed query pair
+#define FX_EF(K, QA, QB, e, f)                                                   \
+  float2 e = __ffma2_rn(make_float2(K.nbl, K.nbl), make_float2(QB.z, QB.w), make_float2(K.C, K.C)); \
+  e = __ffma2_rn(make_float2(K.Ax, K.Ax), make_float2(QA.x, QA.y), e);          \
+  e = __ffma2_rn(make_float2(K.Ay, K.Ay), make_float2(QA.z, QA.w), e);          \
+  e = __ffma2_rn(make_float2(K.Az, K.Az), make_float2(QB.x, QB.y), e);          \
+  float2 f = __ffma2_rn(make_float2(K.gx, K.gx), make_float2(QA.x, QA.y), make_float2(K.c, K.c)); \
+  f = __ffma2_rn(make_float2(K.gy, K.gy), make_float2(QA.z, QA.w), f);          \
+  f = __ffma2_rn(make_float2(K.gz, K.gz), make_float2(QB.x, QB.y), f);
+
+// Forward sums, lanes = keys: one round = 32 candidate keys (records one round ahead, ids two),
+// every lane walks the item's query pairs; Z, M per query pair in registers; one transpose-
+// reduction per item returns Z_j, M_j to lane j. NPM = query pairs held (8: <= 16 queries).
+template <int NPM>
+__device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
+                                           const int nact, const float3 o, const float4* sQA,
+                                           const float4* sQB, float& Zj, float& Mj) {
+  const int lane = threadIdx.x & 31;
+  const int npairs = (nact + 1) >> 1;
+  float2 Z[NPM], M[NPM];
+#pragma unroll
+  for (int pp = 0; pp < NPM; ++pp) {
+    Z[pp] = make_float2(0.f, 0.f);
+    M[pp] = make_float2(0.f, 0.f);
+  }
+  auto round = [&](const KeyX& K) {
+#define FX_PAIR(pp)                                  \
+  {                                                  \
+    const float4 QA = sQA[pp], QB = sQB[pp];         \
+    FX_EF(K, QA, QB, e, f)                           \
+    const float2 w = make_float2(ex2f(e.x), ex2f(e.y)); \
+    Z[pp] = __fadd2_rn(Z[pp], w);                    \
+    M[pp] = __ffma2_rn(w, f, M[pp]);                 \
+  }
+    // groups of 4 pairs without a branch inside; a last group of 1-2 pairs runs as 2, of 3 as 4
+    // (padding slots are idle queries with qq = 1e30: weight exactly 0)
+#pragma unroll
+    for (int pg = 0; pg < NPM; pg += 4) {
+      const int rem = npairs - pg;
+      if (rem >= 3) {
+        FX_PAIR(pg) FX_PAIR(pg + 1) FX_PAIR(pg + 2) FX_PAIR(pg + 3)
+      } else if (rem > 0) {
+        FX_PAIR(pg) FX_PAIR(pg + 1)
+      }
+    }
+#undef FX_PAIR
+  };
+  // idle lanes of the last round get a far-away zero key: weight exactly 0
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
+  uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : far_a;
+  float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
+  for (uint32_t base = 0; base < wn; base += 32) {
+    const uint32_t k = base + lane;
+    const float4 ka = a1, kb = b1;
+    id1 = id2;
+    id2 = (k + 64 < wn) ? L[k + 64] : 0u;
+    a1 = far_a;
+    b1 = z4;
+    if (k + 32 < wn) {
+      a1 = __ldg(&kv.grid_raw[2 * id1]);
+      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+    }
+    round(key_x(ka, kb, o));
+  }
+  // transpose-reduce {Zx, Zy, Mx, My} of every pair; lane j then fetches its query's totals
+  if (NPM == 8) {
+    float v[32];
+#pragma unroll
+    for (int pp = 0; pp < 8; ++pp) {
+      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
+    }
+    warp_reduce_scatter<32>(v, lane);  // lane l holds value l
+    const int j = lane & 15;
+    Zj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + (j & 1));
+    Mj = __shfl_sync(~0u, v[0], 4 * (j >> 1) + 2 + (j & 1));
+  } else {
+    float v[64];
+#pragma unroll
+    for (int pp = 0; pp < NPM; ++pp) {
+      v[4 * pp] = Z[pp].x; v[4 * pp + 1] = Z[pp].y; v[4 * pp + 2] = M[pp].x; v[4 * pp + 3] = M[pp].y;
+    }
+    warp_reduce_scatter<64>(v, lane);  // lane l holds values 2l, 2l+1
+    const int src = lane & ~1;
+    const float z0 = __shfl_sync(~0u, v[0], src), z1 = __shfl_sync(~0u, v[1], src);
+    const float m0 = __shfl_sync(~0u, v[0], src + 1), m1 = __shfl_sync(~0u, v[1], src + 1);
+    Zj = (lane & 1) ? z1 : z0;
+    Mj = (lane & 1) ? m1 : m0;
+  }
+}
+
+// Backward sums of one key (lane) over the item's query pairs in q' coordinates, mapped to the
+// d = q - k sums of MseSums (k_pair.cuh) at the end.
+__device__ __forceinline__ MseSums bwd_sums_x(const KeyX& K, const int npairs, const float4* pA, const float4* pB,
+                                              const float4* pC) {
+  float2 Sc = make_float2(0.f, 0.f), Stx = Sc, Sty = Sc, Stz = Sc, Su = Sc, Sux = Sc, Suy = Sc, Suz = Sc, Suq = Sc;
+  auto pair = [&](const int jp) {
+    const float4 QA = pA[jp], QB = pB[jp], QC = pC[jp];
+    FX_EF(K, QA, QB, e, f)
+    const float2 p = make_float2(ex2f(e.x), ex2f(e.y));
+    const float2 del = __fadd2_rn(f, make_float2(QC.z, QC.w));
+    const float2 t = __fmul2_rn(make_float2(QC.x, QC.y), p);
+    const float2 u = __fmul2_rn(t, del);
+    Sc = __fadd2_rn(Sc, t);
+    Stx = __ffma2_rn(t, make_float2(QA.x, QA.y), Stx);
+    Sty = __ffma2_rn(t, make_float2(QA.z, QA.w), Sty);
+    Stz = __ffma2_rn(t, make_float2(QB.x, QB.y), Stz);
+    Su = __fadd2_rn(Su, u);
+    Sux = __ffma2_rn(u, make_float2(QA.x, QA.y), Sux);
+    Suy = __ffma2_rn(u, make_float2(QA.z, QA.w), Suy);
+    Suz = __ffma2_rn(u, make_float2(QB.x, QB.y), Suz);
+    Suq = __ffma2_rn(u, make_float2(QB.z, QB.w), Suq);
+  };
+  // an even number of pairs (a padding slot is an idle query: qq = 1e30, rho = 0 -> exactly 0)
+  const int np2 = (npairs + 1) & ~1;
+#pragma unroll 2
+  for (int jp = 0; jp < np2; jp += 2) {
+    pair(jp);
+    pair(jp + 1);
+  }
+  const float sc = Sc.x + Sc.y, su = Su.x + Su.y;
+  const float sux = Sux.x + Sux.y, suy = Suy.x + Suy.y, suz = Suz.x + Suz.y;
+  MseSums s;
+  s.sc = sc;
+  s.sgx = fmaf(-K.kx, sc, Stx.x + Stx.y);
+  s.sgy = fmaf(-K.ky, sc, Sty.x + Sty.y);
+  s.sgz = fmaf(-K.kz, sc, Stz.x + Stz.y);
+  s.ss = fmaf(K.kk, su, fmaf(-2.0f * K.kx, sux, fmaf(-2.0f * K.ky, suy, fmaf(-2.0f * K.kz, suz, Suq.x + Suq.y))));
+  s.sdx = fmaf(-K.kx, su, sux);
+  s.sdy = fmaf(-K.ky, su, suy);
+  s.sdz = fmaf(-K.kz, su, suz);
+  return s;
+}
 
 __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* L) {
   const FwdArgs& A = F.f;
@@ -46,18 +213,18 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
     return;
   }
-  // 1. shift bounds, box, candidate ids
+  // 1. box, candidate ids
   const bool act = lane < nact;
   const int64_t js = (int64_t)it.x + lane;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-  float mh = INFINITY, f0 = 0.f;
-  float3 g0 = make_float3(0.f, 0.f, 0.f);
+  float mh = INFINITY;
   if (act) {
     q = A.qs[js];
-    shift_bound(kv, q, mh, f0, g0);
+    mh = A.qmh[js];  // shift bound from k_gather_queries_mh
   }
   Box box = warp_box(act, q.x, q.y, q.z, mh);
   box.thr += A.T_l;
+  const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
   __syncwarp();  // the previous item's readers of L and S are done
   uint32_t wn = 0;
   stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
@@ -66,42 +233,36 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     wn += __popc(bal);
   });
   // 2. forward
+  const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
+  const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;  // idle slot: weight 0 (finite: u qq = 0)
   {
-    const float mhs = act ? mh : -INFINITY;  // an idle slot has shift -inf (weight 0)
-    const float xo = __shfl_xor_sync(~0u, q.x, 1), yo = __shfl_xor_sync(~0u, q.y, 1);
-    const float zo = __shfl_xor_sync(~0u, q.z, 1), mo = __shfl_xor_sync(~0u, mhs, 1);
+    const float xo = __shfl_xor_sync(~0u, qx, 1), yo = __shfl_xor_sync(~0u, qy, 1);
+    const float zo = __shfl_xor_sync(~0u, qz, 1), qo = __shfl_xor_sync(~0u, qq, 1);
     if ((lane & 1) == 0) {
-      S.qa[lane >> 1] = make_float4(q.x, xo, q.y, yo);
-      S.qb[lane >> 1] = make_float4(q.z, zo, mhs, mo);
+      S.qa[lane >> 1] = make_float4(qx, xo, qy, yo);
+      S.qb[lane >> 1] = make_float4(qz, zo, qq, qo);
     }
   }
   __syncwarp();
   float Z, M;
-  if (FT_NPM == 16) {
-    if (nact <= 16) fwd_keys_sums<8>(kv, L, wn, nact, S.qa, S.qb, Z, M);
-    else fwd_keys_sums<16>(kv, L, wn, nact, S.qa, S.qb, Z, M);
-  } else {
-    float Z0, M0, Z1 = 0.f, M1 = 0.f;
-    fwd_keys_sums<8>(kv, L, wn, min(nact, 16), S.qa, S.qb, Z0, M0);
-    if (nact > 16) fwd_keys_sums<8>(kv, L, wn, nact - 16, S.qa + 8, S.qb + 8, Z1, M1);
-    Z = lane < 16 ? Z0 : Z1;
-    M = lane < 16 ? M0 : M1;
-  }
-  const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
-  if (__any_sync(~0u, bad)) {  // shift bound overflowed: the split kernels redo it exactly
+  if (nact <= 16) fwd_sums_x<8>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+  else fwd_sums_x<16>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+  const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
+  if (__any_sync(~0u, bad)) {  // Z underflow (far queries): the split kernels shift exactly
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
     return;
   }
-  float O = 0.f, nlam = -INFINITY, r = 0.f, lossj = 0.f;
+  float O = 0.f, rho = 0.f, lossj = 0.f;
   if (act) {
-    O = M * (1.0f / Z);
-    nlam = mh - log2f(Z);  // -lambda_j * log2(e):  p_ij = 2^(nlam - bl_i dd_ij)
+    const float iz = 1.0f / Z;
+    O = M * iz;
     const float diff = O - q.w;
-    r = 2.0f * diff * A.inv_J;
+    const float r = 2.0f * diff * A.inv_J;
+    rho = r * iz;  // t_ij = r_j p_ij = (r_j / Z_j) 2^(-a_ij log2 e)
     lossj = diff * diff * A.inv_J;
     if (A.O) A.O[A.perm[js]] = O;
   }
-  for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
+  for (int s = 16; s > 0; s >>= 1) lossj += __shfl_xor_sync(~0u, lossj, s);
   if (lane == 0) {
     A.loss_part[item] = lossj;
     atomicAdd(&A.ds->cand_pairs, (unsigned long long)wn * (unsigned long long)nact);
@@ -109,14 +270,8 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   // 3. backward over the same candidates
   {
     const float nO = -O;
-    const float xo = __shfl_xor_sync(~0u, q.x, 1), yo = __shfl_xor_sync(~0u, q.y, 1);
-    const float zo = __shfl_xor_sync(~0u, q.z, 1), wo = __shfl_xor_sync(~0u, nlam, 1);
-    const float ro = __shfl_xor_sync(~0u, r, 1), nOo = __shfl_xor_sync(~0u, nO, 1);
-    if ((lane & 1) == 0) {
-      S.pa[lane >> 1] = make_float4(q.x, xo, q.y, yo);
-      S.pb[lane >> 1] = make_float4(q.z, zo, nlam, wo);
-      S.pc[lane >> 1] = make_float4(r, ro, nO, nOo);
-    }
+    const float ro = __shfl_xor_sync(~0u, rho, 1), nOo = __shfl_xor_sync(~0u, nO, 1);
+    if ((lane & 1) == 0) S.pc[lane >> 1] = make_float4(rho, ro, nO, nOo);
   }
   __syncwarp();
   const int npairs = (nact + 1) >> 1;
@@ -136,7 +291,7 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
       b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
     }
     if (k < wn) {
-      const MseSums ms = bwd_mse_sums(a, b, npairs, S.pa, S.pb, S.pc);
+      const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
       bwd_mse_red(ms, a, b, (int)id, kv.n_nodes, F.gpad);
     }
   }

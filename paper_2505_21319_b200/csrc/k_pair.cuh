@@ -69,16 +69,15 @@ __device__ __forceinline__ void fwd_keys_sums(const KeysView& kv, const uint32_t
     const float2 c = make_float2(kb.x, kb.x), gx = make_float2(kb.y, kb.y), gy = make_float2(kb.z, kb.z),
                  gz = make_float2(kb.w, kb.w);
     // groups of 4 pairs without a branch inside, so the scheduler can interleave their chains;
-    // the last 1-3 pairs one by one (an odd query count pads one slot with shift -inf: weight 0)
+    // a last group of 1-2 pairs runs as 2, of 3 as 4: the padding slots hold idle queries (shift
+    // -inf: weight exactly 0), wasted FP32 work instead of a latency-bound serial tail
 #pragma unroll
     for (int pg = 0; pg < NPM; pg += 4) {
       const int rem = npairs - pg;
-      if (rem >= 4) {
+      if (rem >= 3) {
         FK_PAIR(pg) FK_PAIR(pg + 1) FK_PAIR(pg + 2) FK_PAIR(pg + 3)
       } else if (rem > 0) {
-        FK_PAIR(pg)
-        if (rem >= 2) FK_PAIR(pg + 1)
-        if (rem >= 3) FK_PAIR(pg + 2)
+        FK_PAIR(pg) FK_PAIR(pg + 1)
       }
     }
   };
@@ -148,8 +147,10 @@ __device__ __forceinline__ MseSums bwd_mse_sums(const float4 a, const float4 b, 
   const float2 c2 = make_float2(b.x, b.x), gx2 = make_float2(b.y, b.y), gy2 = make_float2(b.z, b.z),
                gz2 = make_float2(b.w, b.w);
   float2 Sc = make_float2(0.f, 0.f), Sgx = Sc, Sgy = Sc, Sgz = Sc, Ss = Sc, Sdx = Sc, Sdy = Sc, Sdz = Sc;
-#pragma unroll(kBwdUnroll)
-  for (int jp = 0; jp < npairs; ++jp) {
+  // an even number of pairs (the padding slot is an idle query: w = -inf, r = 0 -> exactly 0), two
+  // independent chains per iteration and no serial remainder
+  const int np2 = (npairs + 1) & ~1;
+  auto pair = [&](const int jp) {
     const float4 QA = pA[jp], QB = pB[jp], QC = pC[jp];
     const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), nx);
     const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), ny);
@@ -173,6 +174,11 @@ __device__ __forceinline__ MseSums bwd_mse_sums(const float4 a, const float4 b, 
     Sdx = __ffma2_rn(u, dx, Sdx);
     Sdy = __ffma2_rn(u, dy, Sdy);
     Sdz = __ffma2_rn(u, dz, Sdz);
+  };
+#pragma unroll(kBwdUnroll)
+  for (int jp = 0; jp < np2; jp += 2) {
+    pair(jp);
+    pair(jp + 1);
   }
   MseSums s;
   s.sc = Sc.x + Sc.y; s.sgx = Sgx.x + Sgx.y; s.sgy = Sgy.x + Sgy.y; s.sgz = Sgz.x + Sgz.y;

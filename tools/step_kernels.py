@@ -18,6 +18,7 @@ from workloads import synth  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--config", default="c2")
 p.add_argument("--steps", type=int, default=5)
+p.add_argument("--split", action="store_true", help="forward + backward instead of forward_backward")
 a = p.parse_args()
 J = (1 << 20) if a.config == "c2" else (1 << 22)
 loss = ef.LOSS_MSE if a.config == "c2" else ef.LOSS_MSE_EIKONAL
@@ -33,8 +34,11 @@ grad = torch.zeros(32 ** 3, 13, device="cuda")
 
 def step(i):
     grad.zero_()
-    m.forward(qd[i % 4], od[i % 4], loss=loss, want_O=False, want_loss=False)
-    m.backward(grad=grad)
+    if a.split:
+        m.forward(qd[i % 4], od[i % 4], loss=loss, want_O=False, want_loss=False)
+        m.backward(grad=grad)
+    else:
+        m.forward_backward(qd[i % 4], od[i % 4], loss=loss, grad=grad, want_loss=False)
     m.adamw_step(grad, hp)
 
 
