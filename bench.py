@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": label, "R": R, "points_per_step_per_gpu": J, "global_batch": J_global,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}",
                        "launch": "cuda-graph per step" if use_graph else "eager",
-                       "path": "split forward/backward" if args.split else "efunc_forward_backward (fused k_fit for MSE)",
+                       "path": "split forward/backward" if (args.split or loss_kind != "mse") else "efunc_forward_backward (fused k_fit for MSE)",
                        "l2": f"inputs larger than L2: pool of {pool} batches x {J * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
