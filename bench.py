@@ -30,7 +30,10 @@ CONFIGS = {
     "c2": (32, 1 << 20, "torus", "mse", "C2: 32^3x13 grid, torus SDF, 2^20 points/step/GPU, MSE"),
     "c3": (32, 1 << 22, "torus", "mse_eikonal", "C3: 32^3x13 grid, torus SDF, 2^22 points/step/GPU, MSE+0.1 Eikonal"),
     "c1": (8, 4096, "sphere", "mse", "C1: 8^3x13 grid, sphere SDF, 4096 points/step"),
+    "c5": (32, 1 << 20, "c5", "mse",
+           "C5: 8 independent 32^3x13 shapes per GPU (seeded rotated tori/spheres/boxes/CSG), 2^20 points/step per shape, MSE"),
 }
+C5_SHAPES_PER_GPU = 8
 SEED = 1234
 POOL = 8                       # distinct batches cycled through; 8 x 16.8 MB > 126 MB L2 at C2
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
@@ -134,7 +137,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from workloads import synth
-    shape = synth.make_shape(shape_name)
+    shape = synth.c5_shapes(1, SEED)[0] if shape_name == "c5" else synth.make_shape(shape_name)
     n = 48 if R >= 32 else 1024
     for w in range(args.warmup):
         oracle_step_time(R, shape, loss_kind, n, seed=SEED + w)
@@ -164,23 +167,37 @@ def run_ours(args, rank, world, local_rank):
     R, J, shape_name, loss_kind, label = CONFIGS[args.config]
     dev = local_rank
     torch.cuda.set_device(dev)
-    shape = synth.make_shape(shape_name)
     loss = ef.LOSS_MSE if loss_kind == "mse" else ef.LOSS_MSE_EIKONAL
-    J_global = edist.global_batch(J, world)
+    # C5: S independent shapes per GPU in one batched handle (replicas: no collective);
+    # otherwise one shape, data parallel over the ranks
+    S = C5_SHAPES_PER_GPU if shape_name == "c5" else 1
+    if S > 1:
+        shapes = synth.c5_shapes(S * world, SEED)[rank * S:(rank + 1) * S]
+        J_global = J  # every shape's loss is its own batch mean
+    else:
+        shapes = [synth.make_shape(shape_name)]
+        J_global = edist.global_batch(J, world)
+    shape = shapes[0]
 
     # model: paper init (s = 7, c ~ N(0, 0.1^2), g = 0) + mean-shift offsets on the GPU
-    th0 = synth.init_theta(R, SEED)
-    m = ef.EFunc(R, th0, device=dev)
-    surf = torch.as_tensor(synth.surface_points(shape, 16384, SEED)).cuda(dev)
-    m.mean_shift_init(surf)
+    th0 = np.stack([synth.init_theta(R, SEED + k) for k in range(S)]) if S > 1 else synth.init_theta(R, SEED)
+    m = ef.EFunc(R, th0, device=dev, n_shapes=S)
+    surf = np.stack([synth.surface_points(sh, 16384, SEED) for sh in shapes])
+    m.mean_shift_init(torch.as_tensor(surf if S > 1 else surf[0]).cuda(dev))
     hp = ef.AdamW()
 
-    # input pool (> L2 at C2); each rank draws its own points
-    pool = max(2, min(POOL, int(np.ceil(160e6 / (16 * J)))))
-    host = [synth.sample_batch(shape, J, seed=edist.rank_seed(SEED, rank, i)) for i in range(pool)]
+    # input pool (> L2); each rank draws its own points
+    pool = max(2, min(POOL, int(np.ceil(160e6 / (16 * J * S)))))
+
+    def draw(i):
+        bs = [synth.sample_batch(sh, J, seed=edist.rank_seed(SEED + 97 * k, rank, i)) for k, sh in enumerate(shapes)]
+        if S == 1:
+            return bs[0]
+        return np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs])
+    host = [draw(i) for i in range(pool)]
     qd = [torch.as_tensor(q).cuda(dev) for q, _ in host]
     od = [torch.as_tensor(o).cuda(dev) for _, o in host]
-    grad = torch.zeros(R ** 3, ef.NCH, dtype=torch.float32, device=f"cuda:{dev}")
+    grad = m._grad_zeros()
 
     # fused path (default): efunc_forward_backward runs the fused fit kernel k_fit for the MSE loss;
     # --split: efunc_forward + efunc_backward (k_item_lists, k_forward_keys, k_backward)
@@ -191,7 +208,7 @@ def run_ours(args, rank, world, local_rank):
             m.backward(grad=grad)
         else:
             m.forward_backward(qd[i], od[i], loss=loss, J_global=J_global, grad=grad, want_loss=False)
-        if world > 1:
+        if world > 1 and S == 1:
             edist.allreduce_grad(grad)
         m.adamw_step(grad, hp)
 
@@ -229,6 +246,7 @@ def run_ours(args, rank, world, local_rank):
     st = m.stats()
     m.set_counting(False)
     kept = st["kept_pairs"]; kept_off = st["kept_pairs_offset"]; cand = st["candidate_pairs"]
+    n_pts = J * S  # points per step per GPU
 
     for w in range(args.warmup):
         step(w % pool)
@@ -271,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.1)
     clk.stop()
     clocks = clk.summary()
-    value = J_global * args.steps / sec
+    value = (J_global if S == 1 else n_pts * world) * args.steps / sec
 
     # e2e: same steps through the public API with pinned host inputs, H2D + loss D2H inside
     e2e = None
@@ -294,9 +312,10 @@ def run_ours(args, rank, world, local_rank):
                 obuf.copy_(ho[i], non_blocking=True)
                 grad.zero_()
                 _, _, L = m.forward_backward(qbuf, obuf, loss=loss, J_global=J_global, grad=grad)
-                edist.allreduce_grad(grad)
+                if S == 1:
+                    edist.allreduce_grad(grad)
                 m.adamw_step(grad, hp)
-                return float(L.item())
+                return float(L.sum().item())
             for w in range(3):
                 estep(w % pool)
             dist.barrier()
@@ -307,8 +326,8 @@ def run_ours(args, rank, world, local_rank):
             tt = torch.tensor([esec], dtype=torch.float64, device=f"cuda:{dev}")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             esec = float(tt[0])
-        e2e = {"value": J_global * args.steps / esec, "unit": "points/s",
-               "h2d_bytes_per_step": int(J * 16), "d2h_bytes_per_step": 4}
+        e2e = {"value": (J_global if S == 1 else n_pts * world) * args.steps / esec, "unit": "points/s",
+               "h2d_bytes_per_step": int(n_pts * 16), "d2h_bytes_per_step": 4 * S}
 
     if rank != 0:
         return
@@ -339,17 +358,18 @@ def run_ours(args, rank, world, local_rank):
                                  "mean over the final steps of the timed region"),
             "share_of_step": bwd_ms * 1e-3 / (sec / args.steps),
             "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz max clock (guide unit counts)",
-            "kept_pairs_per_point": kept / J, "candidate_pairs_per_point": cand / J}
+            "kept_pairs_per_point": kept / n_pts, "candidate_pairs_per_point": cand / n_pts}
     if clocks.get("sm_mhz"):
         roof["frac_at_observed_clock"] = achieved / (SM_COUNT * FP32_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
     line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": label, "R": R, "points_per_step_per_gpu": J, "global_batch": J_global,
-                       "cutoff_T": 20.0, "parallelism": f"dp{world}",
+            "config": {"workload": label, "R": R, "points_per_step_per_gpu": n_pts,
+                       "global_batch": J_global if S == 1 else n_pts * world, "shapes_per_gpu": S,
+                       "cutoff_T": 20.0, "parallelism": f"dp{world}" if S == 1 else f"replicas{world}",
                        "launch": "cuda-graph per step" if use_graph else "eager",
                        "path": "split forward/backward" if (args.split or loss_kind != "mse") else "efunc_forward_backward (fused k_fit for MSE)",
-                       "l2": f"inputs larger than L2: pool of {pool} batches x {J * 16 / 1e6:.1f} MB cycled"},
+                       "l2": f"inputs larger than L2: pool of {pool} batches x {n_pts * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(R, shape, loss_kind)

@@ -78,7 +78,11 @@ typedef struct {
   int32_t fit_graph;      /* 1: efunc_fit_step replays a CUDA graph of its device work, captured on
                              the second call with the same J, pointers, loss and hyper-parameters
                              (any workspace reallocation drops it); 0: plain launches */
-  int32_t reserved[4];    /* must be 0 */
+  int32_t n_shapes;       /* 0 or 1: one grid. S > 1: S independent grids ("shapes", BASELINE config
+                             C5) in one handle; every per-shape array gains a leading [S] axis
+                             (theta/grad/m/v [S][R^3][13], q [S][J][3], o/O [S][J], G [S][J][3],
+                             loss_out [S], surf [S][N][3]) and J, N are per shape. */
+  int32_t reserved[3];    /* must be 0 */
 } efunc_config;
 
 typedef enum { EFUNC_LOSS_NONE = 0, EFUNC_LOSS_MSE = 1, EFUNC_LOSS_MSE_EIKONAL = 2 } efunc_loss_kind;

@@ -137,7 +137,7 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
   // per-brick candidate lists for the next forward/backward (query independent)
   h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
-                                    h->bl_off, h->bl_n, h->ds, s);
+                                    h->bl_off, h->bl_n, h->ds, h->scratch, s);
   h->launches += launch_list_snapshot(h->key_raw, h->key_ref, h->n_keys, h->ds, s);
   CK(cudaMemsetAsync(&h->ds->lists_invalid, 0, sizeof(uint32_t), s));
   CK(cudaGetLastError());
@@ -222,7 +222,7 @@ void free_all(efunc_t* h) {
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
-  dfree(h->fit_scratch);
+  dfree(h->scratch);
   drop_fit_graph(h);
   free_timing(h);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
@@ -402,10 +402,6 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   if (!q || !o) return fail(h, EFUNC_EINVAL, "q or o is NULL");
   if (J > (int64_t)0x7fffffff) return fail(h, EFUNC_EINVAL, "J > 2^31-1 per call");
   h->have_fwd = 0;
-  if (!h->fit_scratch) {
-    drop_fit_graph(h);
-    CK(dalloc(&h->fit_scratch, fit_scratch_entries()));
-  }
   FwdArgs a;
   RET(prep_queries(h, q, o, J, loss, a, s, 1));
   a.O = O;
@@ -413,7 +409,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   FitArgs f;
   f.f = a;
   f.gpad = h->gpad;
-  f.scratch = h->fit_scratch;
+  f.scratch = h->scratch;
   const int slot = timing_begin(h, s);
   h->launches += launch_fit(f, h->fwd_items_bound, s);
   timing_end(h, slot, s);
@@ -454,6 +450,17 @@ efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cuda
   return rebuild_keys(h, s);
 }
 
+// batched handles (n_shapes > 1): the k-th shape's slice of a per-shape array, and error relay
+template <class T>
+T* off(T* p, int64_t per_shape, size_t k) {
+  return p ? p + per_shape * (int64_t)k : nullptr;
+}
+
+efunc_status kid_ok(efunc_t* h, size_t k, efunc_status st) {
+  if (st != EFUNC_OK) h->err = "shape " + std::to_string(k) + ": " + h->kids[k]->err;
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -470,6 +477,28 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
   if (!cfg || !out) return fail(nullptr, EFUNC_EINVAL, "NULL argument");
   *out = nullptr;
   if (cfg->R < 2 || cfg->R > 256) return fail(nullptr, EFUNC_EINVAL, "R must be in [2, 256]");
+  if (cfg->n_shapes < 0 || cfg->n_shapes > 4096) return fail(nullptr, EFUNC_EINVAL, "n_shapes must be in [0, 4096]");
+  if (cfg->n_shapes > 1) {  // C5: one single-shape handle per shape behind this one
+    efunc_t* p = new (std::nothrow) efunc();
+    if (!p) return fail(nullptr, EFUNC_ENOMEM, "host allocation failed");
+    p->cfg = *cfg;
+    p->R = cfg->R;
+    p->n_nodes = cfg->R * cfg->R * cfg->R;
+    efunc_config c1 = *cfg;
+    c1.n_shapes = 1;
+    for (int k = 0; k < cfg->n_shapes; ++k) {
+      efunc_t* kid = nullptr;
+      const efunc_status st = efunc_create(&c1, off(theta_host, p->n_nodes * (int64_t)EF_NCH, k), &kid);
+      if (st != EFUNC_OK) {
+        for (efunc_t* q : p->kids) efunc_destroy(q);
+        delete p;
+        return st;
+      }
+      p->kids.push_back(kid);
+    }
+    *out = p;
+    return EFUNC_OK;
+  }
   if (cfg->degree != 1) return fail(nullptr, EFUNC_EINVAL, "only degree 1 is implemented");
   if (cfg->variant != EFUNC_VARIANT_COMBINED) return fail(nullptr, EFUNC_EINVAL, "only the COMBINED variant");
   int ndev = 0;
@@ -502,6 +531,7 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->cell_start, h->n_cells + 1));
     CK(dalloc(&h->cell_fill, h->n_cells + 1));
     CK(dalloc(&h->ds, 1));
+    CK(dalloc(&h->scratch, (size_t)SCRATCH_WARPS * SCRATCH_STRIDE));
     h->bg = brick_geom(h->cfg, h->NC, h->h);
     const size_t nbins = (size_t)h->bg.n_codes * QSUB + 1;
     CK(dalloc(&h->bl_off, h->bg.n_codes));
@@ -544,6 +574,11 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
 }
 
 efunc_status efunc_destroy(efunc_t* h) {
+  if (h && !h->kids.empty()) {
+    for (efunc_t* k : h->kids) efunc_destroy(k);
+    delete h;
+    return EFUNC_OK;
+  }
   if (!h) return EFUNC_OK;
   {
     DeviceGuard dg(h->cfg.device);
@@ -556,12 +591,27 @@ efunc_status efunc_destroy(efunc_t* h) {
 
 efunc_status efunc_forward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
                            float* O, float* G, float* loss_out, void* stream) {
+  if (h && !h->kids.empty()) {
+    const size_t S = h->kids.size();
+    for (size_t k = 0; k < S; ++k)
+      RET(kid_ok(h, k, efunc_forward(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, off(O, J, k),
+                                     off(G, 3 * J, k), off(loss_out, 1, k), stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_forward(h, q, o, J, loss, O, G, loss_out, 1, (cudaStream_t)stream);
 }
 
 efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k) {
+      const int64_t J = h->kids[k]->fwd_J;
+      RET(kid_ok(h, k, efunc_backward(h->kids[k], off(dL_dO, J, k), off(dL_dG, 3 * J, k),
+                                      off(grad, h->kids[k]->n_nodes * (int64_t)EF_NCH, k), stream)));
+    }
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_backward(h, dL_dO, dL_dG, grad, (cudaStream_t)stream);
@@ -569,18 +619,35 @@ efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, 
 
 efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
                                     float* O, float* grad, float* loss_out, void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_forward_backward(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, off(O, J, k),
+                                              off(grad, h->n_nodes * (int64_t)EF_NCH, k), off(loss_out, 1, k),
+                                              stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_forward_backward(h, q, o, J, loss, O, grad, loss_out, (cudaStream_t)stream);
 }
 
 efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_adamw_step(h->kids[k], off(grad, h->n_nodes * (int64_t)EF_NCH, k), hp, stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_adamw(h, grad, hp, (cudaStream_t)stream);
 }
 
 efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, float* O, float* G, void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_eval_grad(h->kids[k], off(q, 3 * J, k), J, off(O, J, k), off(G, 3 * J, k), stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_forward(h, q, nullptr, J, nullptr, O, G, nullptr, 0, (cudaStream_t)stream);
@@ -589,6 +656,13 @@ efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, float* O, fl
 efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
                             const efunc_adamw* hp, float* grad_ws, float* loss_out, int32_t host_io,
                             void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_fit_step(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, hp,
+                                      off(grad_ws, h->n_nodes * (int64_t)EF_NCH, k), off(loss_out, 1, k), host_io,
+                                      stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "fit_step needs a loss");
   if (!hp) return fail(h, EFUNC_EINVAL, "NULL AdamW parameters");
@@ -664,6 +738,11 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
 }
 
 efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, float bandwidth, void* stream) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_mean_shift_init(h->kids[k], off(surf, 3 * N, k), N, bandwidth, stream)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (!surf || N < 1) return fail(h, EFUNC_EINVAL, "mean shift needs N >= 1 surface points");
   if (!(bandwidth > 0.0f)) return fail(h, EFUNC_EINVAL, "bandwidth must be > 0");
@@ -675,6 +754,11 @@ efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, flo
 }
 
 efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream) {
+  if (h && !h->kids.empty() && dst) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_get_params(h->kids[k], off(dst, h->n_nodes * (int64_t)EF_NCH, k), on_device, stream)));
+    return EFUNC_OK;
+  }
   if (!h || !dst) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -685,6 +769,11 @@ efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* s
 }
 
 efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, void* stream) {
+  if (h && !h->kids.empty() && src) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_set_params(h->kids[k], off(src, h->n_nodes * (int64_t)EF_NCH, k), on_device, stream)));
+    return EFUNC_OK;
+  }
   if (!h || !src) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -696,6 +785,12 @@ efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, v
 }
 
 efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int64_t* step) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_get_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)EF_NCH, k),
+                                            off(v_host, h->n_nodes * (int64_t)EF_NCH, k), k == 0 ? step : nullptr)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
@@ -711,6 +806,12 @@ efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int6
 }
 
 efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* v_host, int64_t step) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k)
+      RET(kid_ok(h, k, efunc_set_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)EF_NCH, k),
+                                            off(v_host, h->n_nodes * (int64_t)EF_NCH, k), step)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (step < 0) return fail(h, EFUNC_EINVAL, "step < 0");
   DeviceGuard dg(h->cfg.device);
@@ -726,12 +827,20 @@ efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* 
 }
 
 efunc_status efunc_set_counting(efunc_t* h, int32_t on) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k) RET(kid_ok(h, k, efunc_set_counting(h->kids[k], on)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   h->count_kept = on ? 1 : 0;
   return EFUNC_OK;
 }
 
 efunc_status efunc_set_timing(efunc_t* h, int32_t slots) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k) RET(kid_ok(h, k, efunc_set_timing(h->kids[k], slots)));
+    return EFUNC_OK;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (slots < 0 || slots > 4096) return fail(h, EFUNC_EINVAL, "slots must be in [0, 4096]");
   DeviceGuard dg(h->cfg.device);
@@ -747,6 +856,15 @@ efunc_status efunc_set_timing(efunc_t* h, int32_t slots) {
 }
 
 efunc_status efunc_get_kernel_ms(efunc_t* h, float* ms_host, int32_t n) {
+  if (h && !h->kids.empty() && ms_host && n > 0) {  // per slot: the sum over shapes
+    std::vector<float> t(n);
+    for (int i = 0; i < n; ++i) ms_host[i] = 0.0f;
+    for (size_t k = 0; k < h->kids.size(); ++k) {
+      RET(kid_ok(h, k, efunc_get_kernel_ms(h->kids[k], t.data(), n)));
+      for (int i = 0; i < n; ++i) ms_host[i] += t[i];
+    }
+    return EFUNC_OK;
+  }
   if (!h || !ms_host) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   const int slots = (int)(h->tev.size() / 2);
@@ -761,6 +879,21 @@ efunc_status efunc_get_kernel_ms(efunc_t* h, float* ms_host, int32_t n) {
 }
 
 efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
+  if (h && !h->kids.empty() && out) {  // counters summed over shapes, beta_min the minimum
+    efunc_stats acc{};
+    acc.beta_min = INFINITY;
+    for (size_t k = 0; k < h->kids.size(); ++k) {
+      efunc_stats t{};
+      RET(kid_ok(h, k, efunc_get_stats(h->kids[k], &t, stream)));
+      acc.J += t.J; acc.items += t.items; acc.candidate_pairs += t.candidate_pairs; acc.kept_pairs += t.kept_pairs;
+      acc.beta_min = fminf(acc.beta_min, t.beta_min); acc.nonfinite |= t.nonfinite;
+      acc.overflow_items += t.overflow_items; acc.kept_pairs_offset += t.kept_pairs_offset;
+      acc.launches += t.launches; acc.list_builds += t.list_builds; acc.list_entries += t.list_entries;
+      acc.list_overflow += t.list_overflow;
+    }
+    *out = acc;
+    return EFUNC_OK;
+  }
   if (!h || !out) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -784,6 +917,14 @@ efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
 }
 
 efunc_status efunc_check(efunc_t* h, void* stream) {
+  if (h && !h->kids.empty()) {
+    efunc_status first = EFUNC_OK;
+    for (size_t k = 0; k < h->kids.size(); ++k) {
+      const efunc_status st = kid_ok(h, k, efunc_check(h->kids[k], stream));
+      if (st != EFUNC_OK && first == EFUNC_OK) first = st;
+    }
+    return first;
+  }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   CK(cudaStreamSynchronize((cudaStream_t)stream));

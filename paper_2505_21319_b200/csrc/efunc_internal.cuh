@@ -31,9 +31,13 @@ namespace ef {
 constexpr int QW = 32;              // queries per work item (one warp; the forward supports 64)
 constexpr int NTHREADS = 32;        // one warp per CTA: items retire independently
 constexpr int NWARP = NTHREADS / 32;
-constexpr int BL_CAP = 4096;        // max staged list length per brick (longer: fallback)
+constexpr int BL_CAP = 16384;       // max list length per brick (longer: enumerate fallback)
 constexpr uint32_t BL_OVERFLOW = 0xffffffffu;
 constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
+// per-warp id scratch of the persistent list builders (k_fit, k_brick_lists): SCRATCH_WARPS slots
+// of BL_CAP ids, padded so the slots do not alias in L1
+constexpr int SCRATCH_WARPS = 148 * 16;
+constexpr size_t SCRATCH_STRIDE = BL_CAP + 32;
 constexpr uint32_t QSUB = 8;        // query bins per brick (octants)
 constexpr int WL_PER_QUERY = 64;    // forward->backward candidate pool capacity per query
 constexpr float SKIN_H = 0.25f;     // Verlet skin of the brick lists, in lattice spacings
@@ -147,7 +151,7 @@ struct BwdArgs {
 struct FitArgs {
   FwdArgs f;
   float* gpad;            // [R^3][16] padded gradient accumulator
-  uint32_t* scratch;      // per-warp candidate-id scratch, fit_scratch_entries() ids
+  uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
 };
 
 constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
@@ -172,7 +176,7 @@ int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_st
 int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted,
                        int* kid, uint32_t n, cudaStream_t s);
 int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool,
-                       uint32_t pool_cap, uint32_t* off, uint32_t* n, DevScalars* ds,
+                       uint32_t pool_cap, uint32_t* off, uint32_t* n, DevScalars* ds, uint32_t* scratch,
                        cudaStream_t s);
 int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom& bg, int NC,
                       float inv_h, uint32_t* bins, uint32_t* count, DevScalars* ds,
@@ -188,7 +192,6 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 int launch_forward_slow(const FwdArgs& a, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
-size_t fit_scratch_entries();
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
 int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);
@@ -262,7 +265,7 @@ struct efunc {
   uint32_t* wl_off = nullptr;       // [items bound]
   uint32_t* wl_n = nullptr;         // [items bound]
   uint32_t* slow_items = nullptr;   // [items bound]
-  uint32_t* fit_scratch = nullptr;  // fused fit kernel: per-warp candidate ids
+  uint32_t* scratch = nullptr;      // per-warp id scratch (k_fit, k_brick_lists): SCRATCH_WARPS x SCRATCH_STRIDE
   int64_t fwd_items_bound = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step
   float* io_o = nullptr;
@@ -290,6 +293,7 @@ struct efunc {
   int64_t fit_launches = 0;          // kernels inside the captured graph
   cudaStream_t cap_stream = nullptr;
   // kernel timing (efunc_set_timing): event pairs, slot = call index mod slots
+  std::vector<efunc*> kids;          // n_shapes > 1: one single-shape handle per shape
   std::vector<cudaEvent_t> tev;
   std::vector<int> tev_used;
   int64_t tseq = 0;

@@ -35,6 +35,7 @@ namespace ef {
 #endif
 constexpr int FT_WARPS = 4;
 constexpr int FT_BLOCKS = 148 * (FT_MIN_WARPS / FT_WARPS);
+static_assert(FT_BLOCKS * FT_WARPS <= SCRATCH_WARPS, "one scratch slot per warp");
 constexpr float FT_ZMIN = 7.8886e-31f;  // 2^-100: smaller Z_j -> exact-shift split path
 
 struct FitSmem {
@@ -300,15 +301,13 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
 __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(const FitArgs F) {
   __shared__ FitSmem smem[FT_WARPS];
   const int w = threadIdx.x >> 5;
-  uint32_t* L = F.scratch + (size_t)(blockIdx.x * FT_WARPS + w) * BL_CAP;
+  uint32_t* L = F.scratch + (size_t)(blockIdx.x * FT_WARPS + w) * SCRATCH_STRIDE;
   for (;;) {
     const int64_t item = fetch_item(&F.f.ds->fit_next, F.f.n_items, nullptr, nullptr);
     if (item < 0) break;
     fit_item(F, (uint32_t)item, smem[w], L);
   }
 }
-
-size_t fit_scratch_entries() { return (size_t)FT_BLOCKS * FT_WARPS * BL_CAP; }
 
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;

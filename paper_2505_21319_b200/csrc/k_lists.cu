@@ -12,10 +12,12 @@ constexpr int KB_WARPS = 2;
 __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv, const BrickGeom bg, float T_l,
                                                           uint32_t* __restrict__ pool, uint32_t pool_cap,
                                                           uint32_t* __restrict__ off, uint32_t* __restrict__ nout,
-                                                          DevScalars* ds) {
-  __shared__ uint32_t st[KB_WARPS][BL_CAP];
+                                                          DevScalars* ds, uint32_t* __restrict__ scratch) {
   __shared__ uint8_t own[KB_WARPS][OWN_CAP];
   __shared__ uint32_t rs[KB_WARPS][32], ro[KB_WARPS][32];
+  // the warp's staging area: a slot of the handle's per-warp scratch (shared with k_fit, which
+  // never runs concurrently), BL_CAP ids, L2-resident
+  uint32_t* const stw = scratch + (size_t)(blockIdx.x * KB_WARPS + (threadIdx.x >> 5)) * SCRATCH_STRIDE;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (!ds->lists_invalid) return;  // the lists of an earlier step are still valid (Verlet skin)
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ds->list_builds, 1u);
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv
     const uint32_t bal = __ballot_sync(~0u, pass);
     if (pass) {
       const uint32_t slot = cnt + __popc(bal & lanemask_lt());
-      if (slot < (uint32_t)BL_CAP) st[w][slot] = (uint32_t)__ldg(&kv.kid[kp]);  // key id
+      if (slot < (uint32_t)BL_CAP) stw[slot] = (uint32_t)__ldg(&kv.kid[kp]);  // key id
     }
     cnt += __popc(bal);
   });
@@ -70,7 +72,7 @@ __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv
     continue;
   }
   __syncwarp();
-  for (uint32_t i = lane; i < cnt; i += 32) pool[base + i] = st[w][i];
+  for (uint32_t i = lane; i < cnt; i += 32) pool[base + i] = stw[i];
   if (lane == 0) {
     off[code] = base;
     nout[code] = cnt;
@@ -80,10 +82,11 @@ __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv
 }
 
 int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool, uint32_t pool_cap,
-                       uint32_t* off, uint32_t* n, DevScalars* ds, cudaStream_t s) {
+                       uint32_t* off, uint32_t* n, DevScalars* ds, uint32_t* scratch, cudaStream_t s) {
   uint32_t blocks = (bg.n_codes + KB_WARPS - 1) / KB_WARPS;
-  if (blocks > 148u * 16u) blocks = 148u * 16u;
-  k_brick_lists<<<blocks, 32 * KB_WARPS, 0, s>>>(kv, bg, T_l, pool, pool_cap, off, n, ds);
+  const uint32_t cap = (uint32_t)(SCRATCH_WARPS / KB_WARPS);  // one scratch slot per warp
+  if (blocks > cap) blocks = cap;
+  k_brick_lists<<<blocks, 32 * KB_WARPS, 0, s>>>(kv, bg, T_l, pool, pool_cap, off, n, ds, scratch);
   return 1;
 }
 

@@ -32,7 +32,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
 class Config(C.Structure):
     _fields_ = [("R", C.c_int32), ("degree", C.c_int32), ("variant", C.c_int32), ("cutoff_T", C.c_float),
                 ("deterministic", C.c_int32), ("device", C.c_int32), ("sync_checks", C.c_int32),
-                ("fit_graph", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("fit_graph", C.c_int32), ("n_shapes", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class Loss(C.Structure):
@@ -135,21 +135,25 @@ class EFunc:
     """One efunc grid (O^{+Delta}, degree 1, R^3 x 13) on one CUDA device."""
 
     def __init__(self, R: int, theta=None, cutoff_T: float = 20.0, device: int = 0,
-                 deterministic: bool = False, sync_checks: bool = False, fit_graph: bool = True):
+                 deterministic: bool = False, sync_checks: bool = False, fit_graph: bool = True,
+                 n_shapes: int = 1):
+        """n_shapes > 1: S independent grids in one handle (BASELINE config C5); theta, grads and
+        the per-query arrays then carry a leading [S] axis and J counts queries per shape."""
         import torch
         self.lib = load_library()
         self.R = int(R)
+        self.S = max(1, int(n_shapes))
         self.device = int(device)
-        self.n_params = self.R ** 3 * NCH
+        self.n_params = self.S * self.R ** 3 * NCH
         cfg = Config(self.R, 1, 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks),
-                     int(fit_graph))
+                     int(fit_graph), self.S)
         th = None
         if theta is not None:
             if isinstance(theta, torch.Tensor):
                 theta = theta.detach().cpu().numpy()
             th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
             if th.size != self.n_params:
-                raise ValueError("theta must have R^3*13 elements")
+                raise ValueError("theta must have n_shapes*R^3*13 elements")
         h = C.c_void_p()
         st = self.lib.efunc_create(C.byref(cfg), None if th is None else th.ctypes.data, C.byref(h))
         if st != OK:
@@ -177,15 +181,28 @@ class EFunc:
             pass
 
     def _empty(self, *shape):
+        if self.S > 1:
+            shape = (self.S,) + shape
         return self._torch.empty(*shape, dtype=self._torch.float32, device=f"cuda:{self.device}")
+
+    def _grad_zeros(self):
+        shape = (self.R ** 3, NCH) if self.S == 1 else (self.S, self.R ** 3, NCH)
+        return self._torch.zeros(*shape, dtype=self._torch.float32, device=f"cuda:{self.device}")
+
+    def _J(self, q):
+        """queries per shape"""
+        return q.numel() // (3 * self.S)
+
+    def _pshape(self):
+        return (self.R ** 3, NCH) if self.S == 1 else (self.S, self.R ** 3, NCH)
 
     # ---------------------------------------------------------------- API
     def forward(self, q, o=None, loss: int = LOSS_NONE, eikonal_lambda: float = 0.1, J_global: int = 0,
                 want_O: bool = True, want_G: bool = False, want_loss: bool = True):
         """Returns (O, G, loss) — tensors or None."""
-        J = q.shape[0] if q.dim() == 2 else q.numel() // 3
-        _check_dev(q, "q", 3 * J, self.device)
-        _check_dev(o, "o", J, self.device)
+        J = self._J(q)
+        _check_dev(q, "q", 3 * J * self.S, self.device)
+        _check_dev(o, "o", J * self.S, self.device)
         O = self._empty(J) if want_O else None
         G = self._empty(J, 3) if want_G else None
         L = self._empty(1) if (want_loss and loss != LOSS_NONE) else None
@@ -196,7 +213,7 @@ class EFunc:
 
     def backward(self, dL_dO=None, dL_dG=None, grad=None):
         if grad is None:
-            grad = self._torch.zeros(self.R ** 3, NCH, dtype=self._torch.float32, device=f"cuda:{self.device}")
+            grad = self._grad_zeros()
         _check_dev(grad, "grad", self.n_params, self.device)
         _check_dev(dL_dO, "dL_dO", None, self.device)
         _check_dev(dL_dG, "dL_dG", None, self.device)
@@ -207,11 +224,11 @@ class EFunc:
                          grad=None, want_O: bool = False, want_loss: bool = True):
         """forward + fused loss upstream + backward in one call (the fused fit kernel for MSE).
         Returns (grad, O, loss); grad is accumulated into (+=) when given."""
-        J = q.shape[0] if q.dim() == 2 else q.numel() // 3
-        _check_dev(q, "q", 3 * J, self.device)
-        _check_dev(o, "o", J, self.device)
+        J = self._J(q)
+        _check_dev(q, "q", 3 * J * self.S, self.device)
+        _check_dev(o, "o", J * self.S, self.device)
         if grad is None:
-            grad = self._torch.zeros(self.R ** 3, NCH, dtype=self._torch.float32, device=f"cuda:{self.device}")
+            grad = self._grad_zeros()
         _check_dev(grad, "grad", self.n_params, self.device)
         O = self._empty(J) if want_O else None
         L = self._empty(1) if want_loss else None
@@ -227,8 +244,8 @@ class EFunc:
         self._ok(self.lib.efunc_adamw_step(self.h, _ptr(grad), C.byref(p), self._stream()))
 
     def eval_grad(self, q, want_O=True, want_G=True):
-        J = q.numel() // 3
-        _check_dev(q, "q", 3 * J, self.device)
+        J = self._J(q)
+        _check_dev(q, "q", 3 * J * self.S, self.device)
         O = self._empty(J) if want_O else None
         G = self._empty(J, 3) if want_G else None
         self._ok(self.lib.efunc_eval_grad(self.h, _ptr(q), J, _ptr(O), _ptr(G), self._stream()))
@@ -239,37 +256,37 @@ class EFunc:
         """forward + loss + backward + AdamW. q/o either CUDA tensors (async, loss_out a device
         tensor) or pinned CPU tensors (host_io: copies inside the call; returns the loss float)."""
         hp = hp or AdamW()
-        J = q.numel() // 3
+        J = self._J(q)
         lc = Loss(loss, eikonal_lambda, J_global)
         p = hp.c()
         host = q.device.type == "cpu"
         if host:
-            lo = C.c_float(0.0)
+            lo = (C.c_float * self.S)()
             self._ok(self.lib.efunc_fit_step(self.h, q.data_ptr(), o.data_ptr(), J, C.byref(lc), C.byref(p),
                                              _ptr(grad_ws), C.addressof(lo), 1, self._stream()))
-            return float(lo.value)
+            return float(lo[0]) if self.S == 1 else [float(x) for x in lo]
         self._ok(self.lib.efunc_fit_step(self.h, _ptr(q), _ptr(o), J, C.byref(lc), C.byref(p), _ptr(grad_ws),
                                          _ptr(loss_out), 0, self._stream()))
         return loss_out
 
     def mean_shift_init(self, surf, bandwidth: float = 100.0):
-        N = surf.numel() // 3
-        _check_dev(surf, "surf", 3 * N, self.device)
+        N = surf.numel() // (3 * self.S)
+        _check_dev(surf, "surf", 3 * N * self.S, self.device)
         self._ok(self.lib.efunc_mean_shift_init(self.h, _ptr(surf), N, float(bandwidth), self._stream()))
 
     def get_params(self) -> np.ndarray:
-        out = np.empty((self.R ** 3, NCH), dtype=np.float32)
+        out = np.empty(self._pshape(), dtype=np.float32)
         self._ok(self.lib.efunc_get_params(self.h, out.ctypes.data, 0, self._stream()))
         return out
 
     def set_params(self, theta):
         th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
         if th.size != self.n_params:
-            raise ValueError("theta must have R^3*13 elements")
+            raise ValueError("theta must have n_shapes*R^3*13 elements")
         self._ok(self.lib.efunc_set_params(self.h, th.ctypes.data, 0, self._stream()))
 
     def get_adam_state(self):
-        m = np.empty((self.R ** 3, NCH), np.float32)
+        m = np.empty(self._pshape(), np.float32)
         v = np.empty_like(m)
         step = C.c_int64(0)
         self._ok(self.lib.efunc_get_adam_state(self.h, m.ctypes.data, v.ctypes.data, C.byref(step)))

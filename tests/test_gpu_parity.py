@@ -490,3 +490,31 @@ def test_forward_backward_r16_parity():
     Lref, r = orc.mse_loss(f.O, o)
     assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
     check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r))
+
+
+# ----------------------------------------------------------------------------- batched shapes (C5)
+def test_batched_shapes_match_single_handles_and_oracle():
+    """n_shapes = 3 in one handle (config C5's layout: [S][...] arrays) against three single
+    handles on the same data, and shape 1 against the oracle."""
+    R, J, S = 8, 1500, 3
+    shapes = synth.c5_shapes(S, 7)
+    ths = np.stack([synth.fitted_like_theta(R, sh, 10 + k) for k, sh in enumerate(shapes)])
+    bs = [synth.sample_batch(sh, J, seed=20 + k) for k, sh in enumerate(shapes)]
+    q = np.stack([b[0] for b in bs]); o = np.stack([b[1] for b in bs])
+    mb = ef.EFunc(R, ths, n_shapes=S)
+    gb, Ob, Lb = mb.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True)
+    assert tuple(gb.shape) == (S, R ** 3, 13) and tuple(Ob.shape) == (S, J) and tuple(Lb.shape) == (S, 1)
+    gb = gb.cpu().numpy(); Ob = Ob.cpu().numpy()
+    for k in range(S):
+        m1 = ef.EFunc(R, ths[k])
+        g1, O1, L1 = m1.forward_backward(dev(q[k]), dev(o[k]), loss=ef.LOSS_MSE, want_O=True)
+        assert np.array_equal(O1.cpu().numpy(), Ob[k])
+        assert np.abs(g1.cpu().numpy() - gb[k]).max() <= 1e-6 * np.abs(gb[k]).max()
+    f = orc.forward(ths[1], R, q[1])
+    _, r = orc.mse_loss(f.O, o[1])
+    assert nw(Ob[1], f.O) <= TOL_VAL
+    check_grads(gb[1], orc.backward(ths[1], R, q[1], f, r))
+    # AdamW and parameter access follow the same layout
+    mb.adamw_step(torch.as_tensor(gb).cuda())
+    th_after = mb.get_params()
+    assert th_after.shape == (S, R ** 3, 13) and not np.array_equal(th_after, ths)

@@ -107,6 +107,32 @@ class Box(Shape):
         d = np.abs(np.asarray(p, np.float64)) - self.b
         return np.linalg.norm(np.maximum(d, 0), axis=1) + np.minimum(np.max(d, axis=1), 0)
 
+    def sample_surface(self, n, g):
+        return _box_surface(self.b, n, g)
+
+
+class Rotated(Shape):
+    """A base shape turned by the rotation M (world = M @ local)."""
+
+    def __init__(self, base: Shape, M: np.ndarray):
+        self.base = base; self.M = np.asarray(M, np.float64); self.name = "rot_" + base.name
+
+    def sdf(self, p):
+        return self.base.sdf(np.asarray(p, np.float64) @ self.M)
+
+    def sample_surface(self, n, g):
+        return self.base.sample_surface(n, g) @ self.M.T
+
+
+def _box_surface(b: np.ndarray, n: int, g: np.random.Generator) -> np.ndarray:
+    """uniform samples on the surface of the box [-b, b]"""
+    areas = np.array([b[1] * b[2], b[0] * b[2], b[0] * b[1]] * 2)
+    face = g.choice(6, size=n, p=areas / areas.sum())
+    p = g.uniform(-1, 1, size=(n, 3)) * b
+    ax = face % 3
+    p[np.arange(n), ax] = np.where(face < 3, 1.0, -1.0) * b[ax]
+    return p
+
 
 class CSG(Shape):
     """min(torus, max(box(0.35), -sphere(0.45)))."""
@@ -118,12 +144,51 @@ class CSG(Shape):
     def sdf(self, p):
         return np.minimum(self.t.sdf(p), np.maximum(self.b.sdf(p), -self.s.sdf(p)))
 
+    def sample_surface(self, n, g):
+        """boundary pieces of the three primitives (torus, box, sphere surfaces weighted by area)
+        kept where they lie on the CSG surface"""
+        areas = np.array([4 * np.pi ** 2 * self.t.R0 * self.t.r0, 24 * 0.35 ** 2, 4 * np.pi * 0.45 ** 2])
+        out, have = [], 0
+        while have < n:
+            m = max(2 * n, 4096)
+            k = g.multinomial(m, areas / areas.sum())
+            c = np.concatenate([self.t.sample_surface(k[0], g), self.b.sample_surface(k[1], g),
+                                self.s.sample_surface(k[2], g)])
+            c = c[np.abs(self.sdf(c)) < 1e-9]
+            out.append(c); have += len(c)
+        p = np.concatenate(out)
+        return p[g.permutation(len(p))[:n]]
+
 
 SHAPES = {"sphere": Sphere, "torus": Torus, "box": Box, "csg": CSG}
 
 
 def make_shape(name: str) -> Shape:
     return SHAPES[name]()
+
+
+def c5_shapes(n: int, seed: int) -> list:
+    """BASELINE config C5: n seeded shapes cycling torus / sphere / box / CSG, size parameter
+    U[0.2, 0.6], each under a random rotation (QR of a Gaussian matrix)."""
+    g = rng(seed, 55)
+    out = []
+    for i in range(n):
+        r = g.uniform(0.2, 0.6)
+        kind = i % 4
+        if kind == 0:
+            base = Torus(R0=r, r0=min(0.25, 0.4 * r))
+        elif kind == 1:
+            base = Sphere(r)
+        elif kind == 2:
+            base = Box(r / np.sqrt(2.0))
+        else:
+            base = CSG()
+        Q, Rr = np.linalg.qr(g.normal(size=(3, 3)))
+        Q = Q * np.sign(np.diag(Rr))
+        if np.linalg.det(Q) < 0:
+            Q[:, 0] = -Q[:, 0]
+        out.append(Rotated(base, Q))
+    return out
 
 
 # ----------------------------------------------------------------------------- batches
