@@ -175,11 +175,21 @@ EFUNC_API efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, fl
 /* efunc_fit_step — forward + loss + backward + AdamW in one call on one device.
  *   host_io == 1: q, o are HOST buffers (pinned for async copies), loss_out is a host float*;
  *                 the call copies q/o in on `stream`, reads the loss back and synchronises.
+ *   host_io == 2: pipelined host I/O: q, o pinned HOST buffers, loss_out a host float*. The
+ *                 call copies q/o into one of two device staging slots on the handle's copy
+ *                 stream, runs the step on `stream` after the copy, reads the loss back into
+ *                 pinned memory, and returns without waiting (it blocks only until the step
+ *                 two calls back is done, then stores that step's loss to its *loss_out).
+ *                 So the copy of step k+1 overlaps the compute of step k. q, o and *loss_out
+ *                 must stay valid until efunc_sync() (or two calls later).
  *   host_io == 0: all pointers are device pointers; no synchronisation.
  * grad_ws: dev float[R^3*13] scratch for the gradient (zeroed by the call). */
 EFUNC_API efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t J,
                             const efunc_loss* loss, const efunc_adamw* hp, float* grad_ws,
                             float* loss_out, int32_t host_io, void* stream);
+
+/* efunc_sync — waits for every step issued with host_io == 2 (their losses are then stored). */
+EFUNC_API efunc_status efunc_sync(efunc_t* h);
 
 /* efunc_mean_shift_init — Delta_n = sum_s e^{-bw||k_n - s||^2} s / sum_s e^{-bw||k_n-s||^2} - k_n
  * (bw = 100, N = 16384 in the paper) written into channels 5..7.

@@ -103,9 +103,11 @@ KeysView keys_view(efunc_t* h) {
 }
 
 void drop_fit_graph(efunc_t* h) {
-  if (h->fit_exec) cudaGraphExecDestroy(h->fit_exec);
-  h->fit_exec = nullptr;
-  h->fit_seen = 0;
+  for (int k = 0; k < 2; ++k) {
+    if (h->fit_exec[k]) cudaGraphExecDestroy(h->fit_exec[k]);
+    h->fit_exec[k] = nullptr;
+    h->fit_seen[k] = 0;
+  }
 }
 
 efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
@@ -146,7 +148,7 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
 }
 
 efunc_status ensure_queries(efunc_t* h, int64_t J) {
-  const int64_t bound = (J + QW - 1) / QW + h->bg.n_codes + 1;
+  const int64_t bound = (J + IQ - 1) / IQ + h->bg.n_codes + 1;
   if (bound > h->items_cap || J > h->J_cap) drop_fit_graph(h);
   if (bound > h->items_cap) {
     dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
@@ -225,6 +227,17 @@ void free_all(efunc_t* h) {
   dfree(h->scratch);
   drop_fit_graph(h);
   free_timing(h);
+  for (int k = 0; k < 2; ++k) {
+    if (h->aio_done[k]) cudaEventSynchronize(h->aio_done[k]);
+    dfree(h->aio_q[k]); dfree(h->aio_o[k]); dfree(h->aio_loss[k]);
+    if (h->aio_copied[k]) cudaEventDestroy(h->aio_copied[k]);
+    if (h->aio_done[k]) cudaEventDestroy(h->aio_done[k]);
+    h->aio_copied[k] = h->aio_done[k] = nullptr;
+  }
+  if (h->aio_pin) cudaFreeHost(h->aio_pin);
+  h->aio_pin = nullptr;
+  if (h->aio_stream) cudaStreamDestroy(h->aio_stream);
+  h->aio_stream = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   h->cap_stream = nullptr;
 }
@@ -255,7 +268,7 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
   h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
   h->launches += launch_items_write(h->bin_start, nb, h->item_off, h->items, s);
-  const int64_t items = (J + QW - 1) / QW + nb + 1;  // launch bound; kernels read the count
+  const int64_t items = (J + IQ - 1) / IQ + nb + 1;  // launch bound; kernels read the count
   h->fwd_items_bound = items;
   a = FwdArgs{};
   a.kv = keys_view(h);
@@ -448,6 +461,111 @@ efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cuda
   h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
   CK(cudaGetLastError());
   return rebuild_keys(h, s);
+}
+
+// The device work of one fit step (grad zero, forward_backward, AdamW) on stream s, replayed from
+// a CUDA graph once the same call repeats (graph slot `slot`: one per staging buffer).
+efunc_status fit_device_step(efunc_t* h, int slot, const float* qd, const float* od, int64_t J,
+                             const efunc_loss* loss, const efunc_adamw* hp, float* grad_ws, float* lossd,
+                             cudaStream_t s) {
+  float* g = grad_ws ? grad_ws : h->fit_grad;
+  auto device_work = [&](cudaStream_t st) -> efunc_status {
+    CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, st));
+    RET(do_forward_backward(h, qd, od, J, loss, nullptr, g, lossd, st));
+    return do_adamw(h, g, hp, st);
+  };
+  efunc_t::FitKey key{};
+  key.q = qd; key.o = od; key.g = g; key.lossd = lossd;
+  key.J = J; key.J_global = loss->J_global; key.kind = loss->kind; key.eik = loss->eikonal_lambda;
+  key.lr = hp->lr; key.b1 = hp->beta1; key.b2 = hp->beta2; key.eps = hp->eps; key.wd = hp->weight_decay;
+  key.mask = hp->decay_mask; key.count_kept = h->count_kept;
+  const bool same = h->fit_seen[slot] && std::memcmp(&key, &h->fit_key[slot], sizeof(key)) == 0;
+  if (h->cfg.fit_graph && !h->cfg.sync_checks && same) {
+    if (!h->fit_exec[slot]) {
+      // second identical call: capture the device work once (nothing reallocates: the first,
+      // eager call sized every workspace) and replay it from now on
+      if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      const int64_t l0 = h->launches;
+      CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const efunc_status st = device_work(h->cap_stream);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(h->cap_stream, &graph);
+      if (st != EFUNC_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      CK(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&h->fit_exec[slot], graph, 0);
+      cudaGraphDestroy(graph);
+      CK(ie);
+      h->fit_launches[slot] = h->launches - l0;
+      h->launches = l0;
+    }
+    CK(cudaGraphLaunch(h->fit_exec[slot], s));
+    h->launches += h->fit_launches[slot];
+  } else {
+    if (h->fit_exec[slot]) cudaGraphExecDestroy(h->fit_exec[slot]);
+    h->fit_exec[slot] = nullptr;
+    RET(device_work(s));
+    h->fit_key[slot] = key;
+    h->fit_seen[slot] = 1;
+  }
+  return EFUNC_OK;
+}
+
+// host_io 2: store a finished step's loss (read back into pinned memory) to the caller's float
+void flush_loss(efunc_t* h, int slot) {
+  efunc_t::LossCopy& c = h->aio_pay[slot];
+  if (c.dst) *c.dst = *c.src;
+  c.dst = nullptr;
+}
+
+// host_io 2: H2D into staging slot k % 2 on the handle's copy stream (after step k-2 released
+// that slot), the step on the caller's stream after the copy, the loss D2H into pinned memory;
+// the host stores it to *loss_out when it next waits on that slot (call k+2 or efunc_sync). The
+// host blocks only for step k-2, so the copy of step k+1 overlaps the compute of step k. (A
+// cudaLaunchHostFunc callback instead serialises the copy stream with the compute: measured.)
+efunc_status fit_step_async(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                            const efunc_adamw* hp, float* grad_ws, float* loss_out, cudaStream_t s) {
+  if (J > 0 && (!q || !o)) return fail(h, EFUNC_EINVAL, "q or o is NULL");
+  if (!h->aio_stream) {
+    CK(cudaStreamCreateWithFlags(&h->aio_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&h->aio_copied[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->aio_done[k], cudaEventDisableTiming));
+      CK(dalloc(&h->aio_loss[k], 1));
+    }
+    CK(cudaHostAlloc((void**)&h->aio_pin, 2 * sizeof(float), cudaHostAllocDefault));
+  }
+  const int slot = (int)(h->aio_seq & 1);
+  CK(cudaEventSynchronize(h->aio_done[slot]));  // step k-2 finished: its loss is in aio_pin
+  flush_loss(h, slot);
+  if (J > h->aio_cap) {
+    CK(cudaEventSynchronize(h->aio_done[slot ^ 1]));
+    drop_fit_graph(h);
+    for (int k = 0; k < 2; ++k) {
+      dfree(h->aio_q[k]);
+      dfree(h->aio_o[k]);
+      CK(dalloc(&h->aio_q[k], 3 * (size_t)J));
+      CK(dalloc(&h->aio_o[k], (size_t)J));
+    }
+    h->aio_cap = J;
+  }
+  ++h->aio_seq;
+  if (J > 0) {
+    CK(cudaMemcpyAsync(h->aio_q[slot], q, sizeof(float) * 3 * (size_t)J, cudaMemcpyHostToDevice, h->aio_stream));
+    CK(cudaMemcpyAsync(h->aio_o[slot], o, sizeof(float) * (size_t)J, cudaMemcpyHostToDevice, h->aio_stream));
+  }
+  CK(cudaEventRecord(h->aio_copied[slot], h->aio_stream));
+  CK(cudaStreamWaitEvent(s, h->aio_copied[slot], 0));
+  RET(fit_device_step(h, slot, h->aio_q[slot], h->aio_o[slot], J, loss, hp, grad_ws, h->aio_loss[slot], s));
+  if (loss_out) {
+    CK(cudaMemcpyAsync(h->aio_pin + slot, h->aio_loss[slot], sizeof(float), cudaMemcpyDeviceToHost, s));
+    h->aio_pay[slot].src = h->aio_pin + slot;
+    h->aio_pay[slot].dst = loss_out;
+  }
+  CK(cudaEventRecord(h->aio_done[slot], s));  // the host waits for it before reusing the slot
+  return EFUNC_OK;
 }
 
 // batched handles (n_shapes > 1): the k-th shape's slice of a per-shape array, and error relay
@@ -666,8 +784,11 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "fit_step needs a loss");
   if (!hp) return fail(h, EFUNC_EINVAL, "NULL AdamW parameters");
+  if (host_io < 0 || host_io > 2) return fail(h, EFUNC_EINVAL, "host_io must be 0, 1 or 2");
+  if (J < 0) return fail(h, EFUNC_EINVAL, "J < 0");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (host_io == 2) return fit_step_async(h, q, o, J, loss, hp, grad_ws, loss_out, s);
   const float* qd = q;
   const float* od = o;
   float* lossd = loss_out;
@@ -689,50 +810,24 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
     od = h->io_o;
     lossd = h->io_loss;
   }
-  float* g = grad_ws ? grad_ws : h->fit_grad;
-  auto device_work = [&](cudaStream_t st) -> efunc_status {
-    CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, st));
-    RET(do_forward_backward(h, qd, od, J, loss, nullptr, g, lossd, st));
-    return do_adamw(h, g, hp, st);
-  };
-  efunc_t::FitKey key{};
-  key.q = qd; key.o = od; key.g = g; key.lossd = lossd;
-  key.J = J; key.J_global = loss->J_global; key.kind = loss->kind; key.eik = loss->eikonal_lambda;
-  key.lr = hp->lr; key.b1 = hp->beta1; key.b2 = hp->beta2; key.eps = hp->eps; key.wd = hp->weight_decay;
-  key.mask = hp->decay_mask; key.count_kept = h->count_kept;
-  const bool same = h->fit_seen && std::memcmp(&key, &h->fit_key, sizeof(key)) == 0;
-  if (h->cfg.fit_graph && !h->cfg.sync_checks && same) {
-    if (!h->fit_exec) {
-      // second identical call: capture the device work once (nothing reallocates: the first,
-      // eager call sized every workspace) and replay it from now on
-      if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
-      const int64_t l0 = h->launches;
-      CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
-      const efunc_status st = device_work(h->cap_stream);
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(h->cap_stream, &graph);
-      if (st != EFUNC_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return st;
-      }
-      CK(ce);
-      const cudaError_t ie = cudaGraphInstantiate(&h->fit_exec, graph, 0);
-      cudaGraphDestroy(graph);
-      CK(ie);
-      h->fit_launches = h->launches - l0;
-      h->launches = l0;
-    }
-    CK(cudaGraphLaunch(h->fit_exec, s));
-    h->launches += h->fit_launches;
-  } else {
-    drop_fit_graph(h);
-    RET(device_work(s));
-    h->fit_key = key;
-    h->fit_seen = 1;
-  }
+  RET(fit_device_step(h, 0, qd, od, J, loss, hp, grad_ws, lossd, s));
   if (host_io) {
     if (loss_out) CK(cudaMemcpyAsync(loss_out, lossd, sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+  }
+  return EFUNC_OK;
+}
+
+efunc_status efunc_sync(efunc_t* h) {
+  if (h && !h->kids.empty()) {
+    for (size_t k = 0; k < h->kids.size(); ++k) RET(kid_ok(h, k, efunc_sync(h->kids[k])));
+    return EFUNC_OK;
+  }
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  DeviceGuard dg(h->cfg.device);
+  for (int k = 0; k < 2; ++k) {
+    if (h->aio_done[k]) CK(cudaEventSynchronize(h->aio_done[k]));
+    flush_loss(h, k);
   }
   return EFUNC_OK;
 }

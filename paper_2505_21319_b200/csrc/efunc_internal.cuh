@@ -28,7 +28,11 @@
 
 namespace ef {
 
-constexpr int QW = 32;              // queries per work item (one warp; the forward supports 64)
+constexpr int QW = 32;              // max queries per work item (one warp)
+#ifndef ITEM_Q
+#define ITEM_Q 32
+#endif
+constexpr int IQ = ITEM_Q;          // queries per work item the binning produces (<= QW)
 constexpr int NTHREADS = 32;        // one warp per CTA: items retire independently
 constexpr int NWARP = NTHREADS / 32;
 constexpr int BL_CAP = 16384;       // max list length per brick (longer: enumerate fallback)
@@ -36,7 +40,7 @@ constexpr uint32_t BL_OVERFLOW = 0xffffffffu;
 constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
 // per-warp id scratch of the persistent list builders (k_fit, k_brick_lists): SCRATCH_WARPS slots
 // of BL_CAP ids, padded so the slots do not alias in L1
-constexpr int SCRATCH_WARPS = 148 * 16;
+constexpr int SCRATCH_WARPS = 148 * 32;
 constexpr size_t SCRATCH_STRIDE = BL_CAP + 32;
 constexpr uint32_t QSUB = 8;        // query bins per brick (octants)
 constexpr int WL_PER_QUERY = 64;    // forward->backward candidate pool capacity per query
@@ -287,10 +291,21 @@ struct efunc {
     double lr, b1, b2, eps, wd;
     uint32_t mask;
     int count_kept;
-  } fit_key{};
-  int fit_seen = 0;                  // fit_key holds the last (eager) call
-  cudaGraphExec_t fit_exec = nullptr;
-  int64_t fit_launches = 0;          // kernels inside the captured graph
+  } fit_key[2]{};
+  int fit_seen[2] = {0, 0};          // fit_key[slot] holds the last (eager) call of that slot
+  cudaGraphExec_t fit_exec[2] = {nullptr, nullptr};  // slot 0: host_io 0/1; slots 0/1: host_io 2
+  int64_t fit_launches[2] = {0, 0};  // kernels inside the captured graphs
+  // host_io 2 (pipelined host I/O): double-buffered device staging, a copy stream, events
+  float* aio_q[2] = {nullptr, nullptr};
+  float* aio_o[2] = {nullptr, nullptr};
+  float* aio_loss[2] = {nullptr, nullptr};
+  float* aio_pin = nullptr;          // pinned host float[2]: the losses read back
+  struct LossCopy { const float* src; float* dst; } aio_pay[2]{};
+  int64_t aio_cap = 0;
+  int64_t aio_seq = 0;
+  cudaStream_t aio_stream = nullptr;
+  cudaEvent_t aio_copied[2] = {nullptr, nullptr};
+  cudaEvent_t aio_done[2] = {nullptr, nullptr};
   cudaStream_t cap_stream = nullptr;
   // kernel timing (efunc_set_timing): event pairs, slot = call index mod slots
   std::vector<efunc*> kids;          // n_shapes > 1: one single-shape handle per shape

@@ -348,7 +348,7 @@ __global__ void k_items_count(const uint32_t* __restrict__ bin_start, uint32_t n
     }
     uint32_t s, n;
     brick_range(bin_start, c, nb, s, n);
-    cnt[c] = (n + QW - 1) / QW;
+    cnt[c] = (n + IQ - 1) / IQ;
   }
 }
 
@@ -358,7 +358,7 @@ __global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t n
     uint32_t s, n;
     brick_range(bin_start, c, nb, s, n);
     if (n == 0) continue;
-    const uint32_t m = (n + QW - 1) / QW;
+    const uint32_t m = (n + IQ - 1) / IQ;
     const uint32_t o = off[c];
     const int brick = (c == nb) ? -1 : (int)c;
     for (uint32_t i = 0; i < m; ++i) {

@@ -246,8 +246,8 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   }
   __syncwarp();
   float Z, M;
-  if (nact <= 16) fwd_sums_x<8>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
-  else fwd_sums_x<16>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+  if (IQ <= 16 || nact <= 16) fwd_sums_x<8>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+  else fwd_sums_x<(IQ > 16 ? 16 : 8)>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
   const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
   if (__any_sync(~0u, bad)) {  // Z underflow (far queries): the split kernels shift exactly
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;

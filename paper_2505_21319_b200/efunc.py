@@ -25,7 +25,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
             "efunc_adamw_step",
             "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
-            "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_last_error",
+            "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_sync", "efunc_last_error",
             "efunc_abi_version"]
 
 
@@ -87,6 +87,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_set_counting": [P, i32],
         "efunc_get_stats": [P, C.POINTER(Stats), P],
         "efunc_check": [P, P],
+        "efunc_sync": [P],
         "efunc_set_timing": [P, i32],
         "efunc_get_kernel_ms": [P, P, i32],
     }
@@ -252,14 +253,22 @@ class EFunc:
         return O, G
 
     def fit_step(self, q, o, hp: AdamW | None = None, loss: int = LOSS_MSE, eikonal_lambda: float = 0.1,
-                 J_global: int = 0, grad_ws=None, loss_out=None):
+                 J_global: int = 0, grad_ws=None, loss_out=None, pipelined: bool = False):
         """forward + loss + backward + AdamW. q/o either CUDA tensors (async, loss_out a device
-        tensor) or pinned CPU tensors (host_io: copies inside the call; returns the loss float)."""
+        tensor) or pinned CPU tensors (host_io: copies inside the call; returns the loss float).
+        pipelined=True with pinned CPU tensors: host_io 2 (the copy of the next step overlaps this
+        step's compute); returns a ctypes float array filled in by the time sync() returns."""
         hp = hp or AdamW()
         J = self._J(q)
         lc = Loss(loss, eikonal_lambda, J_global)
         p = hp.c()
         host = q.device.type == "cpu"
+        if host and pipelined:
+            lo = (C.c_float * self.S)()
+            self._aio_keep = (getattr(self, "_aio_keep", []) + [(lo, q, o)])[-4:]  # alive until reused
+            self._ok(self.lib.efunc_fit_step(self.h, q.data_ptr(), o.data_ptr(), J, C.byref(lc), C.byref(p),
+                                             _ptr(grad_ws), C.addressof(lo), 2, self._stream()))
+            return lo
         if host:
             lo = (C.c_float * self.S)()
             self._ok(self.lib.efunc_fit_step(self.h, q.data_ptr(), o.data_ptr(), J, C.byref(lc), C.byref(p),
@@ -300,6 +309,10 @@ class EFunc:
 
     def set_counting(self, on: bool):
         self._ok(self.lib.efunc_set_counting(self.h, int(on)))
+
+    def sync(self):
+        """wait for the pipelined (host_io 2) fit steps"""
+        self._ok(self.lib.efunc_sync(self.h))
 
     def set_timing(self, slots: int):
         """Record CUDA events around the dominant kernel of each backward/forward_backward call."""
