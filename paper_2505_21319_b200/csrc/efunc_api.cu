@@ -2,6 +2,7 @@
 // Every step of the path runs in the kernels of k_bin.cu / k_lists.cu / k_forward.cu / k_backward.cu / k_adamw.cu; this
 // file only validates arguments, sizes workspaces and enqueues launches on the caller's stream.
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <new>
 #include <string>
@@ -252,18 +253,24 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   const uint32_t nbins = nb * QSUB + 1;          // octant bins + the out-of-domain bin
   CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
-  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->wl_top, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->slow_n, 0, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->cand_pairs, 0, 3 * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(&h->ds->fwd_next, 0, 3 * sizeof(uint32_t), s));  // fwd_next, bwd_next, fit_next
+  static_assert(offsetof(DevScalars, kept_pairs_offset) + sizeof(unsigned long long) == sizeof(DevScalars),
+                "the per-forward counters end DevScalars");
+  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(DevScalars) - offsetof(DevScalars, overflow_items), s));
   h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
-  h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
-  if (with_mh)  // + the per-query shift bound (fused path)
+  if (with_mh && !h->cfg.deterministic) {
+    // fused path: the atomic scatter order inside a bin is kept (only deterministic mode needs the
+    // stable rank); the gather then runs in sorted order, so the shift bounds' key loads of
+    // neighbouring threads hit the same cells
+    h->launches += launch_scatter_only(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_order, s);
     h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh, s);
-  else
-    h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
+  } else {
+    h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
+    if (with_mh)  // + the per-query shift bound
+      h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh, s);
+    else
+      h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
+  }
   // work items: balanced runs of <= QW sorted queries of one brick
   h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
   h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);

@@ -66,28 +66,29 @@ struct KeysView {
 struct DevScalars {
   float bl_min;            // as float; written via atomicMin on its bits (bl > 0)
   uint32_t nonfinite;
-  uint32_t overflow_items;
   uint32_t pool_top;       // brick-list pool allocation cursor
   uint32_t lists_invalid;  // 1: the brick lists must be rebuilt (skin exceeded / new theta)
   uint32_t list_builds;    // number of brick-list builds (diagnostics)
   uint32_t ovf_count;      // bricks overflowed in the running build
   uint32_t pool_used;      // entries of the last completed build
   uint32_t ovf_last;       // overflowed bricks of the last completed build
-  uint32_t wl_top;         // per-item candidate-list pool cursor (reset every forward)
   float umax;              // deterministic backward: max_j (|dL/dO_j| + |dL/dG_j|_1) of the call
   uint32_t fix_overflow;   // deterministic backward: a partial left the fixed-point range
-  uint32_t slow_n;         // items k_forward_keys left to the exact-min slow path (reset every forward)
   uint32_t adam_done;      // k_adamw blocks finished (the last one advances adam_t and resets this)
   uint32_t keys_resort;    // an offset key changed lattice cell: re-sort the keys (else only regather)
-  uint32_t pad1_;
   unsigned long long adam_t;  // AdamW step counter (device-side so CUDA graphs replay it correctly)
+  // ---- reset by every forward (one memset from overflow_items to the end)
+  uint32_t overflow_items;
+  uint32_t wl_top;         // per-item candidate-list pool cursor
+  uint32_t slow_n;         // items left to the exact-shift / no-list split kernels
+  uint32_t fwd_next;       // persistent fetch cursors
+  uint32_t bwd_next;
+  uint32_t fit_next;
   unsigned long long cand_pairs;
   unsigned long long kept_pairs;
   unsigned long long kept_pairs_offset;
-  uint32_t fwd_next;       // persistent fetch cursors (reset before each launch)
-  uint32_t bwd_next;
-  uint32_t fit_next;
 };
+
 
 
 struct FwdArgs {
@@ -189,6 +190,8 @@ int launch_gather_queries(const uint32_t* order, const float* q, const float* o,
                           float4* qs, int* perm, cudaStream_t s);
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
                              float4* qs, int* perm, float* qmh, cudaStream_t s);
+int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
+                        uint32_t* out_idx, cudaStream_t s);
 int launch_items_count(const uint32_t* bin_start, uint32_t nbins, uint32_t* cnt, cudaStream_t s);
 int launch_items_write(const uint32_t* bin_start, uint32_t nbins, const uint32_t* off, int4* items,
                        cudaStream_t s);

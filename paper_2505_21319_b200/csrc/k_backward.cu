@@ -297,7 +297,8 @@ static unsigned bwd_blocks(int64_t n_items) {
 
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
-  const unsigned blocks = bwd_blocks(n_items);
+  // list mode (the fused path's leftover items, usually none): one CTA per SM
+  const unsigned blocks = a.list ? 148u : bwd_blocks(n_items);
   if (a.eik) k_backward<true, false><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
   else k_backward<false, false><<<blocks, 32 * BW_WARPS, 0, s>>>(a);
   return 1;

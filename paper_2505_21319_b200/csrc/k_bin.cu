@@ -237,6 +237,14 @@ int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_st
   return 2;
 }
 
+// The counting sort without the stable rank (bin order only; within a bin, atomics' order).
+int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
+                        uint32_t* out_idx, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, out_idx, nullptr);
+  return 1;
+}
+
 __global__ void k_gather_keys(const uint32_t* __restrict__ order, const float4* __restrict__ key_raw,
                               float4* __restrict__ key_sorted, int* __restrict__ kid, uint32_t n) {
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {

@@ -508,7 +508,9 @@ def test_batched_shapes_match_single_handles_and_oracle():
     for k in range(S):
         m1 = ef.EFunc(R, ths[k])
         g1, O1, L1 = m1.forward_backward(dev(q[k]), dev(o[k]), loss=ef.LOSS_MSE, want_O=True)
-        assert np.array_equal(O1.cpu().numpy(), Ob[k])
+        # same kernels on the same data; the in-bin query order (atomic scatter) may differ, which
+        # changes item composition and hence only the rounding of negligible candidate pairs
+        assert nw(O1.cpu().numpy(), Ob[k]) <= 1e-6
         assert np.abs(g1.cpu().numpy() - gb[k]).max() <= 1e-6 * np.abs(gb[k]).max()
     f = orc.forward(ths[1], R, q[1])
     _, r = orc.mse_loss(f.O, o[1])
