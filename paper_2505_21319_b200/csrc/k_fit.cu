@@ -33,6 +33,9 @@ namespace ef {
 #ifndef FT_MIN_WARPS
 #define FT_MIN_WARPS 16  // warps per SM (measured 16..28; the 16-pair forward needs 128 registers)
 #endif
+#ifndef FT_BWD2
+#define FT_BWD2 1  // backward: two candidate keys per lane
+#endif
 constexpr int FT_WARPS = 4;
 constexpr int FT_BLOCKS = 148 * (FT_MIN_WARPS / FT_WARPS);
 static_assert(FT_BLOCKS * FT_WARPS <= SCRATCH_WARPS, "one scratch slot per warp");
@@ -202,6 +205,57 @@ __device__ __forceinline__ MseSums bwd_sums_x(const KeyX& K, const int npairs, c
   return s;
 }
 
+// Two keys per lane (rounds of 64 keys): every query pair loaded from shared memory serves both,
+// halving the backward's shared-memory wavefronts per pair and doubling the independent chains.
+__device__ __forceinline__ void bwd_sums_x2(const KeyX& KA, const KeyX& KB, const int npairs, const float4* pA,
+                                            const float4* pB, const float4* pC, MseSums& sa, MseSums& sb) {
+  float2 Sc[2], Stx[2], Sty[2], Stz[2], Su[2], Sux[2], Suy[2], Suz[2], Suq[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    Sc[u] = Stx[u] = Sty[u] = Stz[u] = Su[u] = Sux[u] = Suy[u] = Suz[u] = Suq[u] = make_float2(0.f, 0.f);
+  }
+  auto pair = [&](const int u, const KeyX& K, const float4 QA, const float4 QB, const float4 QC) {
+    FX_EF(K, QA, QB, e, f)
+    const float2 p = make_float2(ex2f(e.x), ex2f(e.y));
+    const float2 del = __fadd2_rn(f, make_float2(QC.z, QC.w));
+    const float2 t = __fmul2_rn(make_float2(QC.x, QC.y), p);
+    const float2 uu = __fmul2_rn(t, del);
+    Sc[u] = __fadd2_rn(Sc[u], t);
+    Stx[u] = __ffma2_rn(t, make_float2(QA.x, QA.y), Stx[u]);
+    Sty[u] = __ffma2_rn(t, make_float2(QA.z, QA.w), Sty[u]);
+    Stz[u] = __ffma2_rn(t, make_float2(QB.x, QB.y), Stz[u]);
+    Su[u] = __fadd2_rn(Su[u], uu);
+    Sux[u] = __ffma2_rn(uu, make_float2(QA.x, QA.y), Sux[u]);
+    Suy[u] = __ffma2_rn(uu, make_float2(QA.z, QA.w), Suy[u]);
+    Suz[u] = __ffma2_rn(uu, make_float2(QB.x, QB.y), Suz[u]);
+    Suq[u] = __ffma2_rn(uu, make_float2(QB.z, QB.w), Suq[u]);
+  };
+  const int np2 = (npairs + 1) & ~1;
+#pragma unroll 1
+  for (int jp = 0; jp < np2; jp += 2) {
+    const float4 QA0 = pA[jp], QB0 = pB[jp], QC0 = pC[jp];
+    const float4 QA1 = pA[jp + 1], QB1 = pB[jp + 1], QC1 = pC[jp + 1];
+    pair(0, KA, QA0, QB0, QC0);
+    pair(1, KB, QA0, QB0, QC0);
+    pair(0, KA, QA1, QB1, QC1);
+    pair(1, KB, QA1, QB1, QC1);
+  }
+  auto fin = [&](const int u, const KeyX& K, MseSums& s) {
+    const float sc = Sc[u].x + Sc[u].y, su = Su[u].x + Su[u].y;
+    const float sux = Sux[u].x + Sux[u].y, suy = Suy[u].x + Suy[u].y, suz = Suz[u].x + Suz[u].y;
+    s.sc = sc;
+    s.sgx = fmaf(-K.kx, sc, Stx[u].x + Stx[u].y);
+    s.sgy = fmaf(-K.ky, sc, Sty[u].x + Sty[u].y);
+    s.sgz = fmaf(-K.kz, sc, Stz[u].x + Stz[u].y);
+    s.ss = fmaf(K.kk, su, fmaf(-2.0f * K.kx, sux, fmaf(-2.0f * K.ky, suy, fmaf(-2.0f * K.kz, suz, Suq[u].x + Suq[u].y))));
+    s.sdx = fmaf(-K.kx, su, sux);
+    s.sdy = fmaf(-K.ky, su, suy);
+    s.sdz = fmaf(-K.kz, su, suz);
+  };
+  fin(0, KA, sa);
+  fin(1, KB, sb);
+}
+
 __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* L) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
@@ -276,6 +330,41 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   }
   __syncwarp();
   const int npairs = (nact + 1) >> 1;
+#if FT_BWD2
+  // rounds of 64 candidates: lane keys base + lane and base + 32 + lane (records one round ahead;
+  // a missing second key is a far zero key whose sums are discarded)
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t iA = ((uint32_t)lane < wn) ? L[lane] : 0u, iB = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 aA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA]) : far_a;
+  float4 bA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA + 1]) : z4;
+  float4 aB = ((uint32_t)lane + 32 < wn) ? __ldg(&kv.grid_raw[2 * iB]) : far_a;
+  float4 bB = ((uint32_t)lane + 32 < wn) ? __ldg(&kv.grid_raw[2 * iB + 1]) : z4;
+  for (uint32_t base = 0; base < wn; base += 64) {
+    const uint32_t k = base + lane;
+    const uint32_t idA = iA, idB = iB;
+    const float4 a0 = aA, b0 = bA, a1 = aB, b1 = bB;
+    iA = (k + 64 < wn) ? L[k + 64] : 0u;
+    iB = (k + 96 < wn) ? L[k + 96] : 0u;
+    aA = far_a; bA = z4; aB = far_a; bB = z4;
+    if (k + 64 < wn) {
+      aA = __ldg(&kv.grid_raw[2 * iA]);
+      bA = __ldg(&kv.grid_raw[2 * iA + 1]);
+    }
+    if (k + 96 < wn) {
+      aB = __ldg(&kv.grid_raw[2 * iB]);
+      bB = __ldg(&kv.grid_raw[2 * iB + 1]);
+    }
+    if (base + 32 < wn) {  // warp-uniform: two keys per lane
+      MseSums s0, s1;
+      bwd_sums_x2(key_x(a0, b0, o), key_x(a1, b1, o), npairs, S.qa, S.qb, S.pc, s0, s1);
+      if (k < wn) bwd_mse_red(s0, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+      if (k + 32 < wn) bwd_mse_red(s1, a1, b1, (int)idB, kv.n_nodes, F.gpad);
+    } else if (k < wn) {
+      const MseSums ms = bwd_sums_x(key_x(a0, b0, o), npairs, S.qa, S.qb, S.pc);
+      bwd_mse_red(ms, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+    }
+  }
+#else
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
   uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
@@ -296,6 +385,7 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
       bwd_mse_red(ms, a, b, (int)id, kv.n_nodes, F.gpad);
     }
   }
+#endif
 }
 
 __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(const FitArgs F) {
