@@ -76,12 +76,18 @@ BrickGeom brick_geom(const efunc_config& cfg, int NC, float h) {
     const double rho = std::sqrt(0.75 * h * h + cfg.cutoff_T / std::exp(7.0));
     int B = 1;
     while (2 * B * h <= 0.5 * rho && 2 * B <= NC) B *= 2;  // largest power of 2 with B h <= rho / 2
+#ifdef EF_BRICK_B
+    B = EF_BRICK_B < NC ? EF_BRICK_B : NC;
+#endif
     g.B = B;
   }
   g.nb = (NC + g.B - 1) / g.B;
   g.bits = 0;
   while ((1 << g.bits) < g.nb) ++g.bits;
   g.n_codes = 1u << (3 * g.bits);
+  g.sub_bits = 0;
+  while ((1 << g.sub_bits) < 2 * g.B) ++g.sub_bits;
+  g.qsub = 1u << (3 * g.sub_bits);
   return g;
 }
 
@@ -250,7 +256,7 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   const int kind = loss ? loss->kind : EFUNC_LOSS_NONE;
   RET(ensure_queries(h, J));
   const uint32_t nb = h->bg.n_codes;             // bricks
-  const uint32_t nbins = nb * QSUB + 1;          // octant bins + the out-of-domain bin
+  const uint32_t nbins = nb * h->bg.qsub + 1;    // half-cell bins + the out-of-domain bin
   CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
   CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
   static_assert(offsetof(DevScalars, kept_pairs_offset) + sizeof(unsigned long long) == sizeof(DevScalars),
@@ -272,9 +278,9 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
       h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
   }
   // work items: balanced runs of <= QW sorted queries of one brick
-  h->launches += launch_items_count(h->bin_start, nb, h->item_cnt, s);
+  h->launches += launch_items_count(h->bin_start, nb, h->bg.qsub, h->item_cnt, s);
   h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
-  h->launches += launch_items_write(h->bin_start, nb, h->item_off, h->items, s);
+  h->launches += launch_items_write(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
   const int64_t items = (J + IQ - 1) / IQ + nb + 1;  // launch bound; kernels read the count
   h->fwd_items_bound = items;
   a = FwdArgs{};
@@ -658,7 +664,7 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->ds, 1));
     CK(dalloc(&h->scratch, (size_t)SCRATCH_WARPS * SCRATCH_STRIDE));
     h->bg = brick_geom(h->cfg, h->NC, h->h);
-    const size_t nbins = (size_t)h->bg.n_codes * QSUB + 1;
+    const size_t nbins = (size_t)h->bg.n_codes * h->bg.qsub + 1;
     CK(dalloc(&h->bl_off, h->bg.n_codes));
     CK(dalloc(&h->bl_n, h->bg.n_codes));
     const double pool = (double)h->n_keys * POOL_PER_KEY;

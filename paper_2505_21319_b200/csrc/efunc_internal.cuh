@@ -42,7 +42,7 @@ constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
 // of BL_CAP ids, padded so the slots do not alias in L1
 constexpr int SCRATCH_WARPS = 148 * 32;
 constexpr size_t SCRATCH_STRIDE = BL_CAP + 32;
-constexpr uint32_t QSUB = 8;        // query bins per brick (octants)
+
 constexpr int WL_PER_QUERY = 64;    // forward->backward candidate pool capacity per query
 constexpr float SKIN_H = 0.25f;     // Verlet skin of the brick lists, in lattice spacings
 constexpr float SKIN_MU = 0.05f;    // allowed relative drift of beta between list builds
@@ -166,6 +166,8 @@ struct BrickGeom {
   int nb;         // bricks per axis
   int bits;       // Morton bits per axis (2^bits >= nb)
   uint32_t n_codes;  // 2^(3 bits)
+  int sub_bits;   // query sub-bins per brick edge = 2^sub_bits = 2B (half-cells)
+  uint32_t qsub;  // query sub-bins per brick = (2B)^3, Morton ordered inside the brick
 };
 
 // ---------------------------------------------------------------- launchers (host)
@@ -192,8 +194,8 @@ int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const fl
                              float4* qs, int* perm, float* qmh, cudaStream_t s);
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
                         uint32_t* out_idx, cudaStream_t s);
-int launch_items_count(const uint32_t* bin_start, uint32_t nbins, uint32_t* cnt, cudaStream_t s);
-int launch_items_write(const uint32_t* bin_start, uint32_t nbins, const uint32_t* off, int4* items,
+int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s);
+int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
                        cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
 int launch_forward_slow(const FwdArgs& a, cudaStream_t s);

@@ -276,8 +276,9 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every 3
 __global__ void k_query_bins(const float* __restrict__ q, const float* __restrict__ o, int64_t J, BrickGeom bg,
                              int NC, float inv_h, uint32_t* __restrict__ bins, uint32_t* __restrict__ count,
                              DevScalars* ds) {
-  const uint32_t outside = bg.n_codes * QSUB;
-  const float sub_scale = 2.0f * inv_h / (float)bg.B;
+  const uint32_t outside = bg.n_codes * bg.qsub;
+  const float sub_scale = 2.0f * inv_h;  // half-cells
+  const int ns = 2 * bg.B;
   bool bad = false;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
     const float x = q[3 * j], y = q[3 * j + 1], z = q[3 * j + 2];
@@ -289,11 +290,12 @@ __global__ void k_query_bins(const float* __restrict__ q, const float* __restric
       const int bx = cell_clamp(x, inv_h, NC) / bg.B;
       const int by = cell_clamp(y, inv_h, NC) / bg.B;
       const int bz = cell_clamp(z, inv_h, NC) / bg.B;
-      // octant of the query inside its brick: the 8 sub-bins of a brick stay contiguous
-      const int sx = min(max((int)floorf((x + 1.0f) * sub_scale) - 2 * bx, 0), 1);
-      const int sy = min(max((int)floorf((y + 1.0f) * sub_scale) - 2 * by, 0), 1);
-      const int sz = min(max((int)floorf((z + 1.0f) * sub_scale) - 2 * bz, 0), 1);
-      b = (spread3(bx) | (spread3(by) << 1) | (spread3(bz) << 2)) * QSUB + (uint32_t)(sx | (sy << 1) | (sz << 2));
+      // half-cell of the query inside its brick (Morton order): a brick's sub-bins stay contiguous
+      const int sx = min(max((int)floorf((x + 1.0f) * sub_scale) - ns * bx, 0), ns - 1);
+      const int sy = min(max((int)floorf((y + 1.0f) * sub_scale) - ns * by, 0), ns - 1);
+      const int sz = min(max((int)floorf((z + 1.0f) * sub_scale) - ns * bz, 0), ns - 1);
+      b = (spread3(bx) | (spread3(by) << 1) | (spread3(bz) << 2)) * bg.qsub +
+          (spread3(sx) | (spread3(sy) << 1) | (spread3(sz) << 2));
     }
     bins[j] = b;
     atomicAdd(&count[b], 1u);
@@ -338,33 +340,34 @@ int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------ work items
-// A work item is a balanced run of <= QW queries of one brick (its QSUB octant bins are
+// A work item is a balanced run of <= QW queries of one brick (its qsub half-cell bins are
 // contiguous in the sorted stream): ceil(n/QW) items per brick. The brick field is the brick's
 // Morton code, or -1 for the out-of-domain bin (index nb = number of bricks).
-__device__ __forceinline__ void brick_range(const uint32_t* bin_start, uint32_t c, uint32_t nb, uint32_t& s,
-                                            uint32_t& n) {
-  s = bin_start[c * QSUB];
-  const uint32_t e = (c == nb) ? bin_start[nb * QSUB + 1] : bin_start[(c + 1) * QSUB];
+__device__ __forceinline__ void brick_range(const uint32_t* bin_start, uint32_t c, uint32_t nb, uint32_t qsub,
+                                            uint32_t& s, uint32_t& n) {
+  s = bin_start[c * qsub];
+  const uint32_t e = (c == nb) ? bin_start[nb * qsub + 1] : bin_start[(c + 1) * qsub];
   n = e - s;
 }
 
-__global__ void k_items_count(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t* __restrict__ cnt) {
+__global__ void k_items_count(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t qsub,
+                              uint32_t* __restrict__ cnt) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb + 1; c += gridDim.x * blockDim.x) {
     if (c == nb + 1) {
       cnt[c] = 0;
       continue;
     }
     uint32_t s, n;
-    brick_range(bin_start, c, nb, s, n);
+    brick_range(bin_start, c, nb, qsub, s, n);
     cnt[c] = (n + IQ - 1) / IQ;
   }
 }
 
-__global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t nb,
+__global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t qsub,
                               const uint32_t* __restrict__ off, int4* __restrict__ items) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb; c += gridDim.x * blockDim.x) {
     uint32_t s, n;
-    brick_range(bin_start, c, nb, s, n);
+    brick_range(bin_start, c, nb, qsub, s, n);
     if (n == 0) continue;
     const uint32_t m = (n + IQ - 1) / IQ;
     const uint32_t o = off[c];
@@ -376,14 +379,14 @@ __global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t n
   }
 }
 
-int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t* cnt, cudaStream_t s) {
-  k_items_count<<<grid_for(nb + 2, 256), 256, 0, s>>>(bin_start, nb, cnt);
+int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s) {
+  k_items_count<<<grid_for(nb + 2, 256), 256, 0, s>>>(bin_start, nb, qsub, cnt);
   return 1;
 }
 
-int launch_items_write(const uint32_t* bin_start, uint32_t nb, const uint32_t* off, int4* items,
+int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
                        cudaStream_t s) {
-  k_items_write<<<grid_for(nb + 1, 128), 128, 0, s>>>(bin_start, nb, off, items);
+  k_items_write<<<grid_for(nb + 1, 128), 128, 0, s>>>(bin_start, nb, qsub, off, items);
   return 1;
 }
 
