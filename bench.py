@@ -30,10 +30,14 @@ CONFIGS = {
     "c2": (32, 1 << 20, "torus", "mse", "C2: 32^3x13 grid, torus SDF, 2^20 points/step/GPU, MSE"),
     "c3": (32, 1 << 22, "torus", "mse_eikonal", "C3: 32^3x13 grid, torus SDF, 2^22 points/step/GPU, MSE+0.1 Eikonal"),
     "c1": (8, 4096, "sphere", "mse", "C1: 8^3x13 grid, sphere SDF, 4096 points/step"),
+    "c4a": (64, 1 << 24, "torus", "mse",
+            "C4a: 64^3x13 grid, torus SDF, 2^24 points/step in total sharded over the GPUs, MSE"),
     "c5": (32, 1 << 20, "c5", "mse",
            "C5: 8 independent 32^3x13 shapes per GPU (seeded rotated tori/spheres/boxes/CSG), 2^20 points/step per shape, MSE"),
 }
 C5_SHAPES_PER_GPU = 8
+# strong scaling: these configs fix the global batch; each of N ranks takes 1/N of it
+STRONG = {"c4a": 1 << 24}
 SEED = 1234
 POOL = 8                       # distinct batches cycled through; 8 x 16.8 MB > 126 MB L2 at C2
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
@@ -165,6 +169,8 @@ def run_ours(args, rank, world, local_rank):
     from workloads import synth
 
     R, J, shape_name, loss_kind, label = CONFIGS[args.config]
+    if args.config in STRONG:
+        J = STRONG[args.config] // world
     dev = local_rank
     torch.cuda.set_device(dev)
     loss = ef.LOSS_MSE if loss_kind == "mse" else ef.LOSS_MSE_EIKONAL
@@ -368,7 +374,8 @@ def run_ours(args, rank, world, local_rank):
         roof["frac_at_observed_clock"] = achieved / (SM_COUNT * FP32_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
     line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "config": {"workload": label, "R": R, "points_per_step_per_gpu": n_pts,
                        "global_batch": J_global if S == 1 else n_pts * world, "shapes_per_gpu": S,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}" if S == 1 else f"replicas{world}",
