@@ -6,6 +6,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "efunc_internal.cuh"
 
@@ -231,7 +232,7 @@ void free_all(efunc_t* h) {
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
-  dfree(h->scratch);
+  dfree(h->scratch); dfree(h->iota);
   drop_fit_graph(h);
   free_timing(h);
   for (int k = 0; k < 2; ++k) {
@@ -436,6 +437,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.f = a;
   f.gpad = h->gpad;
   f.scratch = h->scratch;
+  f.iota = h->iota;
   const int slot = timing_begin(h, s);
   h->launches += launch_fit(f, h->fwd_items_bound, s);
   timing_end(h, slot, s);
@@ -663,6 +665,12 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->cell_fill, h->n_cells + 1));
     CK(dalloc(&h->ds, 1));
     CK(dalloc(&h->scratch, (size_t)SCRATCH_WARPS * SCRATCH_STRIDE));
+    if (std::isinf(cutoff_log2(h->cfg))) {  // dense mode: the fused kernel's all-keys list
+      std::vector<uint32_t> ids((size_t)h->n_keys);
+      for (size_t i = 0; i < ids.size(); ++i) ids[i] = (uint32_t)i;
+      CK(dalloc(&h->iota, ids.size()));
+      CK(cudaMemcpy(h->iota, ids.data(), ids.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
     h->bg = brick_geom(h->cfg, h->NC, h->h);
     const size_t nbins = (size_t)h->bg.n_codes * h->bg.qsub + 1;
     CK(dalloc(&h->bl_off, h->bg.n_codes));

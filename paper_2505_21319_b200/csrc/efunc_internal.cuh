@@ -157,6 +157,7 @@ struct FitArgs {
   FwdArgs f;
   float* gpad;            // [R^3][16] padded gradient accumulator
   uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
+  const uint32_t* iota;   // dense mode (cutoff_T = inf): 0 .. 2R^3-1, every key a candidate; else null
 };
 
 constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
@@ -274,6 +275,7 @@ struct efunc {
   uint32_t* wl_off = nullptr;       // [items bound]
   uint32_t* wl_n = nullptr;         // [items bound]
   uint32_t* slow_items = nullptr;   // [items bound]
+  uint32_t* iota = nullptr;         // dense mode: key ids 0 .. 2R^3-1 (k_fit candidate list)
   uint32_t* scratch = nullptr;      // per-warp id scratch (k_fit, k_brick_lists): SCRATCH_WARPS x SCRATCH_STRIDE
   int64_t fwd_items_bound = 0;
   float* io_q = nullptr;  // device staging for host_io fit_step

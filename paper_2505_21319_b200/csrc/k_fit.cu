@@ -256,14 +256,15 @@ __device__ __forceinline__ void bwd_sums_x2(const KeyX& KA, const KeyX& KB, cons
   fin(1, KB, sb);
 }
 
-__device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* L) {
+__device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
   const int lane = threadIdx.x & 31;
   const int4 it = A.items[item];
   const int nact = it.y;
+  const bool dense = F.iota != nullptr;  // cutoff_T = inf: every key is a candidate, no lists
   uint32_t nb = BL_OVERFLOW;
-  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (it.z >= 0) nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
   if (nb == BL_OVERFLOW) {  // no brick list (out of domain / overflowed brick): split kernels
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
     return;
@@ -282,11 +283,17 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
   __syncwarp();  // the previous item's readers of L and S are done
   uint32_t wn = 0;
-  stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
-    const uint32_t bal = __ballot_sync(~0u, pass);
-    if (pass) L[wn + __popc(bal & lanemask_lt())] = id;
-    wn += __popc(bal);
-  });
+  const uint32_t* L = Lw;  // the candidate ids the passes read
+  if (dense) {  // all 2R^3 keys in id order (coalesced record loads)
+    L = F.iota;
+    wn = 2u * (uint32_t)kv.n_nodes;
+  } else {
+    stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      if (pass) Lw[wn + __popc(bal & lanemask_lt())] = id;
+      wn += __popc(bal);
+    });
+  }
   // 2. forward
   const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
   const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;  // idle slot: weight 0 (finite: u qq = 0)

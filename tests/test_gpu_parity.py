@@ -576,3 +576,19 @@ def test_c4a_grid_sampled_parity():
     # a few bricks inside dense offset-key clusters exceed the 16384-entry list cap; their items
     # take the enumerate path (exact, slower)
     assert m.stats()["list_overflow"] <= 0.01 * 32 ** 3
+
+
+@pytest.mark.parametrize("R", [8, 16])
+def test_forward_backward_dense_mode_parity(R):
+    """cutoff_T = inf (the paper's dense definition, every pair): the fused kernel walks all 2R^3
+    keys per item; against the oracle's global sums."""
+    tor = synth.Torus()
+    th = synth.fitted_like_theta(R, tor, 101)
+    q, o = synth.sample_batch(tor, 3000, seed=102)
+    m = ef.EFunc(R, th, cutoff_T=float("inf"))
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True)
+    f = orc.forward(th, R, q)
+    Lref, r = orc.mse_loss(f.O, o)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r))
+    assert m.stats()["candidate_pairs"] == 3000 * 2 * R ** 3

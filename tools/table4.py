@@ -1,0 +1,75 @@
+"""Table 4 of the paper on this build: forward and backward time for J = 16384
+queries at I = 4^3 ... 64^3 keys per bank, certified cutoff (T = 20) and dense (T = inf), next to the
+paper's own CUDA numbers (unknown GPU, variant unstated).
+
+  python tools/table4.py [--out profiles/r1_table4.md]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2505_21319_b200 as ef  # noqa: E402
+from workloads import synth  # noqa: E402
+
+PAPER = {4: (0.129, 0.896), 8: (0.185, 1.046), 16: (0.553, 2.321), 32: (3.064, 10.561), 64: (22.576, 82.097)}
+
+
+def timed(fn, reps):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(); fn(); b.record()
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--out", default=None)
+    p.add_argument("--J", type=int, default=16384)
+    a = p.parse_args()
+    tor = synth.Torus()
+    q, o = synth.sample_batch(tor, a.J, seed=7)
+    qd, od = torch.as_tensor(q).cuda(), torch.as_tensor(o).cuda()
+    surf = torch.as_tensor(synth.surface_points(tor, 16384, 8)).cuda()
+    rows = []
+    for R in (4, 8, 16, 32, 64):
+        for T in (20.0, float("inf")):
+            m = ef.EFunc(R, synth.init_theta(R, 9), cutoff_T=T)
+            m.mean_shift_init(surf)
+            grad = torch.zeros(R ** 3, ef.NCH, device="cuda")
+            fwd = lambda: m.forward(qd, od, loss=ef.LOSS_MSE, want_O=True, want_loss=False)  # noqa: E731
+            for _ in range(3):
+                fwd(); m.backward(grad=grad)
+            reps = 20 if R < 64 or T == 20.0 else 5
+            t_f = timed(fwd, reps)
+            fwd()
+            t_b = timed(lambda: m.backward(grad=grad), reps)
+            t_fb = timed(lambda: m.forward_backward(qd, od, grad=grad, want_loss=False), reps)
+            rows.append({"R": R, "T": T, "fwd_ms": t_f, "bwd_ms": t_b, "fused_fwd_bwd_ms": t_fb,
+                         "paper_fwd_ms": PAPER[R][0], "paper_bwd_ms": PAPER[R][1]})
+            print(json.dumps(rows[-1]), flush=True)
+    lines = ["# Table 4 on B200 (J = 16384 queries; torus, paper init + mean-shift offsets)", "",
+             "Paper: PAPER.md:L842-846 (Table 4), their CUDA kernels, GPU/variant unstated, dense global sums. "
+             "Here: the O^{+Delta} variant (2 I keys: I lattice keys + I offset keys), fp32, one B200, median of CUDA-event "
+             "times; forward = efunc_forward (O + MSE upstream), backward = efunc_backward (MSE), fused = "
+             "efunc_forward_backward. T = inf evaluates every pair (the paper's definition); T = 20 is the "
+             "certified cutoff (DESIGN.md R-1).", "",
+             "| I (per bank) | T | fwd ms | bwd ms | fused fwd+bwd ms | paper fwd ms | paper bwd ms | paper / ours (fwd+bwd) |",
+             "|---|---|---|---|---|---|---|---|"]
+    for r in rows:
+        ours = min(r["fwd_ms"] + r["bwd_ms"], r["fused_fwd_bwd_ms"])
+        lines.append(f"| {r['R']}^3 | {r['T']:g} | {r['fwd_ms']:.3f} | {r['bwd_ms']:.3f} | {r['fused_fwd_bwd_ms']:.3f} | "
+                     f"{r['paper_fwd_ms']} | {r['paper_bwd_ms']} | {(r['paper_fwd_ms'] + r['paper_bwd_ms']) / ours:.1f}x |")
+    txt = "\n".join(lines) + "\n"
+    print(txt)
+    if a.out:
+        open(a.out, "w").write(txt)
+
+
+if __name__ == "__main__":
+    main()
