@@ -43,6 +43,7 @@ POOL = 8                       # distinct batches cycled through; 8 x 16.8 MB > 
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
 # algorithmic FP32 lane-ops per kept pair (FFMA = 1 op), DESIGN.md "Roofline"
 OPS_FWD = 12
+OPS_FWD_G = 26  # forward with the spatial gradient G (Eq. func-normal)
 OPS_BWD_GRID, OPS_BWD_OFF = 18, 21
 OPS_BWD_EIK_GRID, OPS_BWD_EIK_OFF = 37, 45
 
@@ -344,14 +345,14 @@ def run_ours(args, rank, world, local_rank):
         return
     # roofline of the dominant kernel: algorithmic lane-ops per launch / its time. k_fit (fused,
     # MSE) does the forward and the backward of every kept pair; k_backward only the backward.
-    fused = loss_kind == "mse" and not args.split
-    kname = "k_fit" if fused else "k_backward"
+    fused = not args.split
+    kname = ("k_fit" if loss_kind == "mse" else "k_fit_eik") if fused else "k_backward"
     if loss_kind == "mse":
         ops = OPS_BWD_GRID * (kept - kept_off) + OPS_BWD_OFF * kept_off
     else:
         ops = OPS_BWD_EIK_GRID * (kept - kept_off) + OPS_BWD_EIK_OFF * kept_off
     if fused:
-        ops += OPS_FWD * kept
+        ops += (OPS_FWD if loss_kind == "mse" else OPS_FWD_G) * kept
     peak = SM_COUNT * FP32_LANES * SM_MAX_MHZ * 1e6 / 1e12
     achieved = ops / (bwd_ms * 1e-3) / 1e12
     traffic = None
@@ -380,7 +381,8 @@ def run_ours(args, rank, world, local_rank):
                        "global_batch": J_global if S == 1 else n_pts * world, "shapes_per_gpu": S,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}" if S == 1 else f"replicas{world}",
                        "launch": "cuda-graph per step" if use_graph else "eager",
-                       "path": "split forward/backward" if (args.split or loss_kind != "mse") else "efunc_forward_backward (fused k_fit for MSE)",
+                       "path": "split forward/backward" if args.split else
+                               f"efunc_forward_backward (fused {'k_fit' if loss_kind == 'mse' else 'k_fit_eik'})",
                        "l2": f"inputs larger than L2: pool of {pool} batches x {n_pts * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:

@@ -417,7 +417,8 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
                                  float* O, float* grad, float* loss_out, cudaStream_t s) {
   if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
   if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "forward_backward needs a loss");
-  const int fused = loss->kind == EFUNC_LOSS_MSE && !h->cfg.deterministic && !h->count_kept;
+  const int eik = loss->kind == EFUNC_LOSS_MSE_EIKONAL;
+  const int fused = !h->cfg.deterministic && !h->count_kept && !(eik && h->iota);  // (dense Eikonal: split)
   if (!fused || J == 0) {
     RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
     RET(do_backward(h, nullptr, nullptr, grad, s));
@@ -430,7 +431,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   if (J > (int64_t)0x7fffffff) return fail(h, EFUNC_EINVAL, "J > 2^31-1 per call");
   h->have_fwd = 0;
   FwdArgs a;
-  RET(prep_queries(h, q, o, J, loss, a, s, 1));
+  RET(prep_queries(h, q, o, J, loss, a, s, eik ? 0 : 1));  // k_fit_eik bounds its own shifts
   a.O = O;
   a.G = nullptr;
   FitArgs f;
@@ -439,12 +440,12 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.scratch = h->scratch;
   f.iota = h->iota;
   const int slot = timing_begin(h, s);
-  h->launches += launch_fit(f, h->fwd_items_bound, s);
+  h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
   timing_end(h, slot, s);
   // items the fused kernel left (no brick list / shift-bound overflow): the split kernels
   h->fwd_J = J;
-  h->launches += launch_forward_slow(a, s);
-  BwdArgs b = bwd_args(h, nullptr, nullptr, grad, 0);
+  h->launches += launch_forward_slow(a, eik, s);
+  BwdArgs b = bwd_args(h, nullptr, nullptr, grad, eik);
   b.list = h->slow_items;
   b.list_n = &h->ds->slow_n;
   h->launches += launch_backward(b, h->fwd_items_bound, s);

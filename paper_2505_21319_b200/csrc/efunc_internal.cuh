@@ -199,9 +199,10 @@ int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, ui
 int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
                        cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
-int launch_forward_slow(const FwdArgs& a, cudaStream_t s);
+int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
+int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
 int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);

@@ -1,0 +1,326 @@
+// k_fit_eik.cu — the fused fit-step kernel for the MSE + Eikonal loss (BASELINE config C3;
+// SURVEY §8(a) S2+S3+S4 with the analytic spatial gradient).
+//
+// The Eikonal upstream h_j = 2 lambda_E (|G_j| - 1) G_j / (|G_j| J) (reading R-12) depends on query
+// j alone, like the MSE upstream, so a work item's forward (O_j and G_j, Eq. func-normal
+// PAPER.md:L425-436), losses and backward (Alg. 2 plus the second-order terms)
+// run in one kernel per item:
+//   1. shift bound, box, brick-list stream + test -> candidate ids in the warp's scratch;
+//   2. forward, lanes = queries (each lane owns one query and its 11 running sums), the round's
+//      32 candidate keys staged in shared memory as packed pairs and walked two keys per f32x2
+//      instruction;
+//   3. O_j, G_j, u_j, losses, r_j, h_j, h.u_j, h.G_j -> the item's query table in shared memory;
+//   4. backward, lanes = candidate keys (two per lane), the item's queries broadcast as packed
+//      pairs, 14 accumulators per key, three red.global.add.v4 per (key, item).
+// Items without a brick list or whose shift bound overflowed go to the split kernels.
+#include <algorithm>
+
+#include "k_pair.cuh"
+
+namespace ef {
+
+#ifndef FE_MIN_WARPS
+#define FE_MIN_WARPS 16  // warps per SM
+#endif
+constexpr int FE_WARPS = 4;
+constexpr int FE_BLOCKS = 148 * (FE_MIN_WARPS / FE_WARPS);
+static_assert(FE_BLOCKS * FE_WARPS <= SCRATCH_WARPS, "one scratch slot per warp");
+
+struct EikSmem {
+  // forward: the round's keys as pairs {x0,x1,y0,y1}, {z0,z1,bl0,bl1}, {c0,c1,gx0,gx1}, {gy0,gy1,gz0,gz1}
+  float kA[QW / 2][4], kB[QW / 2][4], kC[QW / 2][4], kD[QW / 2][4];
+  // backward: the item's queries as pairs {x,y}, {z,w}, {r+hu, O}, {hx,hy}, {hz, T}
+  float4 pA[QW / 2], pB[QW / 2], pC[QW / 2], pD[QW / 2], pE[QW / 2];
+};
+
+// forward sums of one query (lane) over the staged keys
+struct EikFwd {
+  float2 Z, M, sgx, sgy, sgz, sux, suy, suz, sfx, sfy, sfz;
+};
+
+__device__ __forceinline__ void eik_fwd_round(const EikSmem& S, const int npk, const float2 qx, const float2 qy,
+                                              const float2 qz, const float2 sh, const float2 f0,
+                                              const float2 g0x, const float2 g0y, const float2 g0z, EikFwd& a) {
+#pragma unroll 2
+  for (int p = 0; p < npk; ++p) {
+    const float4 A = *reinterpret_cast<const float4*>(S.kA[p]);
+    const float4 B = *reinterpret_cast<const float4*>(S.kB[p]);
+    const float4 C = *reinterpret_cast<const float4*>(S.kC[p]);
+    const float4 D = *reinterpret_cast<const float4*>(S.kD[p]);
+    const float2 dx = __fadd2_rn(qx, make_float2(-A.x, -A.y));
+    const float2 dy = __fadd2_rn(qy, make_float2(-A.z, -A.w));
+    const float2 dz = __fadd2_rn(qz, make_float2(-B.x, -B.y));
+    float2 dd = __fmul2_rn(dz, dz);
+    dd = __ffma2_rn(dy, dy, dd);
+    dd = __ffma2_rn(dx, dx, dd);
+    const float2 bl = make_float2(B.z, B.w);
+    const float2 e = __ffma2_rn(make_float2(-B.z, -B.w), dd, sh);
+    const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
+    // f - f0 and g - g0: the shift key's value (accuracy of G)
+    float2 f = __ffma2_rn(make_float2(C.z, C.w), dx, __fadd2_rn(make_float2(C.x, C.y), f0));
+    f = __ffma2_rn(make_float2(D.x, D.y), dy, f);
+    f = __ffma2_rn(make_float2(D.z, D.w), dz, f);
+    a.Z = __fadd2_rn(a.Z, w);
+    a.M = __ffma2_rn(w, f, a.M);
+    a.sgx = __ffma2_rn(w, __fadd2_rn(make_float2(C.z, C.w), g0x), a.sgx);
+    a.sgy = __ffma2_rn(w, __fadd2_rn(make_float2(D.x, D.y), g0y), a.sgy);
+    a.sgz = __ffma2_rn(w, __fadd2_rn(make_float2(D.z, D.w), g0z), a.sgz);
+    const float2 wbl = __fmul2_rn(w, bl);
+    a.sux = __ffma2_rn(wbl, dx, a.sux);
+    a.suy = __ffma2_rn(wbl, dy, a.suy);
+    a.suz = __ffma2_rn(wbl, dz, a.suz);
+    const float2 wbf = __fmul2_rn(wbl, f);
+    a.sfx = __ffma2_rn(wbf, dx, a.sfx);
+    a.sfy = __ffma2_rn(wbf, dy, a.sfy);
+    a.sfz = __ffma2_rn(wbf, dz, a.sfz);
+  }
+}
+
+// backward sums of one key over the item's query pairs (MSE + Eikonal second-order terms)
+struct EikBwd {
+  float2 sc, sgx, sgy, sgz, phx, phy, phz, ss, sdx, sdy, sdz, pdx, pdy, pdz;
+};
+
+__device__ __forceinline__ void eik_bwd_pair(const float4 a, const float4 b, const float beta2,
+                                             const float4 QA, const float4 QB, const float4 QC,
+                                             const float4 QD, const float4 QE, EikBwd& s) {
+  const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), make_float2(-a.x, -a.x));
+  const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), make_float2(-a.y, -a.y));
+  const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), make_float2(-a.z, -a.z));
+  float2 dd = __fmul2_rn(dz, dz);
+  dd = __ffma2_rn(dy, dy, dd);
+  dd = __ffma2_rn(dx, dx, dd);
+  const float2 p = [&] {
+    const float2 e = __ffma2_rn(make_float2(-a.w, -a.w), dd, make_float2(QB.z, QB.w));
+    return make_float2(ex2f(e.x), ex2f(e.y));
+  }();
+  float2 f = __ffma2_rn(make_float2(b.y, b.y), dx, make_float2(b.x, b.x));
+  f = __ffma2_rn(make_float2(b.z, b.z), dy, f);
+  f = __ffma2_rn(make_float2(b.w, b.w), dz, f);
+  const float2 hx = make_float2(QD.x, QD.y), hy = make_float2(QD.z, QD.w), hz = make_float2(QE.x, QE.y);
+  const float2 del = __fadd2_rn(f, make_float2(-QC.z, -QC.w));                       // f - O
+  float2 hd = __fmul2_rn(hz, dz);
+  hd = __ffma2_rn(hy, dy, hd);
+  hd = __ffma2_rn(hx, dx, hd);
+  const float2 hu = __fmul2_rn(make_float2(beta2, beta2), hd);                        // 2 beta h.d
+  float2 hg = __fmul2_rn(hz, make_float2(b.w, b.w));
+  hg = __ffma2_rn(hy, make_float2(b.z, b.z), hg);
+  hg = __ffma2_rn(hx, make_float2(b.y, b.y), hg);                                     // h.g
+  const float2 rh = make_float2(QC.x, QC.y);                                          // r + h.u
+  const float2 alpha = __fadd2_rn(rh, make_float2(-hu.x, -hu.y));
+  const float2 tt = __ffma2_rn(make_float2(-hu.x, -hu.y), del, hg);
+  const float2 gam = __ffma2_rn(rh, del, __fadd2_rn(tt, make_float2(-QE.z, -QE.w)));  // - h.G
+  const float2 pa = __fmul2_rn(p, alpha);
+  s.sc = __fadd2_rn(s.sc, pa);
+  s.sgx = __ffma2_rn(pa, dx, s.sgx);
+  s.sgy = __ffma2_rn(pa, dy, s.sgy);
+  s.sgz = __ffma2_rn(pa, dz, s.sgz);
+  s.phx = __ffma2_rn(p, hx, s.phx);
+  s.phy = __ffma2_rn(p, hy, s.phy);
+  s.phz = __ffma2_rn(p, hz, s.phz);
+  // ss: p (beta dd gam + hu del), beta = beta2 / 2
+  const float2 bdd = __fmul2_rn(make_float2(0.5f * beta2, 0.5f * beta2), dd);
+  s.ss = __ffma2_rn(p, __ffma2_rn(bdd, gam, __fmul2_rn(hu, del)), s.ss);
+  const float2 pg = __fmul2_rn(p, gam);
+  s.sdx = __ffma2_rn(pg, dx, s.sdx);
+  s.sdy = __ffma2_rn(pg, dy, s.sdy);
+  s.sdz = __ffma2_rn(pg, dz, s.sdz);
+  const float2 pdel = __fmul2_rn(p, del);
+  s.pdx = __ffma2_rn(pdel, hx, s.pdx);
+  s.pdy = __ffma2_rn(pdel, hy, s.pdy);
+  s.pdz = __ffma2_rn(pdel, hz, s.pdz);
+}
+
+__device__ __forceinline__ float hsum(const float2 v) { return v.x + v.y; }
+
+// one key's gradients into the padded accumulator (k_backward's EIK channel map)
+__device__ __forceinline__ void eik_red(const EikBwd& s, const float4 a, const float4 b, const int id,
+                                        const int n_nodes, float* gpad) {
+  const float beta = a.w * EF_LN2;
+  const float sc = hsum(s.sc);
+  const float dsv = -hsum(s.ss);
+  const float dgx = hsum(s.sgx) + hsum(s.phx), dgy = hsum(s.sgy) + hsum(s.phy), dgz = hsum(s.sgz) + hsum(s.phz);
+  if (id < n_nodes) {
+    float* gp = gpad + (size_t)id * 16;
+    red_v4(gp, dsv, sc, dgx, dgy);
+    atomicAdd(gp + 4, dgz);
+  } else {
+    const float dkx = fmaf(-b.y, sc, 2.0f * beta * (hsum(s.sdx) + hsum(s.pdx)));
+    const float dky = fmaf(-b.z, sc, 2.0f * beta * (hsum(s.sdy) + hsum(s.pdy)));
+    const float dkz = fmaf(-b.w, sc, 2.0f * beta * (hsum(s.sdz) + hsum(s.pdz)));
+    float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
+    red_v4(gp, dkx, dky, dkz, dsv);
+    red_v4(gp + 4, sc, dgx, dgy, dgz);
+  }
+}
+
+__device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, EikSmem& S, uint32_t* L) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  uint32_t nb = BL_OVERFLOW;
+  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (nb == BL_OVERFLOW) {
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  // 1. shift bound (and the shift key's f0, g0), box, candidates
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY, f0 = 0.f;
+  float3 g0 = make_float3(0.f, 0.f, 0.f);
+  if (act) {
+    q = A.qs[js];
+    shift_bound(kv, q, mh, f0, g0);
+  }
+  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  box.thr += A.T_l;
+  __syncwarp();  // the previous item's readers of L and S are done
+  uint32_t wn = 0;
+  stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) L[wn + __popc(bal & lanemask_lt())] = id;
+    wn += __popc(bal);
+  });
+  __syncwarp();
+  // 2. forward, lanes = queries
+  EikFwd fa;
+  fa.Z = fa.M = fa.sgx = fa.sgy = fa.sgz = fa.sux = fa.suy = fa.suz = fa.sfx = fa.sfy = fa.sfz = make_float2(0.f, 0.f);
+  {
+    const float sh = act ? mh : -INFINITY;
+    const float2 qx = make_float2(q.x, q.x), qy = make_float2(q.y, q.y), qz = make_float2(q.z, q.z);
+    const float2 sh2 = make_float2(sh, sh), nf0 = make_float2(-f0, -f0);
+    const float2 ng0x = make_float2(-g0.x, -g0.x), ng0y = make_float2(-g0.y, -g0.y), ng0z = make_float2(-g0.z, -g0.z);
+    const int hi = lane & 1, slot = lane >> 1;
+    for (uint32_t base = 0; base < wn; base += 32) {
+      const uint32_t k = base + lane;
+      float4 a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b = make_float4(0.f, 0.f, 0.f, 0.f);  // far: weight 0
+      if (k < wn) {
+        const uint32_t id = L[k];
+        a = __ldg(&kv.grid_raw[2 * id]);
+        b = __ldg(&kv.grid_raw[2 * id + 1]);
+      }
+      __syncwarp();  // the previous round's readers are done
+      S.kA[slot][hi] = a.x; S.kA[slot][2 + hi] = a.y;
+      S.kB[slot][hi] = a.z; S.kB[slot][2 + hi] = a.w;
+      S.kC[slot][hi] = b.x; S.kC[slot][2 + hi] = b.y;
+      S.kD[slot][hi] = b.z; S.kD[slot][2 + hi] = b.w;
+      __syncwarp();
+      const int npk = ((int)min(wn - base, 32u) + 1) >> 1;
+      eik_fwd_round(S, npk, qx, qy, qz, sh2, nf0, ng0x, ng0y, ng0z, fa);
+    }
+  }
+  const float Z = hsum(fa.Z), M = hsum(fa.M);
+  const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
+  if (__any_sync(~0u, bad)) {
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  // 3. O, G, u, losses and upstreams (Eq. func-normal; Eq. loss; reading R-12)
+  float lossj = 0.f;
+  float4 PA = make_float4(0.f, 0.f, 0.f, 0.f);
+  float rh = 0.f, Oj = 0.f, hx = 0.f, hy = 0.f, hz = 0.f, Tj = 0.f, nlam = -INFINITY;
+  if (act) {
+    const float iz = 1.0f / Z;
+    Oj = f0 + M * iz;
+    nlam = mh - log2f(Z);
+    const float c2 = 2.0f * EF_LN2 * iz;
+    const float Of = Oj - f0;
+    const float Gx = g0.x + (hsum(fa.sgx) * iz + c2 * fmaf(Of, hsum(fa.sux), -hsum(fa.sfx)));
+    const float Gy = g0.y + (hsum(fa.sgy) * iz + c2 * fmaf(Of, hsum(fa.suy), -hsum(fa.sfy)));
+    const float Gz = g0.z + (hsum(fa.sgz) * iz + c2 * fmaf(Of, hsum(fa.suz), -hsum(fa.sfz)));
+    const float ux = c2 * hsum(fa.sux), uy = c2 * hsum(fa.suy), uz = c2 * hsum(fa.suz);
+    const float diff = Oj - q.w;
+    const float r = 2.0f * diff * A.inv_J;
+    lossj = diff * diff * A.inv_J;
+    const float nrm = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
+    lossj = fmaf(A.eik_lambda * (nrm - 1.0f) * (nrm - 1.0f), A.inv_J, lossj);
+    const float sc = nrm > 0.0f ? 2.0f * A.eik_lambda * (nrm - 1.0f) / nrm * A.inv_J : 0.0f;
+    hx = sc * Gx; hy = sc * Gy; hz = sc * Gz;
+    rh = r + (hx * ux + hy * uy + hz * uz);
+    Tj = hx * Gx + hy * Gy + hz * Gz;
+    const int ju = A.perm[js];
+    if (A.O) A.O[ju] = Oj;
+    if (A.G) {
+      A.G[3 * (size_t)ju] = Gx;
+      A.G[3 * (size_t)ju + 1] = Gy;
+      A.G[3 * (size_t)ju + 2] = Gz;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
+  if (lane == 0) {
+    A.loss_part[item] = lossj;
+    atomicAdd(&A.ds->cand_pairs, (unsigned long long)wn * (unsigned long long)nact);
+  }
+  // the item's query table as packed pairs (an idle slot: w = -inf, all upstreams 0)
+  {
+    auto pk = [&](float v, float4& dst, bool second) {
+      const float o = __shfl_xor_sync(~0u, v, 1);
+      if ((lane & 1) == 0) {
+        if (!second) { dst.x = v; dst.y = o; } else { dst.z = v; dst.w = o; }
+      }
+    };
+    const int sl = lane >> 1;
+    pk(q.x, S.pA[sl], false); pk(q.y, S.pA[sl], true);
+    pk(q.z, S.pB[sl], false); pk(nlam, S.pB[sl], true);
+    pk(rh, S.pC[sl], false); pk(Oj, S.pC[sl], true);
+    pk(hx, S.pD[sl], false); pk(hy, S.pD[sl], true);
+    pk(hz, S.pE[sl], false); pk(Tj, S.pE[sl], true);
+  }
+  __syncwarp();
+  // 4. backward, lanes = keys (two per lane)
+  const int np2 = (((nact + 1) >> 1) + 1) & ~1;  // even (padding slots are idle queries)
+  for (uint32_t base = 0; base < wn; base += 64) {
+    const uint32_t k0 = base + lane, k1 = base + 32 + lane;
+    const bool h0 = k0 < wn, h1 = k1 < wn;
+    uint32_t id0 = 0, id1 = 0;
+    float4 a0 = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b1 = b0;
+    if (h0) {
+      id0 = L[k0];
+      a0 = __ldg(&kv.grid_raw[2 * id0]);
+      b0 = __ldg(&kv.grid_raw[2 * id0 + 1]);
+    }
+    if (h1) {
+      id1 = L[k1];
+      a1 = __ldg(&kv.grid_raw[2 * id1]);
+      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+    }
+    const float beta20 = 2.0f * a0.w * EF_LN2, beta21 = 2.0f * a1.w * EF_LN2;
+    EikBwd s0, s1;
+    s0.sc = s0.sgx = s0.sgy = s0.sgz = s0.phx = s0.phy = s0.phz = s0.ss = s0.sdx = s0.sdy = s0.sdz = s0.pdx =
+        s0.pdy = s0.pdz = make_float2(0.f, 0.f);
+    s1 = s0;
+    const bool two = base + 32 < wn;  // warp-uniform
+#pragma unroll 1
+    for (int jp = 0; jp < np2; ++jp) {
+      const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+      eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
+      if (two) eik_bwd_pair(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
+    }
+    if (h0) eik_red(s0, a0, b0, (int)id0, kv.n_nodes, F.gpad);
+    if (h1) eik_red(s1, a1, b1, (int)id1, kv.n_nodes, F.gpad);
+  }
+}
+
+__global__ void __launch_bounds__(32 * FE_WARPS, FE_MIN_WARPS / FE_WARPS) k_fit_eik(const FitArgs F) {
+  __shared__ EikSmem smem[FE_WARPS];
+  const int w = threadIdx.x >> 5;
+  uint32_t* L = F.scratch + (size_t)(blockIdx.x * FE_WARPS + w) * SCRATCH_STRIDE;
+  for (;;) {
+    const int64_t item = fetch_item(&F.f.ds->fit_next, F.f.n_items, nullptr, nullptr);
+    if (item < 0) break;
+    eik_item(F, (uint32_t)item, smem[w], L);
+  }
+}
+
+int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n_items + FE_WARPS - 1) / FE_WARPS, FE_BLOCKS);
+  k_fit_eik<<<blocks, 32 * FE_WARPS, 0, s>>>(a);
+  return 1;
+}
+
+}  // namespace ef

@@ -411,8 +411,10 @@ int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const fl
   return 1;
 }
 
-int launch_forward_slow(const FwdArgs& a, cudaStream_t s) {
-  k_forward<false><<<148 * 4, NTHREADS, 0, s>>>(a, 1);  // the items in a.slow_items (usually none)
+int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s) {
+  // the items in a.slow_items (usually none)
+  if (want_g) k_forward<true><<<148 * 4, NTHREADS, 0, s>>>(a, 1);
+  else k_forward<false><<<148 * 4, NTHREADS, 0, s>>>(a, 1);
   return 1;
 }
 

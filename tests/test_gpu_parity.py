@@ -592,3 +592,55 @@ def test_forward_backward_dense_mode_parity(R):
     assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
     check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r))
     assert m.stats()["candidate_pairs"] == 3000 * 2 * R ** 3
+
+
+# ----------------------------------------------------------------------------- fused Eikonal (C3)
+@pytest.mark.parametrize("J", [33, 4096])
+def test_forward_backward_eikonal_fused_parity(J):
+    """k_fit_eik (forward with G, MSE + Eikonal upstreams, second-order backward per item)
+    against the oracle: O, G and the loss, and all 13 gradient channels."""
+    th, q, o = c1_case(seed=111, J=4096)
+    if J < 4096:
+        th = synth.random_theta(8, 112)
+    q, o = q[:J], o[:J]
+    m = ef.EFunc(8, th)
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1, want_O=True)
+    f = orc.forward(th, 8, q)
+    Lm, r = orc.mse_loss(f.O, o)
+    Le, h = orc.eikonal_loss(f.G, 0.1)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    assert abs(float(L.item()) - (Lm + Le)) <= 1e-5 * (Lm + Le) + 2e-5 * np.abs(f.O - o).mean() * np.abs(f.O).max()
+    check_grads(g.cpu().numpy(), orc.backward(th, 8, q, f, r, h), floor=1e-6)
+
+
+def test_forward_backward_eikonal_fused_slow_paths():
+    R = 8
+    th = synth.random_theta(R, 113, log_scale_mean=7.5, log_scale_std=1.5)
+    rg = synth.rng(114)
+    q = np.concatenate([rg.uniform(-1, 1, size=(2500, 3)), rg.uniform(-1.6, 1.6, size=(500, 3))]).astype(np.float32)
+    o = rg.normal(scale=0.2, size=3000).astype(np.float32)
+    m = ef.EFunc(R, th)
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1, want_O=True)
+    f = orc.forward(th, R, q)
+    _, r = orc.mse_loss(f.O, o)
+    _, h = orc.eikonal_loss(f.G, 0.1)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r, h), floor=1e-6)
+
+
+def test_forward_backward_eikonal_fused_matches_split_c3():
+    """C3 geometry at full size (2^22 torus points): fused vs split (forward with G + Eikonal
+    backward) agree to 1e-5 per channel."""
+    R, J = 32, 1 << 22
+    tor = synth.Torus()
+    m = ef.EFunc(R, synth.init_theta(R, 115))
+    m.mean_shift_init(dev(synth.surface_points(tor, 16384, seed=116)))
+    q, o = synth.sample_batch(tor, J, seed=117)
+    qd, od = dev(q), dev(o)
+    g1, _, L1 = m.forward_backward(qd, od, loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1)
+    _, _, L2 = m.forward(qd, od, loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1, want_G=True)
+    g2 = m.backward().cpu().numpy()
+    g1 = g1.cpu().numpy()
+    for ch in range(13):
+        assert nw(g1[:, ch], g2[:, ch]) <= 1e-5, ch
+    assert abs(float(L1.item()) - float(L2.item())) <= 1e-6 * float(L2.item())
