@@ -293,12 +293,19 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     s0.sc = s0.sgx = s0.sgy = s0.sgz = s0.phx = s0.phy = s0.phz = s0.ss = s0.sdx = s0.sdy = s0.sdz = s0.pdx =
         s0.pdy = s0.pdz = make_float2(0.f, 0.f);
     s1 = s0;
-    const bool two = base + 32 < wn;  // warp-uniform
+    if (base + 32 < wn) {  // warp-uniform: two keys per lane
 #pragma unroll 1
-    for (int jp = 0; jp < np2; ++jp) {
-      const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
-      eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
-      if (two) eik_bwd_pair(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
+      for (int jp = 0; jp < np2; ++jp) {
+        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+        eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
+        eik_bwd_pair(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
+      }
+    } else {
+#pragma unroll 2
+      for (int jp = 0; jp < np2; ++jp) {
+        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+        eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
+      }
     }
     if (h0) eik_red(s0, a0, b0, (int)id0, kv.n_nodes, F.gpad);
     if (h1) eik_red(s1, a1, b1, (int)id1, kv.n_nodes, F.gpad);

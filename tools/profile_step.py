@@ -14,6 +14,7 @@ p.add_argument("--steps", type=int, default=3)
 p.add_argument("--R", type=int, default=32)
 p.add_argument("--J", type=int, default=1 << 20)
 p.add_argument("--eikonal", action="store_true")
+p.add_argument("--split", action="store_true", help="forward + backward instead of forward_backward")
 a = p.parse_args()
 tor = synth.Torus()
 m = ef.EFunc(a.R, synth.init_theta(a.R, 1234))
@@ -24,8 +25,11 @@ grad = torch.zeros(a.R ** 3, 13, device="cuda")
 loss = ef.LOSS_MSE_EIKONAL if a.eikonal else ef.LOSS_MSE
 for s in range(a.steps):
     grad.zero_()
-    m.forward(qd, od, loss=loss, want_O=False, want_loss=False)
-    m.backward(grad=grad)
+    if a.split:
+        m.forward(qd, od, loss=loss, want_O=False, want_loss=False)
+        m.backward(grad=grad)
+    else:
+        m.forward_backward(qd, od, loss=loss, grad=grad, want_loss=False)
     m.adamw_step(grad)
 torch.cuda.synchronize()
 print("done", m.stats())
