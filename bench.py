@@ -398,13 +398,22 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # EFUNC_BENCH_SHARED_GPU=1 (code-path check only, not a measurement): every rank on the GPUs
+    # that exist (ranks share them) and gloo for the collectives (NCCL refuses a shared GPU)
+    shared = os.environ.get("EFUNC_BENCH_SHARED_GPU") == "1"
+    dev = local_rank
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if shared:
+            dev = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(dev)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, rank, world, dev)
     finally:
         if world > 1:
             import torch.distributed as dist
