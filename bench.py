@@ -32,12 +32,14 @@ CONFIGS = {
     "c1": (8, 4096, "sphere", "mse", "C1: 8^3x13 grid, sphere SDF, 4096 points/step"),
     "c4a": (64, 1 << 24, "torus", "mse",
             "C4a: 64^3x13 grid, torus SDF, 2^24 points/step in total sharded over the GPUs, MSE"),
+    "c4b": (128, 1 << 24, "torus", "mse",
+            "C4b: 128^3x13 grid, torus SDF, 2^24 points/step in total sharded over the GPUs, MSE"),
     "c5": (32, 1 << 20, "c5", "mse",
            "C5: 8 independent 32^3x13 shapes per GPU (seeded rotated tori/spheres/boxes/CSG), 2^20 points/step per shape, MSE"),
 }
 C5_SHAPES_PER_GPU = 8
 # strong scaling: these configs fix the global batch; each of N ranks takes 1/N of it
-STRONG = {"c4a": 1 << 24}
+STRONG = {"c4a": 1 << 24, "c4b": 1 << 24}
 SEED = 1234
 POOL = 8                       # distinct batches cycled through; 8 x 16.8 MB > 126 MB L2 at C2
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0

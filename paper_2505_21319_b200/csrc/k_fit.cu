@@ -84,17 +84,11 @@ __device__ __forceinline__ KeyX key_x(const float4 a, const float4 b, const floa
 // every lane walks the item's query pairs; Z, M per query pair in registers; one transpose-
 // reduction per item returns Z_j, M_j to lane j. NPM = query pairs held (8: <= 16 queries).
 template <int NPM>
-__device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
-                                           const int nact, const float3 o, const float4* sQA,
-                                           const float4* sQB, float& Zj, float& Mj) {
+__device__ __forceinline__ void fwd_accum_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
+                                            const int nact, const float3 o, const float4* sQA,
+                                            const float4* sQB, float2 (&Z)[NPM], float2 (&M)[NPM]) {
   const int lane = threadIdx.x & 31;
   const int npairs = (nact + 1) >> 1;
-  float2 Z[NPM], M[NPM];
-#pragma unroll
-  for (int pp = 0; pp < NPM; ++pp) {
-    Z[pp] = make_float2(0.f, 0.f);
-    M[pp] = make_float2(0.f, 0.f);
-  }
   auto round = [&](const KeyX& K) {
 #define FX_PAIR(pp)                                  \
   {                                                  \
@@ -136,7 +130,12 @@ __device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L
     }
     round(key_x(ka, kb, o));
   }
-  // transpose-reduce {Zx, Zy, Mx, My} of every pair; lane j then fetches its query's totals
+}
+
+// transpose-reduce {Zx, Zy, Mx, My} of every pair; lane j then fetches its query's totals
+template <int NPM>
+__device__ __forceinline__ void fwd_reduce_x(const float2 (&Z)[NPM], const float2 (&M)[NPM], float& Zj, float& Mj) {
+  const int lane = threadIdx.x & 31;
   if (NPM == 8) {
     float v[32];
 #pragma unroll
@@ -160,6 +159,20 @@ __device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L
     Zj = (lane & 1) ? z1 : z0;
     Mj = (lane & 1) ? m1 : m0;
   }
+}
+
+template <int NPM>
+__device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
+                                           const int nact, const float3 o, const float4* sQA,
+                                           const float4* sQB, float& Zj, float& Mj) {
+  float2 Z[NPM], M[NPM];
+#pragma unroll
+  for (int pp = 0; pp < NPM; ++pp) {
+    Z[pp] = make_float2(0.f, 0.f);
+    M[pp] = make_float2(0.f, 0.f);
+  }
+  fwd_accum_x<NPM>(kv, L, wn, nact, o, sQA, sQB, Z, M);
+  fwd_reduce_x<NPM>(Z, M, Zj, Mj);
 }
 
 // Backward sums of one key (lane) over the item's query pairs in q' coordinates, mapped to the
@@ -256,6 +269,198 @@ __device__ __forceinline__ void bwd_sums_x2(const KeyX& KA, const KeyX& KB, cons
   fin(1, KB, sb);
 }
 
+// The backward over candidate ids L[0 .. wn) (rounds of 64: two keys per lane), the item's query
+// table in S (qa, qb: positions; pc: rho, -O).
+__device__ __forceinline__ void bwd_pass_x(const FitArgs& F, const uint32_t* L, const uint32_t wn,
+                                           const int npairs, const float3 o, FitSmem& S) {
+  const KeysView& kv = F.f.kv;
+  const int lane = threadIdx.x & 31;
+#if FT_BWD2
+  // rounds of 64 candidates: lane keys base + lane and base + 32 + lane (records one round ahead;
+  // a missing second key is a far zero key whose sums are discarded)
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t iA = ((uint32_t)lane < wn) ? L[lane] : 0u, iB = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 aA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA]) : far_a;
+  float4 bA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA + 1]) : z4;
+  float4 aB = ((uint32_t)lane + 32 < wn) ? __ldg(&kv.grid_raw[2 * iB]) : far_a;
+  float4 bB = ((uint32_t)lane + 32 < wn) ? __ldg(&kv.grid_raw[2 * iB + 1]) : z4;
+  for (uint32_t base = 0; base < wn; base += 64) {
+    const uint32_t k = base + lane;
+    const uint32_t idA = iA, idB = iB;
+    const float4 a0 = aA, b0 = bA, a1 = aB, b1 = bB;
+    iA = (k + 64 < wn) ? L[k + 64] : 0u;
+    iB = (k + 96 < wn) ? L[k + 96] : 0u;
+    aA = far_a; bA = z4; aB = far_a; bB = z4;
+    if (k + 64 < wn) {
+      aA = __ldg(&kv.grid_raw[2 * iA]);
+      bA = __ldg(&kv.grid_raw[2 * iA + 1]);
+    }
+    if (k + 96 < wn) {
+      aB = __ldg(&kv.grid_raw[2 * iB]);
+      bB = __ldg(&kv.grid_raw[2 * iB + 1]);
+    }
+    if (base + 32 < wn) {  // warp-uniform: two keys per lane
+      MseSums s0, s1;
+      bwd_sums_x2(key_x(a0, b0, o), key_x(a1, b1, o), npairs, S.qa, S.qb, S.pc, s0, s1);
+      if (k < wn) bwd_mse_red(s0, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+      if (k + 32 < wn) bwd_mse_red(s1, a1, b1, (int)idB, kv.n_nodes, F.gpad);
+    } else if (k < wn) {
+      const MseSums ms = bwd_sums_x(key_x(a0, b0, o), npairs, S.qa, S.qb, S.pc);
+      bwd_mse_red(ms, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+    }
+  }
+#else
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
+  uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 a1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1]) : z4;
+  float4 b1 = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * id1 + 1]) : z4;
+  for (uint32_t base = 0; base < wn; base += 32) {
+    const uint32_t k = base + lane;
+    const uint32_t id = id1;
+    const float4 a = a1, b = b1;
+    id1 = id2;
+    id2 = (k + 64 < wn) ? L[k + 64] : 0u;
+    if (k + 32 < wn) {
+      a1 = __ldg(&kv.grid_raw[2 * id1]);
+      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+    }
+    if (k < wn) {
+      const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
+      bwd_mse_red(ms, a, b, (int)id, kv.n_nodes, F.gpad);
+    }
+  }
+#endif
+}
+
+// Items of overflowed bricks (C4b at 128^3: ~35k keys per brick).
+__device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool dense = F.iota != nullptr;  // cutoff_T = inf: every key is a candidate, no lists
+  if (it.z < 0) {  // out-of-domain queries: the split kernels
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  const uint32_t nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
+  // an overflowed brick (no list): candidates by direct enumeration of the lattice cells around
+  // the item, in chunks of BL_CAP ids (each chunk re-enumerates: cheap next to its pair work)
+  const bool enum_mode = !dense && nb == BL_OVERFLOW;
+  // 1. box, candidate ids
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY;
+  if (act) {
+    q = A.qs[js];
+    mh = A.qmh[js];  // shift bound from k_gather_queries_mh
+  }
+  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  box.thr += A.T_l;
+  const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
+  __syncwarp();  // the previous item's readers of L and S are done
+  uint32_t total = 0;  // candidates of the item (all chunks)
+  const uint32_t* L = Lw;  // the candidate ids the passes read
+  // builds chunk c of the candidate ids into Lw (or points L at them); returns its length
+  auto build = [&](const uint32_t c) -> uint32_t {
+    if (dense) {  // all 2R^3 keys in id order (coalesced record loads)
+      L = F.iota;
+      total = 2u * (uint32_t)kv.n_nodes;
+      return total;
+    }
+    uint32_t cnt = 0;
+    if (!enum_mode) {
+      stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
+        const uint32_t bal = __ballot_sync(~0u, pass);
+        if (pass) Lw[cnt + __popc(bal & lanemask_lt())] = id;
+        cnt += __popc(bal);
+      });
+      total = cnt;
+      return cnt;
+    }
+    const uint32_t lo = c * (uint32_t)BL_CAP;
+    enumerate(kv, box, [&](bool pass, uint32_t kp, float4) {
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      const uint32_t idx = cnt + __popc(bal & lanemask_lt());
+      if (pass && idx >= lo && idx < lo + (uint32_t)BL_CAP) Lw[idx - lo] = (uint32_t)__ldg(&kv.kid[kp]);
+      cnt += __popc(bal);
+    });
+    total = cnt;
+    return cnt > lo ? min(cnt - lo, (uint32_t)BL_CAP) : 0u;
+  };
+  // 2. forward
+  const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
+  const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;  // idle slot: weight 0 (finite: u qq = 0)
+  {
+    const float xo = __shfl_xor_sync(~0u, qx, 1), yo = __shfl_xor_sync(~0u, qy, 1);
+    const float zo = __shfl_xor_sync(~0u, qz, 1), qo = __shfl_xor_sync(~0u, qq, 1);
+    if ((lane & 1) == 0) {
+      S.qa[lane >> 1] = make_float4(qx, xo, qy, yo);
+      S.qb[lane >> 1] = make_float4(qz, zo, qq, qo);
+    }
+  }
+  uint32_t wn = build(0);
+  __syncwarp();
+  float Z, M;
+  if (!enum_mode) {
+    if (IQ <= 16 || nact <= 16) fwd_sums_x<8>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+    else fwd_sums_x<(IQ > 16 ? 16 : 8)>(kv, L, wn, nact, o, S.qa, S.qb, Z, M);
+  } else {
+    float2 Za[16], Ma[16];
+#pragma unroll
+    for (int pp = 0; pp < 16; ++pp) Za[pp] = Ma[pp] = make_float2(0.f, 0.f);
+    for (uint32_t c = 0;; ++c) {
+      if (c > 0) {
+        __syncwarp();  // readers of the previous chunk are done
+        wn = build(c);
+        __syncwarp();
+      }
+      fwd_accum_x<16>(kv, L, wn, nact, o, S.qa, S.qb, Za, Ma);
+      if ((c + 1) * (uint32_t)BL_CAP >= total) break;
+    }
+    fwd_reduce_x<16>(Za, Ma, Z, M);
+  }
+  const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
+  if (__any_sync(~0u, bad)) {  // Z underflow (far queries): the split kernels shift exactly
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  float O = 0.f, rho = 0.f, lossj = 0.f;
+  if (act) {
+    const float iz = 1.0f / Z;
+    O = M * iz;
+    const float diff = O - q.w;
+    const float r = 2.0f * diff * A.inv_J;
+    rho = r * iz;  // t_ij = r_j p_ij = (r_j / Z_j) 2^(-a_ij log2 e)
+    lossj = diff * diff * A.inv_J;
+    if (A.O) A.O[A.perm[js]] = O;
+  }
+  for (int s = 16; s > 0; s >>= 1) lossj += __shfl_xor_sync(~0u, lossj, s);
+  if (lane == 0) {
+    A.loss_part[item] = lossj;
+    atomicAdd(&A.ds->cand_pairs, (unsigned long long)total * (unsigned long long)nact);
+  }
+  // 3. backward over the same candidates
+  {
+    const float nO = -O;
+    const float ro = __shfl_xor_sync(~0u, rho, 1), nOo = __shfl_xor_sync(~0u, nO, 1);
+    if ((lane & 1) == 0) S.pc[lane >> 1] = make_float4(rho, ro, nO, nOo);
+  }
+  __syncwarp();
+  const uint32_t nchunks = enum_mode ? (total + BL_CAP - 1) / BL_CAP : 1u;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    if (nchunks > 1) {  // the scratch holds the last forward chunk: rebuild chunk c
+      __syncwarp();
+      wn = build(c);
+      __syncwarp();
+    }
+    bwd_pass_x(F, L, wn, (nact + 1) >> 1, o, S);
+  }
+}
+
 __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
@@ -265,8 +470,12 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   const bool dense = F.iota != nullptr;  // cutoff_T = inf: every key is a candidate, no lists
   uint32_t nb = BL_OVERFLOW;
   if (it.z >= 0) nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
-  if (nb == BL_OVERFLOW) {  // no brick list (out of domain / overflowed brick): split kernels
-    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+  if (nb == BL_OVERFLOW) {
+    if (it.z >= 0) {  // an overflowed brick: candidates by direct enumeration (fit_item_enum)
+      fit_item_enum(F, item, S, Lw);
+      return;
+    }
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;  // out of domain: split kernels
     return;
   }
   // 1. box, candidate ids
