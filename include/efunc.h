@@ -69,7 +69,9 @@ typedef enum { EFUNC_VARIANT_COMBINED = 0 } efunc_variant; /* O^{+Delta}, 13 cha
 
 typedef struct {
   int32_t R;              /* lattice resolution per axis, 2 <= R <= 256 */
-  int32_t degree;         /* polynomial degree of f; must be 1 */
+  int32_t degree;         /* polynomial degree of f: 1 (f = c + g.(q-k)) or 0 (f = c, Table 3 G-0:
+                             the g channels 2-4, 10-12 are held at 0 and AdamW skips them; their
+                             gradient entries are the degree-1 ones at g = 0 and carry no update) */
   int32_t variant;        /* EFUNC_VARIANT_COMBINED */
   float cutoff_T;         /* certified cutoff in nats (20.0f default); <=0 or inf: dense */
   int32_t deterministic;  /* 1: gradients bitwise reproducible run to run (no float atomics) */
@@ -116,7 +118,7 @@ typedef struct {
 
 /* efunc_create — allocate a handle on cfg->device and upload theta.
  *   theta_host: host float[R^3*13] in the layout above (NULL = all zeros).
- *   Returns EFUNC_EINVAL for R outside [2,256], degree != 1, variant != COMBINED. */
+ *   Returns EFUNC_EINVAL for R outside [2,256], degree not 0 or 1, variant != COMBINED. */
 EFUNC_API efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efunc_t** out);
 EFUNC_API efunc_status efunc_destroy(efunc_t* h);
 

@@ -130,7 +130,13 @@ efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
 
 // S0 + key binning + brick lists. force = 1: theta was replaced wholesale, rebuild the lists
 // regardless of the Verlet skin.
+// degree 0 (Table 3 G-0: f = c): the g channels of both banks held at 0
+uint32_t g_channels(const efunc_t* h) {
+  return h->cfg.degree == 0 ? ((7u << 2) | (7u << 10)) : 0u;
+}
+
 efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
+  if (force) h->launches += launch_zero_channels(h->theta, h->n_nodes, g_channels(h), s);
   CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(h->cell_fill, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
@@ -474,6 +480,7 @@ efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cuda
   hc.eps = hp->eps;
   hc.weight_decay = hp->weight_decay;
   hc.decay_mask = hp->decay_mask;
+  hc.frozen_mask = g_channels(h);
   h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
   CK(cudaGetLastError());
   return rebuild_keys(h, s);
@@ -633,7 +640,7 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     *out = p;
     return EFUNC_OK;
   }
-  if (cfg->degree != 1) return fail(nullptr, EFUNC_EINVAL, "only degree 1 is implemented");
+  if (cfg->degree != 0 && cfg->degree != 1) return fail(nullptr, EFUNC_EINVAL, "degree must be 0 or 1");
   if (cfg->variant != EFUNC_VARIANT_COMBINED) return fail(nullptr, EFUNC_EINVAL, "only the COMBINED variant");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(nullptr, EFUNC_ECUDA, "no CUDA device");

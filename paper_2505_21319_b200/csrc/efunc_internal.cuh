@@ -210,12 +210,14 @@ int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, in
 struct AdamWConst {  // the efunc_adamw hyper-parameters (doubles, like torch's python floats)
   double lr, beta1, beta2, eps, weight_decay;
   uint32_t decay_mask;
+  uint32_t frozen_mask;  // channels AdamW leaves untouched (degree 0: the g channels, held at 0)
 };
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,
                  DevScalars* ds, cudaStream_t s);
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
+int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s);
 
 }  // namespace ef
 

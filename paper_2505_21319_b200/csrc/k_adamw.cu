@@ -32,6 +32,7 @@ __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ gra
   const uint32_t mask = hc.decay_mask;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % EF_NCH);
+    if ((hc.frozen_mask >> ch) & 1u) continue;  // degree 0: g channels stay exactly 0
     float p = theta[i];
     const float g = grad[i];
     if ((mask >> ch) & 1u) p *= decay;
@@ -54,6 +55,21 @@ __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ gra
       ds->adam_done = 0;
     }
   }
+}
+
+// theta[n][c] = 0 for the channels in mask (degree 0: the polynomial gradients g0, g1)
+__global__ void k_zero_channels(float* __restrict__ theta, int n_nodes, uint32_t mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n_nodes * EF_NCH;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if ((mask >> (int)(i % EF_NCH)) & 1u) theta[i] = 0.0f;
+}
+
+int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s) {
+  if (!mask) return 0;
+  int blocks = (int)(((int64_t)n_nodes * EF_NCH + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_zero_channels<<<blocks, 256, 0, s>>>(theta, n_nodes, mask);
+  return 1;
 }
 
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,

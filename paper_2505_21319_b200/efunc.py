@@ -137,7 +137,7 @@ class EFunc:
 
     def __init__(self, R: int, theta=None, cutoff_T: float = 20.0, device: int = 0,
                  deterministic: bool = False, sync_checks: bool = False, fit_graph: bool = True,
-                 n_shapes: int = 1):
+                 n_shapes: int = 1, degree: int = 1):
         """n_shapes > 1: S independent grids in one handle (BASELINE config C5); theta, grads and
         the per-query arrays then carry a leading [S] axis and J counts queries per shape."""
         import torch
@@ -146,7 +146,7 @@ class EFunc:
         self.S = max(1, int(n_shapes))
         self.device = int(device)
         self.n_params = self.S * self.R ** 3 * NCH
-        cfg = Config(self.R, 1, 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks),
+        cfg = Config(self.R, int(degree), 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks),
                      int(fit_graph), self.S)
         th = None
         if theta is not None:

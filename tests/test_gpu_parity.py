@@ -668,3 +668,28 @@ def test_c4b_grid_128_functional_parity():
     gs = m.backward(dL_dO=dev(r)).cpu().numpy()
     fs = orc.forward(thg, R, q[sub])
     check_grads(gs, orc.backward(thg, R, q[sub], fs, r[sub].astype(np.float64)))
+
+
+# ----------------------------------------------------------------------------- degree 0 (NEXT-4)
+def test_degree0_variant_parity_and_frozen_g():
+    """degree = 0 (Table 3 G-0, f = c): the g channels are zeroed at creation and never updated;
+    values and the c / s / Delta gradients match the oracle on the same theta with g = 0."""
+    th, q, o = c1_case(seed=121, J=3000)
+    m = ef.EFunc(8, th, degree=0)
+    th0 = th.copy()
+    th0[:, 2:5] = 0.0
+    th0[:, 10:13] = 0.0
+    assert np.array_equal(m.get_params(), th0)
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True)
+    f = orc.forward(th0, 8, q)
+    _, r = orc.mse_loss(f.O, o)
+    ref = orc.backward(th0, 8, q, f, r)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    g = g.cpu().numpy()
+    for ch in (0, 1, 5, 6, 7, 8, 9):
+        assert nw(g[:, ch], ref[:, ch]) <= TOL_GRAD, ch
+    for _ in range(3):
+        m.fit_step(dev(q), dev(o))
+    p = m.get_params()
+    assert np.all(p[:, 2:5] == 0.0) and np.all(p[:, 10:13] == 0.0)
+    assert not np.array_equal(p[:, 1], th0[:, 1])
