@@ -549,8 +549,11 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
 #if FT_BWD2
   // rounds of 64 candidates: lane keys base + lane and base + 32 + lane (records one round ahead;
   // a missing second key is a far zero key whose sums are discarded)
+  // ids two rounds ahead, records one round ahead: a record gather never waits on an id load
+  // issued in the same round
   const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t iA = ((uint32_t)lane < wn) ? L[lane] : 0u, iB = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  uint32_t iA2 = ((uint32_t)lane + 64 < wn) ? L[lane + 64] : 0u, iB2 = ((uint32_t)lane + 96 < wn) ? L[lane + 96] : 0u;
   float4 aA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA]) : far_a;
   float4 bA = ((uint32_t)lane < wn) ? __ldg(&kv.grid_raw[2 * iA + 1]) : z4;
   float4 aB = ((uint32_t)lane + 32 < wn) ? __ldg(&kv.grid_raw[2 * iB]) : far_a;
@@ -559,8 +562,10 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     const uint32_t k = base + lane;
     const uint32_t idA = iA, idB = iB;
     const float4 a0 = aA, b0 = bA, a1 = aB, b1 = bB;
-    iA = (k + 64 < wn) ? L[k + 64] : 0u;
-    iB = (k + 96 < wn) ? L[k + 96] : 0u;
+    iA = iA2;
+    iB = iB2;
+    iA2 = (k + 128 < wn) ? L[k + 128] : 0u;
+    iB2 = (k + 160 < wn) ? L[k + 160] : 0u;
     aA = far_a; bA = z4; aB = far_a; bB = z4;
     if (k + 64 < wn) {
       aA = __ldg(&kv.grid_raw[2 * iA]);
