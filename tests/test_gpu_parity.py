@@ -693,3 +693,27 @@ def test_degree0_variant_parity_and_frozen_g():
     p = m.get_params()
     assert np.all(p[:, 2:5] == 0.0) and np.all(p[:, 10:13] == 0.0)
     assert not np.array_equal(p[:, 1], th0[:, 1])
+
+
+def test_batched_shapes_pipelined_host_io():
+    """n_shapes = 2 with pipelined host I/O: each shape's fit step and loss read-back through the
+    batched handle equals two single-shape handles stepping the same batches."""
+    R, J, S = 8, 2000, 2
+    shapes = synth.c5_shapes(S, 17)
+    ths = np.stack([synth.fitted_like_theta(R, sh, 30 + k) for k, sh in enumerate(shapes)])
+    batches = []
+    for i in range(3):
+        bs = [synth.sample_batch(sh, J, seed=40 + 10 * i + k) for k, sh in enumerate(shapes)]
+        batches.append((np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs])))
+    mb = ef.EFunc(R, ths, n_shapes=S, fit_graph=False)
+    outs = [mb.fit_step(torch.as_tensor(q).pin_memory(), torch.as_tensor(o).pin_memory(), pipelined=True)
+            for q, o in batches]
+    mb.sync()
+    for k in range(S):
+        m1 = ef.EFunc(R, ths[k], fit_graph=False)
+        for i, (q, o) in enumerate(batches):
+            lo = torch.zeros(1, device="cuda")
+            m1.fit_step(dev(q[k]), dev(o[k]), loss_out=lo)
+            assert abs(float(lo.item()) - float(outs[i][k])) <= 1e-5 * float(lo.item())
+        d = np.abs(m1.get_params() - mb.get_params()[k])
+        assert np.mean(d > 1e-5) <= 1e-3
