@@ -14,6 +14,13 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// One key record (2 float4, 32-byte aligned) in one 256-bit read-only load (sm_100: LDG.256).
+__device__ __forceinline__ void ld_rec(const float4* rec, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(rec));
+}
+
 __device__ __forceinline__ int cellc(float p, float inv_h, int NC) {
   float c = floorf((p + 1.0f) * inv_h);
   c = fminf(fmaxf(c, 0.0f), (float)(NC - 1));

@@ -292,12 +292,10 @@ __device__ __forceinline__ void bwd_pass_x(const FitArgs& F, const uint32_t* L, 
     iB = (k + 96 < wn) ? L[k + 96] : 0u;
     aA = far_a; bA = z4; aB = far_a; bB = z4;
     if (k + 64 < wn) {
-      aA = __ldg(&kv.grid_raw[2 * iA]);
-      bA = __ldg(&kv.grid_raw[2 * iA + 1]);
+      ld_rec(&kv.grid_raw[2 * iA], aA, bA);
     }
     if (k + 96 < wn) {
-      aB = __ldg(&kv.grid_raw[2 * iB]);
-      bB = __ldg(&kv.grid_raw[2 * iB + 1]);
+      ld_rec(&kv.grid_raw[2 * iB], aB, bB);
     }
     if (base + 32 < wn) {  // warp-uniform: two keys per lane
       MseSums s0, s1;
@@ -322,8 +320,7 @@ __device__ __forceinline__ void bwd_pass_x(const FitArgs& F, const uint32_t* L, 
     id1 = id2;
     id2 = (k + 64 < wn) ? L[k + 64] : 0u;
     if (k + 32 < wn) {
-      a1 = __ldg(&kv.grid_raw[2 * id1]);
-      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+      ld_rec(&kv.grid_raw[2 * id1], a1, b1);
     }
     if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
@@ -568,12 +565,10 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     iB2 = (k + 160 < wn) ? L[k + 160] : 0u;
     aA = far_a; bA = z4; aB = far_a; bB = z4;
     if (k + 64 < wn) {
-      aA = __ldg(&kv.grid_raw[2 * iA]);
-      bA = __ldg(&kv.grid_raw[2 * iA + 1]);
+      ld_rec(&kv.grid_raw[2 * iA], aA, bA);
     }
     if (k + 96 < wn) {
-      aB = __ldg(&kv.grid_raw[2 * iB]);
-      bB = __ldg(&kv.grid_raw[2 * iB + 1]);
+      ld_rec(&kv.grid_raw[2 * iB], aB, bB);
     }
     if (base + 32 < wn) {  // warp-uniform: two keys per lane
       MseSums s0, s1;
@@ -598,8 +593,7 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     id1 = id2;
     id2 = (k + 64 < wn) ? L[k + 64] : 0u;
     if (k + 32 < wn) {
-      a1 = __ldg(&kv.grid_raw[2 * id1]);
-      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+      ld_rec(&kv.grid_raw[2 * id1], a1, b1);
     }
     if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
