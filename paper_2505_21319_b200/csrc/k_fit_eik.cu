@@ -200,8 +200,7 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
       float4 a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b = make_float4(0.f, 0.f, 0.f, 0.f);  // far: weight 0
       if (k < wn) {
         const uint32_t id = L[k];
-        a = __ldg(&kv.grid_raw[2 * id]);
-        b = __ldg(&kv.grid_raw[2 * id + 1]);
+        ld_rec(&kv.grid_raw[2 * id], a, b);
       }
       __syncwarp();  // the previous round's readers are done
       S.kA[slot][hi] = a.x; S.kA[slot][2 + hi] = a.y;
@@ -280,13 +279,11 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     float4 a0 = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b1 = b0;
     if (h0) {
       id0 = L[k0];
-      a0 = __ldg(&kv.grid_raw[2 * id0]);
-      b0 = __ldg(&kv.grid_raw[2 * id0 + 1]);
+      ld_rec(&kv.grid_raw[2 * id0], a0, b0);
     }
     if (h1) {
       id1 = L[k1];
-      a1 = __ldg(&kv.grid_raw[2 * id1]);
-      b1 = __ldg(&kv.grid_raw[2 * id1 + 1]);
+      ld_rec(&kv.grid_raw[2 * id1], a1, b1);
     }
     const float beta20 = 2.0f * a0.w * EF_LN2, beta21 = 2.0f * a1.w * EF_LN2;
     EikBwd s0, s1;
