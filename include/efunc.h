@@ -117,7 +117,8 @@ typedef struct {
 } efunc_stats;
 
 /* efunc_create — allocate a handle on cfg->device and upload theta.
- *   theta_host: host float[R^3*13] in the layout above (NULL = all zeros).
+ *   theta_host: host float[R^3*13] in the layout above (NULL = all zeros); [n_shapes][R^3*13]
+ *               for a batched handle.
  *   Returns EFUNC_EINVAL for R outside [2,256], degree not 0 or 1, variant != COMBINED. */
 EFUNC_API efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efunc_t** out);
 EFUNC_API efunc_status efunc_destroy(efunc_t* h);
@@ -155,10 +156,11 @@ EFUNC_API efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const floa
  *   O     dev float[J] output values or NULL
  *   grad  dev float[R^3*13], accumulated into (+=)
  *   loss_out dev float[1] or NULL
- * For the MSE loss (non-deterministic mode, counting off) it runs one fused kernel per work
- * item: the MSE upstream of a query depends on that query alone, so each item's forward and
- * backward share one candidate-key pass. Otherwise it is exactly forward + backward. Leaves
- * no saved forward state (a following efunc_backward returns EFUNC_ESTATE). */
+ * Outside deterministic mode (and with counting off) it runs one fused kernel per work item:
+ * k_fit for MSE, k_fit_eik for MSE_EIKONAL (the MSE and Eikonal upstreams of a query depend on
+ * that query alone, so each item's forward and backward share one candidate-key pass). Otherwise
+ * it is exactly forward + backward. Leaves no saved forward state (a following efunc_backward
+ * returns EFUNC_ESTATE). */
 EFUNC_API efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J,
                                     const efunc_loss* loss, float* O, float* grad, float* loss_out,
                                     void* stream);
