@@ -717,3 +717,21 @@ def test_batched_shapes_pipelined_host_io():
             assert abs(float(lo.item()) - float(outs[i][k])) <= 1e-5 * float(lo.item())
         d = np.abs(m1.get_params() - mb.get_params()[k])
         assert np.mean(d > 1e-5) <= 1e-3
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_forward_backward_tiny_grids(R):
+    """R = 2, 3 (one or a few cells; the out-of-domain queries go to the split kernels) through
+    the fused call, and J = 0."""
+    th = synth.random_theta(R, 140 + R, log_scale_mean=1.0)
+    rg = synth.rng(150 + R)
+    q = rg.uniform(-1.5, 1.5, size=(700, 3)).astype(np.float32)
+    o = rg.normal(scale=0.3, size=700).astype(np.float32)
+    m = ef.EFunc(R, th)
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True)
+    f = orc.forward(th, R, q)
+    _, r = orc.mse_loss(f.O, o)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r), floor=1e-6)
+    g0, _, L0 = m.forward_backward(dev(q[:0]), dev(o[:0]), loss=ef.LOSS_MSE)
+    assert float(g0.abs().sum()) == 0.0 and float(L0.item()) == 0.0
