@@ -735,3 +735,23 @@ def test_forward_backward_tiny_grids(R):
     check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r), floor=1e-6)
     g0, _, L0 = m.forward_backward(dev(q[:0]), dev(o[:0]), loss=ef.LOSS_MSE)
     assert float(g0.abs().sum()) == 0.0 and float(L0.item()) == 0.0
+
+
+def test_forward_backward_large_beta_accuracy():
+    """Large scales (s ~ 9 +- 0.5, beta ~ 8e3, as after long fits) at 32^3: the fused kernel's
+    item-local expansion of the exponent keeps O and all 13 gradient channels within tolerance
+    of the oracle (full batch, every query's upstream)."""
+    R, J = 32, 2000
+    tor = synth.Torus()
+    th = synth.fitted_like_theta(R, tor, 160)
+    rg = synth.rng(161)
+    th[:, 0] = 9.0 + rg.normal(scale=0.5, size=R ** 3)
+    th[:, 8] = 9.0 + rg.normal(scale=0.5, size=R ** 3)
+    th = th.astype(np.float32)
+    q, o = synth.sample_batch(tor, J, seed=162)
+    m = ef.EFunc(R, th)
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True)
+    f = orc.forward(th, R, q)
+    _, r = orc.mse_loss(f.O, o)
+    assert nw(O.cpu().numpy(), f.O) <= TOL_VAL
+    check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r))
