@@ -40,12 +40,22 @@ constexpr uint32_t BL_OVERFLOW = 0xffffffffu;
 constexpr int POOL_PER_KEY = 640;   // brick-list pool capacity per key
 // per-warp id scratch of the persistent list builders (k_fit, k_brick_lists): SCRATCH_WARPS slots
 // of BL_CAP ids, padded so the slots do not alias in L1
-constexpr int SCRATCH_WARPS = 148 * 32;
-constexpr size_t SCRATCH_STRIDE = BL_CAP + 32;
+constexpr int SCRATCH_WARPS = 148 * 16;
+constexpr int ENUM_CAP = 32768;     // k_fit: candidate ids per enumeration chunk (overflowed bricks)
+// a slot also holds two k_brick_lists warps' staging (BL_CAP ids each), so the list build runs
+// 2 x SCRATCH_WARPS warps
+constexpr size_t SCRATCH_HALF = BL_CAP + 32;
+constexpr size_t SCRATCH_STRIDE = (2 * SCRATCH_HALF > (size_t)ENUM_CAP + 32 ? 2 * SCRATCH_HALF : (size_t)ENUM_CAP + 32);
 
 constexpr int WL_PER_QUERY = 64;    // forward->backward candidate pool capacity per query
-constexpr float SKIN_H = 0.25f;     // Verlet skin of the brick lists, in lattice spacings
-constexpr float SKIN_MU = 0.05f;    // allowed relative drift of beta between list builds
+#ifndef EF_SKIN_H
+#define EF_SKIN_H 0.25f
+#endif
+#ifndef EF_SKIN_MU
+#define EF_SKIN_MU 0.05f
+#endif
+constexpr float SKIN_H = EF_SKIN_H;    // Verlet skin of the brick lists, in lattice spacings
+constexpr float SKIN_MU = EF_SKIN_MU;  // allowed relative drift of beta between list builds
 
 struct KeysView {
   const float4* ks;        // sorted records, 2 float4 per key (a at 2k, b at 2k+1)

@@ -344,7 +344,7 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
   }
   const uint32_t nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
   // an overflowed brick (no list): candidates by direct enumeration of the lattice cells around
-  // the item, in chunks of BL_CAP ids (each chunk re-enumerates: cheap next to its pair work)
+  // the item, in chunks of ENUM_CAP ids (each chunk re-enumerates: cheap next to its pair work)
   const bool enum_mode = !dense && nb == BL_OVERFLOW;
   // 1. box, candidate ids
   const bool act = lane < nact;
@@ -378,15 +378,15 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
       total = cnt;
       return cnt;
     }
-    const uint32_t lo = c * (uint32_t)BL_CAP;
+    const uint32_t lo = c * (uint32_t)ENUM_CAP;
     enumerate(kv, box, [&](bool pass, uint32_t kp, float4) {
       const uint32_t bal = __ballot_sync(~0u, pass);
       const uint32_t idx = cnt + __popc(bal & lanemask_lt());
-      if (pass && idx >= lo && idx < lo + (uint32_t)BL_CAP) Lw[idx - lo] = (uint32_t)__ldg(&kv.kid[kp]);
+      if (pass && idx >= lo && idx < lo + (uint32_t)ENUM_CAP) Lw[idx - lo] = (uint32_t)__ldg(&kv.kid[kp]);
       cnt += __popc(bal);
     });
     total = cnt;
-    return cnt > lo ? min(cnt - lo, (uint32_t)BL_CAP) : 0u;
+    return cnt > lo ? min(cnt - lo, (uint32_t)ENUM_CAP) : 0u;
   };
   // 2. forward
   const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
@@ -416,7 +416,7 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
         __syncwarp();
       }
       fwd_accum_x<16>(kv, L, wn, nact, o, S.qa, S.qb, Za, Ma);
-      if ((c + 1) * (uint32_t)BL_CAP >= total) break;
+      if ((c + 1) * (uint32_t)ENUM_CAP >= total) break;
     }
     fwd_reduce_x<16>(Za, Ma, Z, M);
   }
@@ -447,7 +447,7 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
     if ((lane & 1) == 0) S.pc[lane >> 1] = make_float4(rho, ro, nO, nOo);
   }
   __syncwarp();
-  const uint32_t nchunks = enum_mode ? (total + BL_CAP - 1) / BL_CAP : 1u;
+  const uint32_t nchunks = enum_mode ? (total + ENUM_CAP - 1) / ENUM_CAP : 1u;
   for (uint32_t c = 0; c < nchunks; ++c) {
     if (nchunks > 1) {  // the scratch holds the last forward chunk: rebuild chunk c
       __syncwarp();

@@ -17,7 +17,8 @@ __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv
   __shared__ uint32_t rs[KB_WARPS][32], ro[KB_WARPS][32];
   // the warp's staging area: a slot of the handle's per-warp scratch (shared with k_fit, which
   // never runs concurrently), BL_CAP ids, L2-resident
-  uint32_t* const stw = scratch + (size_t)(blockIdx.x * KB_WARPS + (threadIdx.x >> 5)) * SCRATCH_STRIDE;
+  const uint32_t gw = blockIdx.x * KB_WARPS + (threadIdx.x >> 5);  // two warps per scratch slot
+  uint32_t* const stw = scratch + (size_t)(gw >> 1) * SCRATCH_STRIDE + (gw & 1) * SCRATCH_HALF;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (!ds->lists_invalid) return;  // the lists of an earlier step are still valid (Verlet skin)
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ds->list_builds, 1u);
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(32 * KB_WARPS) k_brick_lists(const KeysView kv
 int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool, uint32_t pool_cap,
                        uint32_t* off, uint32_t* n, DevScalars* ds, uint32_t* scratch, cudaStream_t s) {
   uint32_t blocks = (bg.n_codes + KB_WARPS - 1) / KB_WARPS;
-  const uint32_t cap = (uint32_t)(SCRATCH_WARPS / KB_WARPS);  // one scratch slot per warp
+  const uint32_t cap = (uint32_t)(2 * SCRATCH_WARPS / KB_WARPS);  // two warps per scratch slot
   if (blocks > cap) blocks = cap;
   k_brick_lists<<<blocks, 32 * KB_WARPS, 0, s>>>(kv, bg, T_l, pool, pool_cap, off, n, ds, scratch);
   return 1;
