@@ -458,7 +458,14 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
   }
 }
 
-__device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
+// Item types the list builder hands on
+constexpr uint32_t IT_NORMAL = 0, IT_ENUM = 1, IT_SKIP = 2, IT_END = 3;
+
+// Part 1 of a work item: the box and its candidate ids (into Lw, or the all-keys list in dense
+// mode). Returns IT_NORMAL with L, wn, o set; IT_ENUM for an overflowed brick (fit_item_enum
+// builds its own chunks); IT_SKIP for out-of-domain items (queued for the split kernels).
+__device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint32_t item, uint32_t* Lw,
+                                                   const uint32_t*& L, uint32_t& wn, float3& o) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
   const int lane = threadIdx.x & 31;
@@ -468,14 +475,10 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   uint32_t nb = BL_OVERFLOW;
   if (it.z >= 0) nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
   if (nb == BL_OVERFLOW) {
-    if (it.z >= 0) {  // an overflowed brick: candidates by direct enumeration (fit_item_enum)
-      fit_item_enum(F, item, S, Lw);
-      return;
-    }
+    if (it.z >= 0) return IT_ENUM;  // an overflowed brick: candidates by direct enumeration
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;  // out of domain: split kernels
-    return;
+    return IT_SKIP;
   }
-  // 1. box, candidate ids
   const bool act = lane < nact;
   const int64_t js = (int64_t)it.x + lane;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -486,20 +489,38 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   }
   Box box = warp_box(act, q.x, q.y, q.z, mh);
   box.thr += A.T_l;
-  const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
-  __syncwarp();  // the previous item's readers of L and S are done
-  uint32_t wn = 0;
-  const uint32_t* L = Lw;  // the candidate ids the passes read
+  o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
+  __syncwarp();  // the previous item's readers of L are done
+  wn = 0;
+  L = Lw;
   if (dense) {  // all 2R^3 keys in id order (coalesced record loads)
     L = F.iota;
     wn = 2u * (uint32_t)kv.n_nodes;
   } else {
+    uint32_t cnt = 0;
     stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
       const uint32_t bal = __ballot_sync(~0u, pass);
-      if (pass) Lw[wn + __popc(bal & lanemask_lt())] = id;
-      wn += __popc(bal);
+      if (pass) Lw[cnt + __popc(bal & lanemask_lt())] = id;
+      cnt += __popc(bal);
     });
+    wn = cnt;
   }
+  return IT_NORMAL;
+}
+
+// Part 2 of a work item: forward, loss, backward over the candidate ids L[0 .. wn).
+__device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_t item, FitSmem& S,
+                                                 const uint32_t* L, const uint32_t wn, const float3 o) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (act) q = A.qs[js];
+  __syncwarp();  // the previous item's readers of S are done
   // 2. forward
   const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
   const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;  // idle slot: weight 0 (finite: u qq = 0)
@@ -601,6 +622,15 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
     }
   }
 #endif
+}
+
+__device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
+  const uint32_t* L;
+  uint32_t wn;
+  float3 o;
+  const uint32_t t = fit_item_build(F, item, Lw, L, wn, o);
+  if (t == IT_ENUM) fit_item_enum(F, item, S, Lw);
+  else if (t == IT_NORMAL) fit_item_compute(F, item, S, L, wn, o);
 }
 
 __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(const FitArgs F) {
