@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--eager", action="store_true", help="N=1: plain launches instead of a CUDA graph per step")
     p.add_argument("--split", action="store_true", help="efunc_forward + efunc_backward instead of the fused call")
+    p.add_argument("--deterministic", action="store_true",
+                   help="deterministic mode (stable sorts, 64-bit fixed-point gradient sums; split path)")
     return p.parse_args()
 
 
@@ -190,7 +192,7 @@ def run_ours(args, rank, world, local_rank):
 
     # model: paper init (s = 7, c ~ N(0, 0.1^2), g = 0) + mean-shift offsets on the GPU
     th0 = np.stack([synth.init_theta(R, SEED + k) for k in range(S)]) if S > 1 else synth.init_theta(R, SEED)
-    m = ef.EFunc(R, th0, device=dev, n_shapes=S)
+    m = ef.EFunc(R, th0, device=dev, n_shapes=S, deterministic=args.deterministic)
     surf = np.stack([synth.surface_points(sh, 16384, SEED) for sh in shapes])
     m.mean_shift_init(torch.as_tensor(surf if S > 1 else surf[0]).cuda(dev))
     hp = ef.AdamW()
@@ -347,7 +349,7 @@ def run_ours(args, rank, world, local_rank):
         return
     # roofline of the dominant kernel: algorithmic lane-ops per launch / its time. k_fit (fused,
     # MSE) does the forward and the backward of every kept pair; k_backward only the backward.
-    fused = not args.split
+    fused = not (args.split or args.deterministic)
     kname = ("k_fit" if loss_kind == "mse" else "k_fit_eik") if fused else "k_backward"
     if loss_kind == "mse":
         ops = OPS_BWD_GRID * (kept - kept_off) + OPS_BWD_OFF * kept_off
@@ -383,7 +385,8 @@ def run_ours(args, rank, world, local_rank):
                        "global_batch": J_global if S == 1 else n_pts * world, "shapes_per_gpu": S,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}" if S == 1 else f"replicas{world}",
                        "launch": "cuda-graph per step" if use_graph else "eager",
-                       "path": "split forward/backward" if args.split else
+                       "deterministic": bool(args.deterministic),
+                       "path": "split forward/backward" if (args.split or args.deterministic) else
                                f"efunc_forward_backward (fused {'k_fit' if loss_kind == 'mse' else 'k_fit_eik'})",
                        "l2": f"inputs larger than L2: pool of {pool} batches x {n_pts * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e}

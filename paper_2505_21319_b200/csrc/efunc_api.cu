@@ -405,7 +405,9 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   CK(cudaMemsetAsync(&h->ds->bwd_next, 0, sizeof(uint32_t), s));
   if (h->cfg.deterministic) {
     CK(cudaMemsetAsync(&h->ds->umax, 0, sizeof(float), s));
+    const int slot = timing_begin(h, s);
     h->launches += launch_backward_det(b, h->fwd_items_bound, s);
+    timing_end(h, slot, s);
     h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);
   } else {
     const int slot = timing_begin(h, s);
