@@ -327,9 +327,6 @@ __device__ __forceinline__ void shift_bound(const KeysView& kv, const float4 q, 
       g0 = make_float3(kb.y, kb.z, kb.w);
     }
   }
-#ifdef EF_CORNERS_ONLY
-  return;
-#endif
   const int cid = (cz * NC + cy) * NC + cx;
   const uint32_t s = __ldg(&kv.cell_start[cid]);
   const uint32_t e_ = min(__ldg(&kv.cell_start[cid + 1]), s + 32u);
