@@ -599,6 +599,33 @@ T* off(T* p, int64_t per_shape, size_t k) {
   return p ? p + per_shape * (int64_t)k : nullptr;
 }
 
+// Batched handles: fork the shapes onto per-shape streams (after the caller's prior work) and
+// join them back, so the shapes' kernels overlap (each shape is a full-GPU persistent launch
+// plus small kernels; overlapping fills one shape's tail and small launches with another's).
+// Capture-safe (event fork/join).
+efunc_status kids_fork(efunc_t* h, cudaStream_t s) {
+  if (h->kid_streams.empty()) {
+    h->kid_streams.resize(h->kids.size());
+    h->kid_events.resize(h->kids.size());
+    for (size_t k = 0; k < h->kids.size(); ++k) {
+      CK(cudaStreamCreateWithFlags(&h->kid_streams[k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->kid_events[k], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&h->fork_event, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(h->fork_event, s));
+  for (cudaStream_t ks : h->kid_streams) CK(cudaStreamWaitEvent(ks, h->fork_event, 0));
+  return EFUNC_OK;
+}
+
+efunc_status kids_join(efunc_t* h, cudaStream_t s) {
+  for (size_t k = 0; k < h->kids.size(); ++k) {
+    CK(cudaEventRecord(h->kid_events[k], h->kid_streams[k]));
+    CK(cudaStreamWaitEvent(s, h->kid_events[k], 0));
+  }
+  return EFUNC_OK;
+}
+
 efunc_status kid_ok(efunc_t* h, size_t k, efunc_status st) {
   if (st != EFUNC_OK) h->err = "shape " + std::to_string(k) + ": " + h->kids[k]->err;
   return st;
@@ -725,6 +752,9 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
 efunc_status efunc_destroy(efunc_t* h) {
   if (h && !h->kids.empty()) {
     for (efunc_t* k : h->kids) efunc_destroy(k);
+    for (cudaStream_t ks : h->kid_streams) cudaStreamDestroy(ks);
+    for (cudaEvent_t e : h->kid_events) cudaEventDestroy(e);
+    if (h->fork_event) cudaEventDestroy(h->fork_event);
     delete h;
     return EFUNC_OK;
   }
@@ -769,11 +799,13 @@ efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, 
 efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
                                     float* O, float* grad, float* loss_out, void* stream) {
   if (h && !h->kids.empty()) {
+    DeviceGuard dg(h->cfg.device);
+    RET(kids_fork(h, (cudaStream_t)stream));
     for (size_t k = 0; k < h->kids.size(); ++k)
       RET(kid_ok(h, k, efunc_forward_backward(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, off(O, J, k),
                                               off(grad, h->n_nodes * (int64_t)EF_NCH, k), off(loss_out, 1, k),
-                                              stream)));
-    return EFUNC_OK;
+                                              h->kid_streams[k])));
+    return kids_join(h, (cudaStream_t)stream);
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
@@ -782,9 +814,12 @@ efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, 
 
 efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream) {
   if (h && !h->kids.empty()) {
+    DeviceGuard dg(h->cfg.device);
+    RET(kids_fork(h, (cudaStream_t)stream));
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_adamw_step(h->kids[k], off(grad, h->n_nodes * (int64_t)EF_NCH, k), hp, stream)));
-    return EFUNC_OK;
+      RET(kid_ok(h, k, efunc_adamw_step(h->kids[k], off(grad, h->n_nodes * (int64_t)EF_NCH, k), hp,
+                                        h->kid_streams[k])));
+    return kids_join(h, (cudaStream_t)stream);
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);

@@ -329,6 +329,9 @@ struct efunc {
   cudaStream_t cap_stream = nullptr;
   // kernel timing (efunc_set_timing): event pairs, slot = call index mod slots
   std::vector<efunc*> kids;          // n_shapes > 1: one single-shape handle per shape
+  std::vector<cudaStream_t> kid_streams;  // batched calls fork the shapes onto these and join
+  std::vector<cudaEvent_t> kid_events;
+  cudaEvent_t fork_event = nullptr;
   std::vector<cudaEvent_t> tev;
   std::vector<int> tev_used;
   int64_t tseq = 0;
