@@ -39,8 +39,7 @@ struct EikFwd {
 };
 
 __device__ __forceinline__ void eik_fwd_round(const EikSmem& S, const int npk, const float2 qx, const float2 qy,
-                                              const float2 qz, const float2 sh, const float2 f0,
-                                              const float2 g0x, const float2 g0y, const float2 g0z, EikFwd& a) {
+                                              const float2 qz, const float2 sh, const float2 f0, EikFwd& a) {
 #pragma unroll 2
   for (int p = 0; p < npk; ++p) {
     const float4 A = *reinterpret_cast<const float4*>(S.kA[p]);
@@ -56,15 +55,16 @@ __device__ __forceinline__ void eik_fwd_round(const EikSmem& S, const int npk, c
     const float2 bl = make_float2(B.z, B.w);
     const float2 e = __ffma2_rn(make_float2(-B.z, -B.w), dd, sh);
     const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
-    // f - f0 and g - g0: the shift key's value (accuracy of G)
+    // f - f0: the shift key's value (accuracy of O and G); S_g = sum w g needs no
+    // shift (a positive-weight mean of the g's)
     float2 f = __ffma2_rn(make_float2(C.z, C.w), dx, __fadd2_rn(make_float2(C.x, C.y), f0));
     f = __ffma2_rn(make_float2(D.x, D.y), dy, f);
     f = __ffma2_rn(make_float2(D.z, D.w), dz, f);
     a.Z = __fadd2_rn(a.Z, w);
     a.M = __ffma2_rn(w, f, a.M);
-    a.sgx = __ffma2_rn(w, __fadd2_rn(make_float2(C.z, C.w), g0x), a.sgx);
-    a.sgy = __ffma2_rn(w, __fadd2_rn(make_float2(D.x, D.y), g0y), a.sgy);
-    a.sgz = __ffma2_rn(w, __fadd2_rn(make_float2(D.z, D.w), g0z), a.sgz);
+    a.sgx = __ffma2_rn(w, make_float2(C.z, C.w), a.sgx);
+    a.sgy = __ffma2_rn(w, make_float2(D.x, D.y), a.sgy);
+    a.sgz = __ffma2_rn(w, make_float2(D.z, D.w), a.sgz);
     const float2 wbl = __fmul2_rn(w, bl);
     a.sux = __ffma2_rn(wbl, dx, a.sux);
     a.suy = __ffma2_rn(wbl, dy, a.suy);
@@ -166,7 +166,7 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
     return;
   }
-  // 1. shift bound (and the shift key's f0, g0), box, candidates
+  // 1. shift bound (and the shift key's f0), box, candidates
   const bool act = lane < nact;
   const int64_t js = (int64_t)it.x + lane;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -193,7 +193,6 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     const float sh = act ? mh : -INFINITY;
     const float2 qx = make_float2(q.x, q.x), qy = make_float2(q.y, q.y), qz = make_float2(q.z, q.z);
     const float2 sh2 = make_float2(sh, sh), nf0 = make_float2(-f0, -f0);
-    const float2 ng0x = make_float2(-g0.x, -g0.x), ng0y = make_float2(-g0.y, -g0.y), ng0z = make_float2(-g0.z, -g0.z);
     const int hi = lane & 1, slot = lane >> 1;
     for (uint32_t base = 0; base < wn; base += 32) {
       const uint32_t k = base + lane;
@@ -209,7 +208,7 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
       S.kD[slot][hi] = b.z; S.kD[slot][2 + hi] = b.w;
       __syncwarp();
       const int npk = ((int)min(wn - base, 32u) + 1) >> 1;
-      eik_fwd_round(S, npk, qx, qy, qz, sh2, nf0, ng0x, ng0y, ng0z, fa);
+      eik_fwd_round(S, npk, qx, qy, qz, sh2, nf0, fa);
     }
   }
   const float Z = hsum(fa.Z), M = hsum(fa.M);
@@ -228,9 +227,9 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     nlam = mh - log2f(Z);
     const float c2 = 2.0f * EF_LN2 * iz;
     const float Of = Oj - f0;
-    const float Gx = g0.x + (hsum(fa.sgx) * iz + c2 * fmaf(Of, hsum(fa.sux), -hsum(fa.sfx)));
-    const float Gy = g0.y + (hsum(fa.sgy) * iz + c2 * fmaf(Of, hsum(fa.suy), -hsum(fa.sfy)));
-    const float Gz = g0.z + (hsum(fa.sgz) * iz + c2 * fmaf(Of, hsum(fa.suz), -hsum(fa.sfz)));
+    const float Gx = fmaf(hsum(fa.sgx), iz, c2 * fmaf(Of, hsum(fa.sux), -hsum(fa.sfx)));
+    const float Gy = fmaf(hsum(fa.sgy), iz, c2 * fmaf(Of, hsum(fa.suy), -hsum(fa.sfy)));
+    const float Gz = fmaf(hsum(fa.sgz), iz, c2 * fmaf(Of, hsum(fa.suz), -hsum(fa.sfz)));
     const float ux = c2 * hsum(fa.sux), uy = c2 * hsum(fa.suy), uz = c2 * hsum(fa.suz);
     const float diff = Oj - q.w;
     const float r = 2.0f * diff * A.inv_J;
