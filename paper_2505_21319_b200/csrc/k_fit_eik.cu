@@ -11,7 +11,8 @@
 //      instruction;
 //   3. O_j, G_j, u_j, losses, r_j, h_j, h.u_j, h.G_j -> the item's query table in shared memory;
 //   4. backward, lanes = candidate keys (two per lane), the item's queries broadcast as packed
-//      pairs, 14 accumulators per key, three red.global.add.v4 per (key, item).
+//      pairs: the grid-bank candidates first (8 accumulators per key, no Delta terms), then the
+//      offset-bank ones (14 accumulators); up to three red.global.add.v4 per (key, item).
 // Items without a brick list or whose shift bound overflowed go to the split kernels.
 #include <algorithm>
 
@@ -81,6 +82,8 @@ struct EikBwd {
   float2 sc, sgx, sgy, sgz, phx, phy, phz, ss, sdx, sdy, sdz, pdx, pdy, pdz;
 };
 
+// OFF: an offset-bank key (also accumulates the Delta sums sd, pd; grid-bank keys have no Delta)
+template <bool OFF>
 __device__ __forceinline__ void eik_bwd_pair(const float4 a, const float4 b, const float beta2,
                                              const float4 QA, const float4 QB, const float4 QC,
                                              const float4 QD, const float4 QE, EikBwd& s) {
@@ -103,13 +106,13 @@ __device__ __forceinline__ void eik_bwd_pair(const float4 a, const float4 b, con
   hd = __ffma2_rn(hy, dy, hd);
   hd = __ffma2_rn(hx, dx, hd);
   const float2 hu = __fmul2_rn(make_float2(beta2, beta2), hd);                        // 2 beta h.d
-  float2 hg = __fmul2_rn(hz, make_float2(b.w, b.w));
-  hg = __ffma2_rn(hy, make_float2(b.z, b.z), hg);
-  hg = __ffma2_rn(hx, make_float2(b.y, b.y), hg);                                     // h.g
+  float2 hgT = __ffma2_rn(hz, make_float2(b.w, b.w), make_float2(-QE.z, -QE.w));
+  hgT = __ffma2_rn(hy, make_float2(b.z, b.z), hgT);
+  hgT = __ffma2_rn(hx, make_float2(b.y, b.y), hgT);                                   // h.g - h.G
   const float2 rh = make_float2(QC.x, QC.y);                                          // r + h.u
   const float2 alpha = __fadd2_rn(rh, make_float2(-hu.x, -hu.y));
-  const float2 tt = __ffma2_rn(make_float2(-hu.x, -hu.y), del, hg);
-  const float2 gam = __ffma2_rn(rh, del, __fadd2_rn(tt, make_float2(-QE.z, -QE.w)));  // - h.G
+  // gam = (r + h.u) del + h.g - h.u del - h.G
+  const float2 gam = __ffma2_rn(alpha, del, hgT);
   const float2 pa = __fmul2_rn(p, alpha);
   s.sc = __fadd2_rn(s.sc, pa);
   s.sgx = __ffma2_rn(pa, dx, s.sgx);
@@ -121,26 +124,29 @@ __device__ __forceinline__ void eik_bwd_pair(const float4 a, const float4 b, con
   // ss: p (beta dd gam + hu del), beta = beta2 / 2
   const float2 bdd = __fmul2_rn(make_float2(0.5f * beta2, 0.5f * beta2), dd);
   s.ss = __ffma2_rn(p, __ffma2_rn(bdd, gam, __fmul2_rn(hu, del)), s.ss);
-  const float2 pg = __fmul2_rn(p, gam);
-  s.sdx = __ffma2_rn(pg, dx, s.sdx);
-  s.sdy = __ffma2_rn(pg, dy, s.sdy);
-  s.sdz = __ffma2_rn(pg, dz, s.sdz);
-  const float2 pdel = __fmul2_rn(p, del);
-  s.pdx = __ffma2_rn(pdel, hx, s.pdx);
-  s.pdy = __ffma2_rn(pdel, hy, s.pdy);
-  s.pdz = __ffma2_rn(pdel, hz, s.pdz);
+  if (OFF) {
+    const float2 pg = __fmul2_rn(p, gam);
+    s.sdx = __ffma2_rn(pg, dx, s.sdx);
+    s.sdy = __ffma2_rn(pg, dy, s.sdy);
+    s.sdz = __ffma2_rn(pg, dz, s.sdz);
+    const float2 pdel = __fmul2_rn(p, del);
+    s.pdx = __ffma2_rn(pdel, hx, s.pdx);
+    s.pdy = __ffma2_rn(pdel, hy, s.pdy);
+    s.pdz = __ffma2_rn(pdel, hz, s.pdz);
+  }
 }
 
 __device__ __forceinline__ float hsum(const float2 v) { return v.x + v.y; }
 
 // one key's gradients into the padded accumulator (k_backward's EIK channel map)
+template <bool OFF>
 __device__ __forceinline__ void eik_red(const EikBwd& s, const float4 a, const float4 b, const int id,
                                         const int n_nodes, float* gpad) {
   const float beta = a.w * EF_LN2;
   const float sc = hsum(s.sc);
   const float dsv = -hsum(s.ss);
   const float dgx = hsum(s.sgx) + hsum(s.phx), dgy = hsum(s.sgy) + hsum(s.phy), dgz = hsum(s.sgz) + hsum(s.phz);
-  if (id < n_nodes) {
+  if (!OFF) {
     float* gp = gpad + (size_t)id * 16;
     red_v4(gp, dsv, sc, dgx, dgy);
     atomicAdd(gp + 4, dgz);
@@ -151,6 +157,48 @@ __device__ __forceinline__ void eik_red(const EikBwd& s, const float4 a, const f
     float* gp = gpad + (size_t)(id - n_nodes) * 16 + 8;
     red_v4(gp, dkx, dky, dkz, dsv);
     red_v4(gp + 4, sc, dgx, dgy, dgz);
+  }
+}
+
+// backward over one bank's candidates Ls[0, n), lanes = keys (two per lane)
+template <bool OFF>
+__device__ __forceinline__ void eik_bwd_segment(const FitArgs& F, const KeysView& kv, const uint32_t* Ls,
+                                                const uint32_t n, const EikSmem& S, const int np2) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = 0; base < n; base += 64) {
+    const uint32_t k0 = base + lane, k1 = base + 32 + lane;
+    const bool h0 = k0 < n, h1 = k1 < n;
+    uint32_t id0 = 0, id1 = 0;
+    float4 a0 = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b1 = b0;
+    if (h0) {
+      id0 = Ls[k0];
+      ld_rec(&kv.grid_raw[2 * id0], a0, b0);
+    }
+    if (h1) {
+      id1 = Ls[k1];
+      ld_rec(&kv.grid_raw[2 * id1], a1, b1);
+    }
+    const float beta20 = 2.0f * a0.w * EF_LN2, beta21 = 2.0f * a1.w * EF_LN2;
+    EikBwd s0, s1;
+    s0.sc = s0.sgx = s0.sgy = s0.sgz = s0.phx = s0.phy = s0.phz = s0.ss = s0.sdx = s0.sdy = s0.sdz = s0.pdx =
+        s0.pdy = s0.pdz = make_float2(0.f, 0.f);
+    s1 = s0;
+    if (base + 32 < n) {  // warp-uniform: two keys per lane
+#pragma unroll 1
+      for (int jp = 0; jp < np2; ++jp) {
+        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+        eik_bwd_pair<OFF>(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
+        eik_bwd_pair<OFF>(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
+      }
+    } else {
+#pragma unroll 2
+      for (int jp = 0; jp < np2; ++jp) {
+        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+        eik_bwd_pair<OFF>(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
+      }
+    }
+    if (h0) eik_red<OFF>(s0, a0, b0, (int)id0, kv.n_nodes, F.gpad);
+    if (h1) eik_red<OFF>(s1, a1, b1, (int)id1, kv.n_nodes, F.gpad);
   }
 }
 
@@ -179,12 +227,20 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
   Box box = warp_box(act, q.x, q.y, q.z, mh);
   box.thr += A.T_l;
   __syncwarp();  // the previous item's readers of L and S are done
-  uint32_t wn = 0;
+  // candidates split by bank: grid keys at L[0, wg), offset keys at LO[0, wo)
+  uint32_t* const LO = L + SCRATCH_HALF;
+  uint32_t wg = 0, wo = 0;
   stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
-    const uint32_t bal = __ballot_sync(~0u, pass);
-    if (pass) L[wn + __popc(bal & lanemask_lt())] = id;
-    wn += __popc(bal);
+    const bool grid = id < (uint32_t)kv.n_nodes;
+    const uint32_t bg = __ballot_sync(~0u, pass && grid), bo = __ballot_sync(~0u, pass && !grid);
+    if (pass) {
+      if (grid) L[wg + __popc(bg & lanemask_lt())] = id;
+      else LO[wo + __popc(bo & lanemask_lt())] = id;
+    }
+    wg += __popc(bg);
+    wo += __popc(bo);
   });
+  const uint32_t wn = wg + wo;
   __syncwarp();
   // 2. forward, lanes = queries
   EikFwd fa;
@@ -198,7 +254,7 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
       const uint32_t k = base + lane;
       float4 a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b = make_float4(0.f, 0.f, 0.f, 0.f);  // far: weight 0
       if (k < wn) {
-        const uint32_t id = L[k];
+        const uint32_t id = k < wg ? L[k] : LO[k - wg];
         ld_rec(&kv.grid_raw[2 * id], a, b);
       }
       __syncwarp();  // the previous round's readers are done
@@ -269,43 +325,10 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     pk(hz, S.pE[sl], false); pk(Tj, S.pE[sl], true);
   }
   __syncwarp();
-  // 4. backward, lanes = keys (two per lane)
+  // 4. backward, lanes = keys (two per lane), one bank at a time
   const int np2 = (((nact + 1) >> 1) + 1) & ~1;  // even (padding slots are idle queries)
-  for (uint32_t base = 0; base < wn; base += 64) {
-    const uint32_t k0 = base + lane, k1 = base + 32 + lane;
-    const bool h0 = k0 < wn, h1 = k1 < wn;
-    uint32_t id0 = 0, id1 = 0;
-    float4 a0 = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b1 = b0;
-    if (h0) {
-      id0 = L[k0];
-      ld_rec(&kv.grid_raw[2 * id0], a0, b0);
-    }
-    if (h1) {
-      id1 = L[k1];
-      ld_rec(&kv.grid_raw[2 * id1], a1, b1);
-    }
-    const float beta20 = 2.0f * a0.w * EF_LN2, beta21 = 2.0f * a1.w * EF_LN2;
-    EikBwd s0, s1;
-    s0.sc = s0.sgx = s0.sgy = s0.sgz = s0.phx = s0.phy = s0.phz = s0.ss = s0.sdx = s0.sdy = s0.sdz = s0.pdx =
-        s0.pdy = s0.pdz = make_float2(0.f, 0.f);
-    s1 = s0;
-    if (base + 32 < wn) {  // warp-uniform: two keys per lane
-#pragma unroll 1
-      for (int jp = 0; jp < np2; ++jp) {
-        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
-        eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
-        eik_bwd_pair(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
-      }
-    } else {
-#pragma unroll 2
-      for (int jp = 0; jp < np2; ++jp) {
-        const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
-        eik_bwd_pair(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
-      }
-    }
-    if (h0) eik_red(s0, a0, b0, (int)id0, kv.n_nodes, F.gpad);
-    if (h1) eik_red(s1, a1, b1, (int)id1, kv.n_nodes, F.gpad);
-  }
+  eik_bwd_segment<false>(F, kv, L, wg, S, np2);
+  eik_bwd_segment<true>(F, kv, LO, wo, S, np2);
 }
 
 __global__ void __launch_bounds__(32 * FE_WARPS, FE_MIN_WARPS / FE_WARPS) k_fit_eik(const FitArgs F) {
