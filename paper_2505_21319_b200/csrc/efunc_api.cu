@@ -183,9 +183,10 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   }
   if (J > h->J_cap) {
     dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
-    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->qmh);
+    dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->qmh); dfree(h->qf0);
     CK(dalloc(&h->q_bin, J));
     CK(dalloc(&h->qmh, J));
+    CK(dalloc(&h->qf0, J));
     CK(dalloc(&h->q_tmp, J));
     CK(dalloc(&h->q_order, J));
     CK(dalloc(&h->qs, J));
@@ -234,7 +235,7 @@ void free_all(efunc_t* h) {
   dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad);
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
-  dfree(h->qmh); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
+  dfree(h->qmh); dfree(h->qf0); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
@@ -276,11 +277,13 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
     // stable rank); the gather then runs in sorted order, so the shift bounds' key loads of
     // neighbouring threads hit the same cells
     h->launches += launch_scatter_only(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_order, s);
-    h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh, s);
+    h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh,
+                                            with_mh == 2 ? h->qf0 : nullptr, s);
   } else {
     h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
     if (with_mh)  // + the per-query shift bound
-      h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh, s);
+      h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh,
+                                              with_mh == 2 ? h->qf0 : nullptr, s);
     else
       h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
   }
@@ -308,6 +311,7 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   a.hs = h->hs;
   a.loss_part = h->loss_part;
   a.qmh = h->qmh;
+  a.qf0 = h->qf0;
   a.wl_pool = h->wl_pool;
   a.wl_cap = h->wl_cap;
   a.wl_off = h->wl_off;
@@ -439,7 +443,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   if (J > (int64_t)0x7fffffff) return fail(h, EFUNC_EINVAL, "J > 2^31-1 per call");
   h->have_fwd = 0;
   FwdArgs a;
-  RET(prep_queries(h, q, o, J, loss, a, s, eik ? 0 : 1));  // k_fit_eik bounds its own shifts
+  RET(prep_queries(h, q, o, J, loss, a, s, eik ? 2 : 1));  // + the shift keys' f0 for k_fit_eik
   a.O = O;
   a.G = nullptr;
   FitArgs f;

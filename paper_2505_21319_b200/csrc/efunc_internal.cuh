@@ -122,6 +122,7 @@ struct FwdArgs {
   float4* hs;             // sorted fused Eikonal upstream h (if loss eikonal)
   float* loss_part;       // per item partial loss
   float* qmh;             // sorted shift bound mh_j (k_item_lists -> k_forward_keys)
+  float* qf0;             // sorted f_j of the shift key (k_fit_eik), or null
   DevScalars* ds;
   int count_kept;
   // per-item candidate key ids handed to the backward (reserved: the brick list length)
@@ -202,7 +203,7 @@ int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom
 int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
                           float4* qs, int* perm, cudaStream_t s);
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
-                             float4* qs, int* perm, float* qmh, cudaStream_t s);
+                             float4* qs, int* perm, float* qmh, float* qf0, cudaStream_t s);
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
                         uint32_t* out_idx, cudaStream_t s);
 int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s);
@@ -281,6 +282,7 @@ struct efunc {
   float4* hs = nullptr;
   float* loss_part = nullptr;
   float* qmh = nullptr;
+  float* qf0 = nullptr;
   int64_t items_cap = 0;
   int4* items = nullptr;            // [items bound]
   uint32_t* wl_pool = nullptr;      // forward -> backward candidate ids

@@ -219,10 +219,10 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
   const int64_t js = (int64_t)it.x + lane;
   float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
   float mh = INFINITY, f0 = 0.f;
-  float3 g0 = make_float3(0.f, 0.f, 0.f);
-  if (act) {
+  if (act) {  // the shift bound and its key's f0 from k_gather_queries_mh
     q = A.qs[js];
-    shift_bound(kv, q, mh, f0, g0);
+    mh = A.qmh[js];
+    f0 = A.qf0[js];
   }
   Box box = warp_box(act, q.x, q.y, q.z, mh);
   box.thr += A.T_l;

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(32 * FK_WARPS, FK_MIN_BLOCKS / FK_WARPS) k_for
 // own-cell key loads run here at full occupancy instead of inside the FP32-bound k_fit.
 __global__ void k_gather_queries_mh(const KeysView kv, const uint32_t* __restrict__ order, const float* __restrict__ q,
                                     const float* __restrict__ o, int64_t J, float4* __restrict__ qs,
-                                    int* __restrict__ perm, float* __restrict__ qmh) {
+                                    int* __restrict__ perm, float* __restrict__ qmh, float* __restrict__ qf0) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < J; p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t j = order[p];
     const float4 v = make_float4(q[3 * (size_t)j], q[3 * (size_t)j + 1], q[3 * (size_t)j + 2], o ? o[j] : 0.0f);
@@ -400,14 +400,15 @@ __global__ void k_gather_queries_mh(const KeysView kv, const uint32_t* __restric
     float3 g0;
     shift_bound(kv, v, mh, f0, g0);
     qmh[p] = mh;
+    if (qf0) qf0[p] = f0;
   }
 }
 
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
-                             float4* qs, int* perm, float* qmh, cudaStream_t s) {
+                             float4* qs, int* perm, float* qmh, float* qf0, cudaStream_t s) {
   if (J == 0) return 0;
   const int64_t blocks = std::min<int64_t>((J + 255) / 256, 148 * 16);
-  k_gather_queries_mh<<<(unsigned)blocks, 256, 0, s>>>(kv, order, q, o, J, qs, perm, qmh);
+  k_gather_queries_mh<<<(unsigned)blocks, 256, 0, s>>>(kv, order, q, o, J, qs, perm, qmh, qf0);
   return 1;
 }
 
