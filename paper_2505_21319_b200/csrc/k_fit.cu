@@ -30,6 +30,14 @@
 
 namespace ef {
 
+#ifndef FT_B1_UNROLL
+#define FT_B1_UNROLL 8  // one-key backward query-pair loop (measured 2/4/8: 8 best by ~0.4%)
+#endif
+#ifndef FT_B2_UNROLL
+#define FT_B2_UNROLL 1  // two-key backward query-pair loop
+#endif
+#define FT_PRAGMA(x) _Pragma(#x)
+#define FT_UNROLL(n) FT_PRAGMA(unroll n)
 #ifndef FT_MIN_WARPS
 #define FT_MIN_WARPS 16  // warps per SM (measured 16..28; the 16-pair forward needs 128 registers)
 #endif
@@ -199,7 +207,7 @@ __device__ __forceinline__ MseSums bwd_sums_x(const KeyX& K, const int npairs, c
   };
   // an even number of pairs (a padding slot is an idle query: qq = 1e30, rho = 0 -> exactly 0)
   const int np2 = (npairs + 1) & ~1;
-#pragma unroll 2
+  FT_UNROLL(FT_B1_UNROLL)
   for (int jp = 0; jp < np2; jp += 2) {
     pair(jp);
     pair(jp + 1);
@@ -244,7 +252,7 @@ __device__ __forceinline__ void bwd_sums_x2(const KeyX& KA, const KeyX& KB, cons
     Suq[u] = __ffma2_rn(uu, make_float2(QB.z, QB.w), Suq[u]);
   };
   const int np2 = (npairs + 1) & ~1;
-#pragma unroll 1
+  FT_UNROLL(FT_B2_UNROLL)
   for (int jp = 0; jp < np2; jp += 2) {
     const float4 QA0 = pA[jp], QB0 = pB[jp], QC0 = pC[jp];
     const float4 QA1 = pA[jp + 1], QB1 = pB[jp + 1], QC1 = pC[jp + 1];

@@ -26,6 +26,9 @@ namespace ef {
 #ifndef FE_FWD_UNROLL
 #define FE_FWD_UNROLL 16  // forward key-pair loop (measured 1/2/4/8/16: 16 best, C3 k_fit_eik 5.16 -> 5.06 ms)
 #endif
+#ifndef FE_BWD1_UNROLL
+#define FE_BWD1_UNROLL 2  // one-key backward query-pair loop (the last < 64 keys of a bank; 2/4/8 within noise)
+#endif
 #ifndef FE_BWD_UNROLL
 #define FE_BWD_UNROLL 1  // two-key backward query-pair loop (2 spills: slower)
 #endif
@@ -199,7 +202,7 @@ __device__ __forceinline__ void eik_bwd_segment(const FitArgs& F, const KeysView
         eik_bwd_pair<OFF>(a1, b1, beta21, QA, QB, QC, QD, QE, s1);
       }
     } else {
-#pragma unroll 2
+      FE_UNROLL(FE_BWD1_UNROLL)
       for (int jp = 0; jp < np2; ++jp) {
         const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
         eik_bwd_pair<OFF>(a0, b0, beta20, QA, QB, QC, QD, QE, s0);
