@@ -288,26 +288,3 @@ def mean_shift_offsets(R: int, surface_pts, bandwidth: float = 100.0) -> np.ndar
         W = np.exp(-(E - E.min(axis=1, keepdims=True)))
         out[i0:i0 + step] = (W @ s) / W.sum(axis=1, keepdims=True) - kk
     return out
-
-
-def fit_step(theta, m, v, step: int, q, o, hp: AdamW, J_global: int | None = None,
-             eikonal_lambda: float = 0.0, cutoff_T: float | None = None):
-    """One fit step (§3.4-3.6, §4.2): forward -> MSE (+Eikonal) -> backward -> AdamW.
-    Returns (theta, m, v, loss, grad)."""
-    f = forward(theta, R_of(theta), q, cutoff_T=cutoff_T)
-    L, r = mse_loss(f.O, o, J_global)
-    h = None
-    if eikonal_lambda:
-        LE, h = eikonal_loss(f.G, eikonal_lambda, J_global)
-        L += LE
-    grad = backward(theta, R_of(theta), q, f, r, h)
-    th, m2, v2 = adamw_step(theta, grad, m, v, step, hp)
-    return th, m2, v2, L, grad
-
-
-def R_of(theta) -> int:
-    n = np.asarray(theta).size // NCH
-    R = int(round(n ** (1.0 / 3.0)))
-    if R ** 3 * NCH != np.asarray(theta).size:
-        raise ValueError("theta is not R^3 x 13")
-    return R

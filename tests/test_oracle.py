@@ -391,3 +391,88 @@ def test_cutoff_truncation_error_small_at_default_T():
     assert t.kept.min() >= 1 and t.kept.max() < 2 * R ** 3
     ti = orc.forward(th, R, q, cutoff_T=float("inf"))
     np.testing.assert_allclose(ti.O, g.O, rtol=0, atol=0)
+
+
+# ----------------------------------------------------------------------------- kept-pair count pins
+def _node_theta(R, s=0.0):
+    """beta = e^s on both banks, Delta = 0 (offset keys on the lattice), zero polynomials."""
+    th = np.zeros((R ** 3, 13))
+    th[:, 0] = s
+    th[:, 8] = s
+    return th
+
+
+def test_kept_counts_lattice_points_at_a_node():
+    """oracle.kept against the three-square counts r3(n) (tests/golden, OEIS A005875): with
+    beta = 1, Delta = 0 and the query ON the centre node of R = 9 (h = 1/4, m_j = 0), the kept set of
+    the cutoff a_ij - m_j <= T (reading R-1) is every key with |v|^2 <= T/h^2, twice (both banks).
+    T sits halfway between shells, so a '<' vs '<=' slip or a missing shell shows."""
+    r3 = {int(a): int(b) for a, b in (ln.split() for ln in _golden_lines("r3_sum_of_three_squares.txt"))}
+    R, h = 9, 0.25
+    th = _node_theta(R)
+    q = np.zeros((1, 3))
+    for n in range(16):
+        T = (n + 0.5) * h * h
+        f = orc.forward(th, R, q, cutoff_T=T)
+        assert f.m[0] == 0.0
+        assert int(f.kept[0]) == 2 * sum(r3[k] for k in range(n + 1)), n
+
+
+def test_kept_counts_use_the_shifted_exponent():
+    """Off a node the test is a_ij - m_j <= T (shifted, m_j = min_i a_ij), not a_ij <= T: at
+    q = 0.3 h e_x the shifted and unshifted counts differ. Reference: integer-vector brute force."""
+    import itertools
+    R, h = 9, 0.25
+    th = _node_theta(R)
+    e = (0.3, 0.0, 0.0)
+    q = np.array([[0.3 * h, 0.0, 0.0]])
+    differs = 0
+    for t in (0.45, 1.2, 2.05, 3.3):
+        T = t * h * h
+        f = orc.forward(th, R, q, cutoff_T=T)
+        d2 = [sum((v[k] - e[k]) ** 2 for k in range(3)) for v in itertools.product(range(-4, 5), repeat=3)]
+        m2 = min(d2)
+        shifted = sum(1 for x in d2 if x - m2 <= t)
+        unshifted = sum(1 for x in d2 if x <= t)
+        assert int(f.kept[0]) == 2 * shifted, t
+        differs += shifted != unshifted
+    assert differs >= 2  # the pin discriminates shifted from unshifted exponents
+
+
+def test_kept_and_values_against_python_loop_brute_force():
+    """R = 2 and 3, random theta (beta spread, offsets) and out-of-domain queries: kept counts, O
+    and lambda against a plain Python double loop over (query, key) with the math module."""
+    for R, seed in ((2, 5), (3, 6)):
+        th = synth.random_theta(R, seed, log_scale_mean=1.0, log_scale_std=0.7, offset_std=0.2).astype(np.float64)
+        q = synth.rng(seed + 10).uniform(-1.4, 1.4, size=(12, 3))
+        T = 2.5
+        f = orc.forward(th, R, q, cutoff_T=T)
+        g = orc.forward(th, R, q)
+        t = [(-1.0 + 2.0 * i / (R - 1)) for i in range(R)]
+        keys = []
+        for z in range(R):
+            for y in range(R):
+                for x in range(R):
+                    n = x + R * (y + R * z)
+                    k = (float(np.float32(t[x])), float(np.float32(t[y])), float(np.float32(t[z])))
+                    keys.append((k, math.exp(th[n, 0]), th[n, 1], th[n, 2:5]))
+        for z in range(R):
+            for y in range(R):
+                for x in range(R):
+                    n = x + R * (y + R * z)
+                    k = keys[n][0]
+                    kd = (k[0] + th[n, 5], k[1] + th[n, 6], k[2] + th[n, 7])
+                    keys.append((kd, math.exp(th[n, 8]), th[n, 9], th[n, 10:13]))
+        for j in range(q.shape[0]):
+            a = []
+            fv = []
+            for (k, beta, c, gg) in keys:
+                d = [q[j, 0] - k[0], q[j, 1] - k[1], q[j, 2] - k[2]]
+                a.append(beta * (d[0] ** 2 + d[1] ** 2 + d[2] ** 2))
+                fv.append(c + gg[0] * d[0] + gg[1] * d[1] + gg[2] * d[2])
+            m = min(a)
+            assert int(f.kept[j]) == sum(1 for x in a if x - m <= T)
+            Z = sum(math.exp(-(x - m)) for x in a)
+            O = sum(math.exp(-(x - m)) * v for x, v in zip(a, fv)) / Z
+            assert abs(g.O[j] - O) <= 1e-12 * max(1.0, abs(O))
+            assert abs(g.lam[j] - (-m + math.log(Z))) <= 1e-12 * max(1.0, abs(m))
