@@ -3,6 +3,7 @@
 // file only validates arguments, sizes workspaces and enqueues launches on the caller's stream.
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -128,6 +129,24 @@ efunc_status ensure_scan_tmp(efunc_t* h, size_t n_elems) {
   return EFUNC_OK;
 }
 
+// scratch of the stable radix sort for up to n elements
+efunc_status ensure_radix(efunc_t* h, size_t n) {
+  if (n <= h->rk_cap) return EFUNC_OK;
+  drop_fit_graph(h);
+  dfree(h->rk);
+  dfree(h->rh);
+  CK(dalloc(&h->rk, 2 * n));
+  CK(dalloc(&h->rh, radix_hist_elems((uint32_t)n)));
+  h->rk_cap = n;
+  return ensure_scan_tmp(h, radix_hist_elems((uint32_t)n));
+}
+
+int bits_for(size_t nvals) {  // bits of the largest value nvals - 1
+  int b = 1;
+  while (b < 32 && ((size_t)1 << b) < nvals) ++b;
+  return b;
+}
+
 // S0 + key binning + brick lists. force = 1: theta was replaced wholesale, rebuild the lists
 // regardless of the Verlet skin.
 // degree 0 (Table 3 G-0: f = c): the g channels of both banks held at 0
@@ -148,8 +167,13 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   // the cell sort only when some offset key changed cell (k_prep_keys sets keys_resort)
   const uint32_t* gate = &h->ds->keys_resort;
   h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s, gate);
-  h->launches += launch_counting_sort(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_tmp,
-                                      h->key_order, s, gate);
+  // deterministic mode: stable (LSD radix) so the per-cell key order, and with it every list and
+  // summation order, repeats run to run; otherwise the atomic scatter (any in-cell order is valid)
+  if (h->cfg.deterministic)
+    h->launches += launch_stable_sort(h->key_cell, h->n_keys, bits_for((size_t)h->n_cells + 1), h->rk, h->rh,
+                                      h->scan_tmp, h->key_tmp, h->key_order, s, gate);
+  else
+    h->launches += launch_scatter_only(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_order, s, gate);
   h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
   // per-brick candidate lists for the next forward/backward (query independent)
   h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
@@ -166,6 +190,8 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
   if (bound > h->items_cap || J > h->J_cap) drop_fit_graph(h);
   if (bound > h->items_cap) {
     dfree(h->loss_part); dfree(h->items); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
+    dfree(h->item_o);
+    CK(dalloc(&h->item_o, bound));
     CK(dalloc(&h->loss_part, bound));
     CK(dalloc(&h->slow_items, bound));
     CK(dalloc(&h->items, bound));
@@ -181,6 +207,7 @@ efunc_status ensure_queries(efunc_t* h, int64_t J) {
     CK(dalloc(&h->wl_pool, (size_t)want));
     h->wl_cap = (uint32_t)want;
   }
+  RET(ensure_radix(h, (size_t)J));
   if (J > h->J_cap) {
     dfree(h->q_bin); dfree(h->q_tmp); dfree(h->q_order); dfree(h->qs); dfree(h->perm);
     dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs); dfree(h->qmh); dfree(h->qf0);
@@ -232,13 +259,13 @@ void free_all(efunc_t* h) {
   dfree(h->theta); dfree(h->m); dfree(h->v);
   dfree(h->key_raw); dfree(h->key_sorted); dfree(h->kid); dfree(h->key_cell);
   dfree(h->cell_count); dfree(h->cell_start); dfree(h->cell_fill); dfree(h->key_tmp); dfree(h->key_order);
-  dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad);
+  dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad); dfree(h->rk); dfree(h->rh);
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
   dfree(h->qmh); dfree(h->qf0); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
-  dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items);
+  dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items); dfree(h->item_o);
   dfree(h->scratch); dfree(h->iota);
   drop_fit_graph(h);
   free_timing(h);
@@ -280,7 +307,8 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
     h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh,
                                             with_mh == 2 ? h->qf0 : nullptr, s);
   } else {
-    h->launches += launch_counting_sort(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_tmp, h->q_order, s);
+    h->launches += launch_stable_sort(h->q_bin, (uint32_t)J, bits_for(nbins), h->rk, h->rh, h->scan_tmp, h->q_tmp,
+                                      h->q_order, s);
     if (with_mh)  // + the per-query shift bound
       h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh,
                                               with_mh == 2 ? h->qf0 : nullptr, s);
@@ -423,6 +451,16 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   return EFUNC_OK;
 }
 
+// EFUNC_FIT_PRE=1: the items' candidate lists are built by k_fit_lists before k_fit (measured
+// slower than k_fit building them itself; kept for A/B runs)
+int fit_pre_off() {
+  static const int off = [] {
+    const char* e = std::getenv("EFUNC_FIT_PRE");
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return off;
+}
+
 // efunc_forward_backward: the fused fit kernel for the MSE loss (k_fit.cu), the split kernels for
 // its leftover items; forward + backward otherwise.
 efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -451,7 +489,12 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.gpad = h->gpad;
   f.scratch = h->scratch;
   f.iota = h->iota;
+  f.item_o = h->item_o;
+  // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
+  // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
+  f.pre = (!eik && !h->iota && !fit_pre_off()) ? 1 : 0;
   const int slot = timing_begin(h, s);
+  if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
   h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
   timing_end(h, slot, s);
   // items the fused kernel left (no brick list / shift-bound overflow): the split kernels
@@ -733,6 +776,7 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     }
     CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
     RET(ensure_scan_tmp(h, h->n_cells + 1));
+    RET(ensure_radix(h, (size_t)h->n_keys));
     if (theta_host) CK(cudaMemcpy(h->theta, theta_host, np * sizeof(float), cudaMemcpyHostToDevice));
     else CK(cudaMemset(h->theta, 0, np * sizeof(float)));
     CK(cudaMemset(h->m, 0, np * sizeof(float)));
@@ -1010,6 +1054,7 @@ efunc_status efunc_set_timing(efunc_t* h, int32_t slots) {
   if (slots < 0 || slots > 4096) return fail(h, EFUNC_EINVAL, "slots must be in [0, 4096]");
   DeviceGuard dg(h->cfg.device);
   CK(cudaDeviceSynchronize());
+  drop_fit_graph(h);  // a captured fit step records into the events about to be destroyed
   free_timing(h);
   for (int i = 0; i < 2 * slots; ++i) {
     cudaEvent_t e = nullptr;

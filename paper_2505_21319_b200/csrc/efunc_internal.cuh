@@ -169,6 +169,8 @@ struct FitArgs {
   float* gpad;            // [R^3][16] padded gradient accumulator
   uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
   const uint32_t* iota;   // dense mode (cutoff_T = inf): 0 .. 2R^3-1, every key a candidate; else null
+  int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
+  float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
 };
 
 constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
@@ -189,9 +191,9 @@ int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, Dev
                          cudaStream_t s);
 int launch_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* block_tmp,
                     cudaStream_t s, const uint32_t* gate = nullptr);
-int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start,
-                         uint32_t* fill, uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s,
-                         const uint32_t* gate = nullptr);
+size_t radix_hist_elems(uint32_t n);
+int launch_stable_sort(const uint32_t* bin, uint32_t n, int bits, uint32_t* rk, uint32_t* hist, uint32_t* scan_tmp,
+                       uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s, const uint32_t* gate = nullptr);
 int launch_gather_keys(const uint32_t* order, const float4* key_raw, float4* key_sorted,
                        int* kid, uint32_t n, cudaStream_t s);
 int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint32_t* pool,
@@ -205,7 +207,7 @@ int launch_gather_queries(const uint32_t* order, const float* q, const float* o,
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
                              float4* qs, int* perm, float* qmh, float* qf0, cudaStream_t s);
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
-                        uint32_t* out_idx, cudaStream_t s);
+                        uint32_t* out_idx, cudaStream_t s, const uint32_t* gate = nullptr);
 int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s);
 int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
                        cudaStream_t s);
@@ -213,6 +215,7 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
+int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
@@ -254,6 +257,9 @@ struct efunc {
   uint32_t* key_order = nullptr;
   uint32_t* scan_tmp = nullptr;     // block sums for scans
   size_t scan_tmp_cap = 0;
+  uint32_t* rk = nullptr;           // stable radix sort: 2 x rk_cap u32 key ping-pong
+  uint32_t* rh = nullptr;           // its digit histograms (radix_hist_elems(rk_cap))
+  size_t rk_cap = 0;
   ef::DevScalars* ds = nullptr;
   float* fit_grad = nullptr;
   float* gpad = nullptr;            // [R^3][16] padded gradient accumulator (kept zero between calls)
@@ -290,6 +296,7 @@ struct efunc {
   uint32_t* wl_off = nullptr;       // [items bound]
   uint32_t* wl_n = nullptr;         // [items bound]
   uint32_t* slow_items = nullptr;   // [items bound]
+  float4* item_o = nullptr;         // [items bound] item box centres (k_fit_lists -> k_fit)
   uint32_t* iota = nullptr;         // dense mode: key ids 0 .. 2R^3-1 (k_fit candidate list)
   uint32_t* scratch = nullptr;      // per-warp id scratch (k_fit, k_brick_lists): SCRATCH_WARPS x SCRATCH_STRIDE
   int64_t fwd_items_bound = 0;

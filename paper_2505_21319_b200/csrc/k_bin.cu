@@ -207,18 +207,67 @@ __global__ void k_scatter(const uint32_t* __restrict__ bin, uint32_t n, const ui
   }
 }
 
-// Rank of each element inside its bin = number of same-bin elements with a smaller index.
-__global__ void k_stable_rank(const uint32_t* __restrict__ bin, uint32_t n, const uint32_t* __restrict__ bin_start,
-                              const uint32_t* __restrict__ tmp_idx, uint32_t* __restrict__ out_idx,
-                              const uint32_t* gate) {
+// ---- stable sort by bin: LSD radix sort, 8-bit digits (deterministic, O(n) per pass)
+// Pass p orders the elements by digit p of their bin, stably: a tile's elements keep their input
+// order inside each digit (ranks from __match_any_sync within a warp and per-warp digit counts in
+// shared memory, chunk by chunk in index order). After ceil(bits/8) passes the elements are sorted
+// by bin and, inside a bin, by their original index: the order does not depend on scheduling.
+constexpr int RX_T = 256, RX_CHUNKS = 16, RX_TILE = RX_T * RX_CHUNKS, RX_W = RX_T / 32;
+
+__global__ void __launch_bounds__(RX_T) k_radix_hist(const uint32_t* __restrict__ key, uint32_t n, int shift,
+                                                      uint32_t* __restrict__ hist, uint32_t ntiles,
+                                                      const uint32_t* gate) {
   GATED;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    const uint32_t i = tmp_idx[p];
-    const uint32_t b = bin[i];
-    const uint32_t s = bin_start[b], e = bin_start[b + 1];
-    uint32_t rank = 0;
-    for (uint32_t k = s; k < e; ++k) rank += (tmp_idx[k] < i) ? 1u : 0u;
-    out_idx[s + rank] = i;
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * RX_TILE;
+  for (int c = 0; c < RX_CHUNKS; ++c) {
+    const uint32_t e = base + c * RX_T + threadIdx.x;
+    if (e < n) atomicAdd(&h[(key[e] >> shift) & 255u], 1u);  // counts: order-independent
+  }
+  __syncthreads();
+  hist[threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];  // digit-major: one scan gives offsets
+}
+
+__global__ void __launch_bounds__(RX_T) k_radix_scatter(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val,
+                                                         uint32_t n, int shift, const uint32_t* __restrict__ off,
+                                                         uint32_t ntiles, uint32_t* __restrict__ key_out,
+                                                         uint32_t* __restrict__ val_out, const uint32_t* gate) {
+  GATED;
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wc[RX_W][256];
+  const int w = threadIdx.x >> 5;
+  run[threadIdx.x] = off[threadIdx.x * ntiles + blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < RX_W; ++k) wc[k][threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * RX_TILE;
+  for (int c = 0; c < RX_CHUNKS; ++c) {
+    const uint32_t e = base + c * RX_T + threadIdx.x;
+    const bool valid = e < n;
+    const uint32_t k = valid ? key[e] : 0u;
+    const uint32_t v = valid ? (val ? val[e] : e) : 0u;
+    const uint32_t d = valid ? ((k >> shift) & 255u) : 256u;
+    const uint32_t peers = __match_any_sync(~0u, d);
+    const uint32_t rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+    if (valid && rank == 0) wc[w][d] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t pre = run[d] + rank;
+      for (int k2 = 0; k2 < w; ++k2) pre += wc[k2][d];
+      if (key_out) key_out[pre] = k;
+      val_out[pre] = v;
+    }
+    __syncthreads();
+    uint32_t add = 0;
+#pragma unroll
+    for (int k2 = 0; k2 < RX_W; ++k2) {
+      add += wc[k2][threadIdx.x];
+      wc[k2][threadIdx.x] = 0;
+    }
+    run[threadIdx.x] += add;
+    __syncthreads();
   }
 }
 
@@ -229,19 +278,38 @@ static int grid_for(uint32_t n, int threads) {
   return (int)b;
 }
 
-int launch_counting_sort(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
-                          uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s, const uint32_t* gate) {
+size_t radix_hist_elems(uint32_t n) { return (size_t)256 * ((n + RX_TILE - 1) / RX_TILE); }
+
+// Stable sort of the indices 0..n-1 by bin[i] < 2^bits into out_idx. rk: 2n u32 key scratch,
+// tmp_idx: n u32 value scratch, hist: radix_hist_elems(n) u32, scan_tmp: the scan's tile sums.
+int launch_stable_sort(const uint32_t* bin, uint32_t n, int bits, uint32_t* rk, uint32_t* hist, uint32_t* scan_tmp,
+                       uint32_t* tmp_idx, uint32_t* out_idx, cudaStream_t s, const uint32_t* gate) {
   if (n == 0) return 0;
-  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, tmp_idx, gate);
-  k_stable_rank<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, tmp_idx, out_idx, gate);
-  return 2;
+  const uint32_t ntiles = (n + RX_TILE - 1) / RX_TILE;
+  const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
+  int launches = 0;
+  const uint32_t* kin = bin;
+  const uint32_t* vin = nullptr;  // identity on the first pass
+  for (int p = 0; p < passes; ++p) {
+    const bool last = p == passes - 1;
+    // ping-pong so that the last pass lands in out_idx
+    uint32_t* vout = last ? out_idx : (((passes - 1 - p) & 1) ? tmp_idx : out_idx);
+    uint32_t* kout = last ? nullptr : rk + (size_t)(p & 1) * n;
+    k_radix_hist<<<ntiles, RX_T, 0, s>>>(kin, n, 8 * p, hist, ntiles, gate);
+    launches += 1 + launch_scan_u32(hist, hist, 256u * ntiles, scan_tmp, s, gate);
+    k_radix_scatter<<<ntiles, RX_T, 0, s>>>(kin, vin, n, 8 * p, hist, ntiles, kout, vout, gate);
+    ++launches;
+    kin = kout;
+    vin = vout;
+  }
+  return launches;
 }
 
 // The counting sort without the stable rank (bin order only; within a bin, atomics' order).
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
-                        uint32_t* out_idx, cudaStream_t s) {
+                        uint32_t* out_idx, cudaStream_t s, const uint32_t* gate) {
   if (n == 0) return 0;
-  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, out_idx, nullptr);
+  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(bin, n, bin_start, fill, out_idx, gate);
   return 1;
 }
 

@@ -480,6 +480,16 @@ __device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint3
   const int4 it = A.items[item];
   const int nact = it.y;
   const bool dense = F.iota != nullptr;  // cutoff_T = inf: every key is a candidate, no lists
+  if (F.pre) {  // k_fit_lists built this item's candidate ids (unless it had no list / no room)
+    const uint32_t pn = __ldcg(&A.wl_n[item]);
+    if (pn != BL_OVERFLOW) {
+      L = A.wl_pool + __ldcg(&A.wl_off[item]);
+      wn = pn;
+      const float4 oo = __ldcg(&F.item_o[item]);
+      o = make_float3(oo.x, oo.y, oo.z);
+      return IT_NORMAL;
+    }
+  }
   uint32_t nb = BL_OVERFLOW;
   if (it.z >= 0) nb = dense ? 0u : __ldg(&kv.bl_n[it.z]);
   if (nb == BL_OVERFLOW) {
@@ -650,6 +660,59 @@ __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(
     if (item < 0) break;
     fit_item(F, (uint32_t)item, smem[w], L);
   }
+}
+
+// The list phase of k_fit as its own launch: per item, the box of its queries (threshold
+// max_j mh_j + T) tested against every key of its brick's list, the passing ids written to the
+// item's slice of wl_pool (reserved: the brick list length), and the box centre. Latency-bound
+// (id -> key record -> test): few registers, 16 warps per CTA, the whole SM's warp slots.
+constexpr int FL_WARPS = 16;
+#ifndef FL_UNROLL
+#define FL_UNROLL 2  // list batches of 32 in flight per warp (48 warps/SM hide the rest)
+#endif
+__global__ void __launch_bounds__(32 * FL_WARPS, 3) k_fit_lists(const FitArgs F) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const uint32_t item = blockIdx.x * FL_WARPS + (threadIdx.x >> 5);
+  if (item >= *A.n_items) return;
+  const int4 it = A.items[item];
+  const bool act = lane < it.y;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY;
+  if (act) {
+    q = A.qs[js];
+    mh = A.qmh[js];
+  }
+  uint32_t nb = BL_OVERFLOW, base = 0;
+  if (it.z >= 0) nb = __ldg(&kv.bl_n[it.z]);
+  if (lane == 0 && nb != BL_OVERFLOW) base = atomicAdd(&A.ds->wl_top, nb);
+  base = __shfl_sync(~0u, base, 0);
+  Box box = warp_box(act, q.x, q.y, q.z, mh);
+  box.thr += A.T_l;
+  if (nb == BL_OVERFLOW || base + nb > A.wl_cap) {  // k_fit handles the item (enumerate / split kernels)
+    if (lane == 0) A.wl_n[item] = BL_OVERFLOW;
+    return;
+  }
+  uint32_t cnt = 0;
+  uint32_t* out = A.wl_pool + base;
+  stream_list<FL_UNROLL>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {
+    const uint32_t bal = __ballot_sync(~0u, pass);
+    if (pass) out[cnt + __popc(bal & lanemask_lt())] = id;
+    cnt += __popc(bal);
+  });
+  if (lane == 0) {
+    A.wl_off[item] = base;
+    A.wl_n[item] = cnt;
+    F.item_o[item] = make_float4(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz), 0.f);
+  }
+}
+
+int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  k_fit_lists<<<(unsigned)((n_items + FL_WARPS - 1) / FL_WARPS), 32 * FL_WARPS, 0, s>>>(a);
+  return 1;
 }
 
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s) {

@@ -293,7 +293,7 @@ __device__ __forceinline__ void eik_item(const FitArgs& F, const uint32_t item, 
     Oj = f0 + M * iz;
     nlam = mh - log2f(Z);
     const float c2 = 2.0f * EF_LN2 * iz;
-    const float Of = Oj - f0;
+    const float Of = M * iz;  // O - f0 before rounding O (PoU: Oj - f0 would round to 0)
     const float Gx = fmaf(hsum(fa.sgx), iz, c2 * fmaf(Of, hsum(fa.sux), -hsum(fa.sfx)));
     const float Gy = fmaf(hsum(fa.sgy), iz, c2 * fmaf(Of, hsum(fa.suy), -hsum(fa.sfy)));
     const float Gz = fmaf(hsum(fa.sgz), iz, c2 * fmaf(Of, hsum(fa.suz), -hsum(fa.sfz)));

@@ -218,7 +218,7 @@ __device__ __forceinline__ void forward_item(const FwdArgs& A, const uint32_t it
     float Gx = 0.f, Gy = 0.f, Gz = 0.f;
     if (WANT_G) {
       const float c2 = 2.0f * EF_LN2 * iz;
-      const float Of = O - f0[u];
+      const float Of = t.M * iz;  // O - f0 before rounding O: (O - f0) loses M/Z below ulp(O)
       Gx = g0[u].x + (t.sgx * iz + c2 * fmaf(Of, t.sux, -t.sfx));
       Gy = g0[u].y + (t.sgy * iz + c2 * fmaf(Of, t.suy, -t.sfy));
       Gz = g0[u].z + (t.sgz * iz + c2 * fmaf(Of, t.suz, -t.sfz));

@@ -119,6 +119,23 @@ def _check_dev(t, name, numel, device):
         raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
 
 
+def _check_io(t, name, numel, device, host, pinned=False):
+    """fit_step inputs: CUDA tensors on the handle's device, or host (CPU) tensors for host_io
+    (pinned when the copy is pipelined): float32, contiguous, exactly numel elements."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float32 torch tensor")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+    if host:
+        if t.device.type != "cpu":
+            raise ValueError(f"{name} must be a host tensor like q")
+        if pinned and not t.is_pinned():
+            raise ValueError(f"{name} must be pinned host memory for pipelined host I/O")
+    elif t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name} must live on cuda:{device}")
+
+
 @dataclass
 class AdamW:
     lr: float = 6e-4
@@ -263,6 +280,11 @@ class EFunc:
         lc = Loss(loss, eikonal_lambda, J_global)
         p = hp.c()
         host = q.device.type == "cpu"
+        _check_io(q, "q", 3 * J * self.S, self.device, host, pinned=host and pipelined)
+        _check_io(o, "o", J * self.S, self.device, host, pinned=host and pipelined)
+        _check_dev(grad_ws, "grad_ws", self.n_params, self.device)
+        if not host:
+            _check_dev(loss_out, "loss_out", self.S, self.device)
         if host and pipelined:
             lo = (C.c_float * self.S)()
             self._aio_keep = (getattr(self, "_aio_keep", []) + [(lo, q, o)])[-4:]  # alive until reused

@@ -86,11 +86,12 @@ def test_partition_of_unity_on_gpu():
     eO = nw(O.cpu().numpy(), exact)
     eG = nw(G.cpu().numpy(), np.broadcast_to(B, (q.shape[0], 3)))
     assert eO <= 2e-6, eO
-    # G's u-term sums p * 2 beta d (O - f): it amplifies the fp32 rounding of f (~1e-8 at
-    # |f - f0| ~ 0.1) by 2 beta |d| ~ 300; on this adversarial exactly-linear field with beta up
-    # to e^8 that reaches ~1.5e-5 normwise (reading R-T). Fitted states: see the C1/C2
-    # parity tests, which hold 1e-5.
-    assert eG <= 3e-5, eG
+    # G's u-term 2((O - f0) S_u - S_uf)/Z takes O - f0 = M/Z before O is rounded (in fp32,
+    # O - f0 would lose M/Z below ulp(O) and leave (M/Z) S_u unbalanced, ~5e-6 here)
+    for a in range(3):
+        eGa = nw(G.cpu().numpy()[:, a], np.full(q.shape[0], B[a]))
+        assert eGa <= TOL_VAL, (a, eGa)
+    assert eG <= TOL_VAL, eG
 
 
 def test_eval_grad_matches_forward_and_oracle():
@@ -242,7 +243,15 @@ def test_c2_pou_full_size():
     m = ef.EFunc(R, th.astype(np.float32))
     O, G, _ = m.forward(dev(q), want_G=True)
     assert nw(O.cpu().numpy(), A + q.astype(np.float64) @ B) <= 2e-6
-    assert np.abs(G.cpu().numpy() - B[None]).max() <= 5e-5
+    # c_i = A + B.k_i rounded to float32 is PoU only up to ulp(c_i): f_i then differ by ~3e-8 and
+    # G's u-term amplifies that by 2 beta |d| (the oracle sees the same float32 theta). So G is
+    # compared with the oracle at sampled queries (1e-5 per component), and with B loosely.
+    Gn = G.cpu().numpy()
+    idx = synth.rng(44).choice(J, size=2048, replace=False)
+    ref = orc.forward(th.astype(np.float32), R, q[idx])
+    for a in range(3):
+        assert nw(Gn[idx, a], ref.G[:, a]) <= TOL_VAL, a
+        assert nw(Gn[:, a], np.full(J, B[a])) <= 3e-5, a
     # sum_i dL/dc_i = sum_j r_j (softmax sums to one)
     r = synth.rng(43).normal(size=J).astype(np.float32) / J
     g = m.backward(dL_dO=dev(r)).cpu().numpy().astype(np.float64)
@@ -284,7 +293,8 @@ def test_large_beta_spread_takes_exact_shift_path():
     O, G, _ = m.forward(dev(q), want_G=True)
     ref = orc.forward(th, R, q)
     assert nw(O.cpu().numpy(), ref.O) <= TOL_VAL
-    assert nw(G.cpu().numpy(), ref.G) <= 1e-4
+    for a in range(3):
+        assert nw(G.cpu().numpy()[:, a], ref.G[:, a]) <= TOL_VAL, a
 
 
 def test_nonfinite_query_reported():
@@ -785,3 +795,32 @@ def test_fit_linear_field_to_zero_and_torus_loss_drops():
         m2.fit_step(dev(q), dev(o), loss_out=lo)
         tl.append(float(lo.item()))
     assert np.mean(tl[-20:]) < 0.65 * np.mean(tl[:20]), (np.mean(tl[:20]), np.mean(tl[-20:]))
+
+
+def test_eval_grad_padded_lattice_many_out_of_domain_queries():
+    """A lattice over a padded box: ~35% of the queries lie outside [-1,1]^3 and share
+    the out-of-domain bin. The stable sort (LSD radix, O(n) per pass) keeps this fast, and the
+    outside queries (exact-shift split kernels) match the oracle."""
+    import time
+    R, N = 16, 96
+    th = synth.fitted_like_theta(R, synth.Torus(), 181)
+    t = np.linspace(-1.15, 1.15, N, dtype=np.float32)
+    z, y, x = np.meshgrid(t, t, t, indexing="ij")
+    q = np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1).astype(np.float32)
+    outside = np.any(np.abs(q) > 1.0, axis=1)
+    assert outside.mean() > 0.3
+    m = ef.EFunc(R, th)
+    qd = dev(q)
+    m.eval_grad(qd)  # warm-up (sizes the workspaces)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    O, G = m.eval_grad(qd)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 5.0
+    rs = synth.rng(182)
+    idx = np.concatenate([rs.choice(np.where(outside)[0], 150, replace=False),
+                          rs.choice(np.where(~outside)[0], 150, replace=False)])
+    ref = orc.forward(th, R, q[idx])
+    assert nw(O.cpu().numpy()[idx], ref.O) <= TOL_VAL
+    for a in range(3):
+        assert nw(G.cpu().numpy()[idx, a], ref.G[:, a]) <= TOL_VAL

@@ -476,3 +476,22 @@ def test_kept_and_values_against_python_loop_brute_force():
             O = sum(math.exp(-(x - m)) * v for x, v in zip(a, fv)) / Z
             assert abs(g.O[j] - O) <= 1e-12 * max(1.0, abs(O))
             assert abs(g.lam[j] - (-m + math.log(Z))) <= 1e-12 * max(1.0, abs(m))
+
+
+def test_sharded_oracle_driver_equals_single_process():
+    """oracle.parallel runs the oracle unchanged on query shards; per-query outputs concatenate and
+    shard gradients add up to the full-batch gradient (additivity)."""
+    from oracle import parallel as par
+    R = 4
+    th = synth.random_theta(R, 17, log_scale_mean=2.0).astype(np.float64)
+    q = synth.rng(18).uniform(-1, 1, size=(37, 3))
+    o = synth.rng(19).normal(size=37)
+    f, L, g = par.fit_eval(th, R, q, o, lam_e=0.1, procs=3)
+    f1 = orc.forward(th, R, q)
+    Lm, r = orc.mse_loss(f1.O, o)
+    Le, h = orc.eikonal_loss(f1.G, 0.1)
+    g1 = orc.backward(th, R, q, f1, r, h)
+    np.testing.assert_allclose(f.O, f1.O, rtol=0, atol=0)
+    np.testing.assert_allclose(f.G, f1.G, rtol=0, atol=0)
+    assert abs(L - (Lm + Le)) <= 1e-14 * (Lm + Le)
+    np.testing.assert_allclose(g, g1, rtol=1e-12, atol=1e-14)

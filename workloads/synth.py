@@ -207,6 +207,24 @@ def sample_batch(shape: Shape, J: int, seed: int, stream: int = 0, sigma: float 
     return np.ascontiguousarray(q), np.ascontiguousarray(o)
 
 
+def sample_patch(shape: Shape, J: int, seed: int, radius: float = 0.06, sigma: float = 0.01):
+    """(q, o): J near-surface points (surface sample + N(0, sigma^2)) confined to the surface patch
+    within `radius` of one surface point: a full-density batch, every work item holds 32 queries
+    (the near-surface density of C2/C3 at a size the float64 oracle finishes in seconds)."""
+    g = rng(seed, 2000)
+    centre = shape.sample_surface(1, g)[0]
+    pts = []
+    have = 0
+    while have < J:
+        p = shape.sample_surface(8 * J, g)
+        p = p[np.linalg.norm(p - centre, axis=1) <= radius]
+        pts.append(p)
+        have += p.shape[0]
+    q = (np.concatenate(pts)[:J] + g.normal(scale=sigma, size=(J, 3))).astype(np.float32)
+    o = shape.sdf(q.astype(np.float64)).astype(np.float32)
+    return np.ascontiguousarray(q), np.ascontiguousarray(o)
+
+
 def surface_points(shape: Shape, N: int, seed: int) -> np.ndarray:
     """N surface samples (N = 16384 for mean-shift)."""
     return shape.sample_surface(N, rng(seed, 7)).astype(np.float32)
