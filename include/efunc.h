@@ -201,6 +201,30 @@ EFUNC_API efunc_status efunc_sync(efunc_t* h);
 EFUNC_API efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, float bandwidth,
                                    void* stream);
 
+/* efunc_mesh — inference to a mesh. PAPER.md:L680 (§4.1): "we first
+ * evaluate O(q) at 512-resolution grid points. Then, we use Marching Cubes on the resulting
+ * grid"; PAPER.md:L962-971 (§4.5): the normals come from "a single forward pass" of
+ * Eq. func-normal (L425-436).
+ *   1. O at the N^3 lattice nodes p(i,j,k) = lo + (hi - lo) * (i,j,k) / (N-1), node
+ *      n = i + N (j + N k), evaluated through the forward path in z-slabs;
+ *   2. Marching Cubes at `iso`: one vertex per lattice edge whose end nodes lie on different
+ *      sides (O < iso is inside), at the linear interpolation of O along the edge, shared by
+ *      the cubes around that edge (indexed, closed mesh away from the lattice boundary);
+ *      triangles are wound so their right-hand normal points from O < iso to O > iso;
+ *   3. normals[v] = G/|G| at every vertex (one eval_grad pass; 0 where G = 0).
+ *   N in [2, 1024]; lo3, hi3 host float[3] with hi3 > lo3 per axis.
+ *   lattice_O: dev float[N^3] or NULL (receives the node values).
+ *   verts, normals: dev float[max_verts*3]; tris: dev int32[max_tris*3] (vertex indices).
+ *   n_verts, n_tris: host int64 outputs, required.
+ * If verts/tris are NULL or too small, only the counts (and lattice_O) are produced and the
+ * call returns EFUNC_OK: allocate and call again. normals may be NULL (skipped).
+ * Synchronises `stream`; invalidates the saved forward state; not for batched handles.
+ * Errors: EINVAL (N, box, NULL counts, n_shapes > 1), ENOMEM, ECUDA. */
+EFUNC_API efunc_status efunc_mesh(efunc_t* h, int32_t N, const float* lo3, const float* hi3, float iso,
+                                  float* lattice_O, float* verts, float* normals, int32_t* tris,
+                                  int64_t max_verts, int64_t max_tris, int64_t* n_verts, int64_t* n_tris,
+                                  void* stream);
+
 /* Parameter / optimizer-state access. on_device=1: ptr is a device pointer, else host.
  * These synchronise the stream. set_params rebuilds keys and clears the saved state. */
 EFUNC_API efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream);

@@ -461,6 +461,16 @@ int fit_pre_off() {
   return off;
 }
 
+// EFUNC_FIT_PIPE=0: k_fit builds each item's candidate list before its forward instead of during
+// the previous item's backward (kept for A/B runs)
+int fit_pipe_on() {
+  static const int on = [] {
+    const char* e = std::getenv("EFUNC_FIT_PIPE");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
 // efunc_forward_backward: the fused fit kernel for the MSE loss (k_fit.cu), the split kernels for
 // its leftover items; forward + backward otherwise.
 efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -493,6 +503,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
   f.pre = (!eik && !h->iota && !fit_pre_off()) ? 1 : 0;
+  f.pipe = fit_pipe_on();
   const int slot = timing_begin(h, s);
   if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
   h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
@@ -883,6 +894,99 @@ efunc_status efunc_eval_grad(efunc_t* h, const float* q, int64_t J, float* O, fl
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
   return do_forward(h, q, nullptr, J, nullptr, O, G, nullptr, 0, (cudaStream_t)stream);
+}
+
+// NEXT-3: lattice O (forward path in z-slabs) -> Marching Cubes (k_mesh.cu) -> vertex normals
+// (one eval_grad pass). Scratch is allocated per call: the call synchronises anyway.
+efunc_status efunc_mesh(efunc_t* h, int32_t N, const float* lo3, const float* hi3, float iso, float* lattice_O,
+                        float* verts, float* normals, int32_t* tris, int64_t max_verts, int64_t max_tris,
+                        int64_t* n_verts, int64_t* n_tris, void* stream) {
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (!h->kids.empty()) return fail(h, EFUNC_EINVAL, "efunc_mesh: batched handle (n_shapes > 1)");
+  if (N < 2 || N > 1024) return fail(h, EFUNC_EINVAL, "efunc_mesh: N must be in [2, 1024]");
+  if (!lo3 || !hi3 || !n_verts || !n_tris) return fail(h, EFUNC_EINVAL, "efunc_mesh: NULL lo/hi/count pointer");
+  for (int a = 0; a < 3; ++a)
+    if (!(hi3[a] > lo3[a]) || !std::isfinite(lo3[a]) || !std::isfinite(hi3[a]))
+      return fail(h, EFUNC_EINVAL, "efunc_mesh: need finite hi > lo on every axis");
+  if (!std::isfinite(iso)) return fail(h, EFUNC_EINVAL, "efunc_mesh: iso must be finite");
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(mc_upload_table());
+  const int64_t NN = (int64_t)N * N, N3 = NN * N;
+  const float step[3] = {(hi3[0] - lo3[0]) / (float)(N - 1), (hi3[1] - lo3[1]) / (float)(N - 1),
+                         (hi3[2] - lo3[2]) / (float)(N - 1)};
+  float* O = lattice_O;
+  float* Own = nullptr;
+  float* q = nullptr;
+  uint8_t* mask = nullptr;
+  uint32_t *vcnt = nullptr, *voff = nullptr, *tcnt = nullptr, *toff = nullptr;
+  efunc_status st = EFUNC_OK;
+  auto cleanup = [&]() {
+    dfree(Own); dfree(q); dfree(mask); dfree(vcnt); dfree(voff); dfree(tcnt); dfree(toff);
+  };
+#define MCK(x)                                                                                    \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) {                                                                      \
+      cleanup();                                                                                  \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? EFUNC_ENOMEM : EFUNC_ECUDA,                \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                               \
+    }                                                                                             \
+  } while (0)
+  if (!O) {
+    MCK(dalloc(&Own, (size_t)N3));
+    O = Own;
+  }
+  // 1. node values, 2^23 lattice points per slab
+  const int nk = (int)std::max<int64_t>(1, std::min<int64_t>(N, ((int64_t)1 << 23) / NN));
+  MCK(dalloc(&q, (size_t)(3 * NN * nk)));
+  for (int k0 = 0; k0 < N; k0 += nk) {
+    const int nz = std::min(nk, N - k0);
+    h->launches += launch_lattice_q(N, lo3, step, k0, nz, q, s);
+    st = do_forward(h, q, nullptr, NN * nz, nullptr, O + k0 * NN, nullptr, nullptr, 0, s);
+    if (st != EFUNC_OK) {
+      cleanup();
+      return st;
+    }
+  }
+  // 2. Marching Cubes: per-node edge masks and vertex counts, per-cube triangle counts, scans
+  MCK(dalloc(&mask, (size_t)N3));
+  MCK(dalloc(&vcnt, (size_t)N3 + 1));
+  MCK(dalloc(&voff, (size_t)N3 + 1));
+  MCK(dalloc(&tcnt, (size_t)N3 + 1));
+  MCK(dalloc(&toff, (size_t)N3 + 1));
+  st = ensure_scan_tmp(h, (size_t)N3 + 1);
+  if (st != EFUNC_OK) {
+    cleanup();
+    return st;
+  }
+  MCK(cudaMemsetAsync(vcnt + N3, 0, sizeof(uint32_t), s));
+  MCK(cudaMemsetAsync(tcnt + N3, 0, sizeof(uint32_t), s));
+  h->launches += launch_mc_count(O, N, iso, mask, vcnt, tcnt, s);
+  h->launches += launch_scan_u32(vcnt, voff, (uint32_t)(N3 + 1), h->scan_tmp, s);
+  h->launches += launch_scan_u32(tcnt, toff, (uint32_t)(N3 + 1), h->scan_tmp, s);
+  uint32_t tot[2] = {0, 0};
+  MCK(cudaMemcpyAsync(&tot[0], voff + N3, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  MCK(cudaMemcpyAsync(&tot[1], toff + N3, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  MCK(cudaStreamSynchronize(s));
+  *n_verts = tot[0];
+  *n_tris = tot[1];
+  if (verts && tris && (int64_t)tot[0] <= max_verts && (int64_t)tot[1] <= max_tris) {
+    h->launches += launch_mc_emit(O, N, iso, lo3, step, mask, voff, toff, verts, tris, s);
+    // 3. normals: G at the vertices (Eq. func-normal), normalised
+    if (normals && tot[0] > 0) {
+      st = do_forward(h, verts, nullptr, (int64_t)tot[0], nullptr, nullptr, normals, nullptr, 0, s);
+      if (st != EFUNC_OK) {
+        cleanup();
+        return st;
+      }
+      h->launches += launch_normalize3(normals, (int64_t)tot[0], s);
+    }
+  }
+  MCK(cudaStreamSynchronize(s));
+#undef MCK
+  cleanup();
+  return EFUNC_OK;
 }
 
 efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,

@@ -170,6 +170,7 @@ struct FitArgs {
   uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
   const uint32_t* iota;   // dense mode (cutoff_T = inf): 0 .. 2R^3-1, every key a candidate; else null
   int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
+  int pipe;               // 1: k_fit builds the next item's candidate ids during this item's backward
   float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
 };
 
@@ -232,6 +233,13 @@ int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float b
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
 int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s);
+// NEXT-3 (k_mesh.cu): lattice queries, Marching Cubes, vertex normals
+cudaError_t mc_upload_table();
+int launch_lattice_q(int N, const float* lo, const float* step, int k0, int nk, float* q, cudaStream_t s);
+int launch_mc_count(const float* O, int N, float iso, uint8_t* mask, uint32_t* vcnt, uint32_t* tcnt, cudaStream_t s);
+int launch_mc_emit(const float* O, int N, float iso, const float* lo, const float* step, const uint8_t* mask,
+                   const uint32_t* voff, const uint32_t* toff, float* verts, int32_t* tris, cudaStream_t s);
+int launch_normalize3(float* v, int64_t n, cudaStream_t s);
 
 }  // namespace ef
 

@@ -26,6 +26,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
             "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
             "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_sync", "efunc_last_error",
+            "efunc_mesh",
             "efunc_abi_version"]
 
 
@@ -90,6 +91,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_sync": [P],
         "efunc_set_timing": [P, i32],
         "efunc_get_kernel_ms": [P, P, i32],
+        "efunc_mesh": [P, i32, P, P, f32, P, P, P, P, i64, i64, C.POINTER(i64), C.POINTER(i64), P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -268,6 +270,32 @@ class EFunc:
         G = self._empty(J, 3) if want_G else None
         self._ok(self.lib.efunc_eval_grad(self.h, _ptr(q), J, _ptr(O), _ptr(G), self._stream()))
         return O, G
+
+    def mesh(self, N: int, lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0), iso: float = 0.0,
+             want_lattice: bool = False, want_normals: bool = True):
+        """NEXT-3: O on the N^3 lattice over [lo, hi], Marching Cubes at
+        iso, unit normals G/|G| at the vertices. Returns (verts [V,3], tris [T,3] int32,
+        normals [V,3] or None, lattice O [N,N,N] (z, y, x) or None), all on the handle's device."""
+        import torch
+        if self.S != 1:
+            raise ValueError("mesh() needs a single-shape handle")
+        lo3 = (C.c_float * 3)(*lo)
+        hi3 = (C.c_float * 3)(*hi)
+        nv, nt = C.c_int64(0), C.c_int64(0)
+        lat = self._empty(N * N * N) if want_lattice else None
+        V, T = 16 * N * N, 32 * N * N  # first guess (a surface crosses ~N^2 cells); retried if short
+        for _ in range(2):
+            verts = self._empty(max(V, 1), 3)
+            normals = self._empty(max(V, 1), 3) if want_normals else None
+            tris = torch.empty(max(T, 1), 3, dtype=torch.int32, device=f"cuda:{self.device}")
+            self._ok(self.lib.efunc_mesh(self.h, int(N), lo3, hi3, float(iso), _ptr(lat), _ptr(verts),
+                                         _ptr(normals), _ptr(tris), V, T, C.byref(nv), C.byref(nt), self._stream()))
+            if nv.value <= V and nt.value <= T:
+                break
+            V, T = nv.value, nt.value
+        V, T = nv.value, nt.value
+        return (verts[:V], tris[:T], None if normals is None else normals[:V],
+                None if lat is None else lat.view(N, N, N))
 
     def fit_step(self, q, o, hp: AdamW | None = None, loss: int = LOSS_MSE, eikonal_lambda: float = 0.1,
                  J_global: int = 0, grad_ws=None, loss_out=None, pipelined: bool = False):

@@ -495,3 +495,49 @@ def test_sharded_oracle_driver_equals_single_process():
     np.testing.assert_allclose(f.G, f1.G, rtol=0, atol=0)
     assert abs(L - (Lm + Le)) <= 1e-14 * (Lm + Le)
     np.testing.assert_allclose(g, g1, rtol=1e-12, atol=1e-14)
+
+
+def test_mc_vertices_brute_force_tiny_lattice():
+    """oracle.mesh_oracle.mc_vertices (Marching Cubes vertex placement) against a
+    plain triple loop over every lattice edge of a random 4^3 field."""
+    from oracle import mesh_oracle as mo
+    N, lo, hi = 4, (-1.0, -0.5, 0.0), (1.0, 0.5, 2.0)
+    O = synth.rng(31).normal(size=(N, N, N))
+    got = mo.mc_vertices(O, lo, hi, iso=0.1)
+    step = [(hi[a] - lo[a]) / (N - 1) for a in range(3)]
+    want = []
+    for k in range(N):
+        for j in range(N):
+            for i in range(N):
+                for (di, dj, dk) in ((1, 0, 0), (0, 1, 0), (0, 0, 1)):
+                    i1, j1, k1 = i + di, j + dj, k + dk
+                    if i1 >= N or j1 >= N or k1 >= N:
+                        continue
+                    v0, v1 = O[k, j, i], O[k1, j1, i1]
+                    if (v0 < 0.1) == (v1 < 0.1):
+                        continue
+                    t = (0.1 - v0) / (v1 - v0)
+                    p0 = [lo[0] + i * step[0], lo[1] + j * step[1], lo[2] + k * step[2]]
+                    p1 = [lo[0] + i1 * step[0], lo[1] + j1 * step[1], lo[2] + k1 * step[2]]
+                    want.append([p0[a] + t * (p1[a] - p0[a]) for a in range(3)])
+    want = np.array(want)
+    assert got.shape == want.shape
+    key = lambda a: np.lexsort(np.round(a, 12).T)  # noqa: E731
+    np.testing.assert_allclose(got[key(got)], want[key(want)], atol=1e-12)
+
+
+def test_mc_vertices_on_sphere_field_lie_on_the_sphere():
+    """For O = |p| - r the vertices sit on the zero set up to the linear-interpolation error
+    (|O| at a vertex <= h^2 / (2 r) on an edge of length h) and their count grows as N^2."""
+    from oracle import mesh_oracle as mo
+    r = 0.6
+    for N in (17, 33):
+        P = mo.lattice_points(N, (-1, -1, -1), (1, 1, 1))
+        O = np.linalg.norm(P, axis=-1) - r
+        v = mo.mc_vertices(O, (-1, -1, -1), (1, 1, 1))
+        h = 2.0 / (N - 1)
+        assert np.abs(np.linalg.norm(v, axis=1) - r).max() <= h * h / (2 * r) + 1e-12
+        # every lattice line along an axis through the disc of radius r crosses the sphere twice:
+        # 2 pi r^2 / h^2 crossing edges per axis
+        est = 6 * math.pi * r * r / (h * h)
+        assert 0.9 * est < len(v) < 1.1 * est, (len(v), est)

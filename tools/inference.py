@@ -23,6 +23,7 @@ def main():
     p.add_argument("--res", type=int, default=256)
     p.add_argument("--chunk", type=int, default=1 << 22)
     p.add_argument("--fit-steps", type=int, default=300)
+    p.add_argument("--mesh", type=str, default="256,512", help="lattice sizes for efunc_mesh timing ('' = none)")
     a = p.parse_args()
     tor = synth.Torus()
     m = ef.EFunc(32, synth.init_theta(32, 1))
@@ -64,6 +65,29 @@ def main():
     res = {"points": N, "grid": "32^3x13 fitted %d steps" % a.fit_steps, "gpu_ms": gpu_ms, "wall_s": wall,
            "points_per_s": N / (gpu_ms / 1e3), "mean_abs_sdf_err": err, "mean_abs_grad_norm_minus_1": gn,
            "paper": "256^3 in about 5 s (PAPER.md:L853, unknown GPU)"}
+    # NEXT-3: efunc_mesh = lattice O + Marching Cubes + vertex normals
+    # on a grid whose keys carry the torus SDF and its gradient (a "fitted-like" state; the short fit
+    # above is far from converged), so the mesh is the torus and its statistics mean something
+    mf = ef.EFunc(32, synth.fitted_like_theta(32, tor, 1))
+    meshes = []
+    for nres in [int(x) for x in a.mesh.split(",") if x]:
+        mf.mesh(nres)  # warm-up (allocations, table upload)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v, t, nrm, _ = mf.mesh(nres)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        vd = v.double().cpu().numpy()
+        err_v = float(np.abs(tor.sdf(vd)).mean())
+        # normal vs the analytic torus gradient at the vertices
+        gt = tor.grad(vd)
+        cosv = float(np.mean(np.sum(gt * nrm.double().cpu().numpy(), axis=1) / np.linalg.norm(gt, axis=1)))
+        meshes.append({"N": nres, "lattice_points": nres ** 3, "verts": int(v.shape[0]), "tris": int(t.shape[0]),
+                       "wall_s": dt, "mean_abs_sdf_at_verts": err_v, "mean_cos_normal_vs_analytic": cosv,
+                       "theta": "fitted_like_theta(32, torus): c = sdf + N(0, 0.01^2), g = grad sdf + N(0, 0.05^2)", "note": "one synchronous efunc_mesh call: lattice O in z-slabs of 2^23 points (value-only "
+                               "forward), Marching Cubes count/scan/emit, normals from one eval_grad pass"})
+    res["mesh"] = meshes
+    res["paper_mesh"] = "O at 512^3 then Marching Cubes (PAPER.md:L680); normals from one forward pass (L962-971)"
     print(json.dumps(res))
 
 
