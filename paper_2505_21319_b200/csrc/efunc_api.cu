@@ -461,16 +461,6 @@ int fit_pre_off() {
   return off;
 }
 
-// EFUNC_FIT_PIPE=0: k_fit builds each item's candidate list before its forward instead of during
-// the previous item's backward (kept for A/B runs)
-int fit_pipe_on() {
-  static const int on = [] {
-    const char* e = std::getenv("EFUNC_FIT_PIPE");
-    return (e && e[0] == '0') ? 0 : 1;
-  }();
-  return on;
-}
-
 // efunc_forward_backward: the fused fit kernel for the MSE loss (k_fit.cu), the split kernels for
 // its leftover items; forward + backward otherwise.
 efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -503,7 +493,6 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
   f.pre = (!eik && !h->iota && !fit_pre_off()) ? 1 : 0;
-  f.pipe = fit_pipe_on();
   const int slot = timing_begin(h, s);
   if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
   h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);

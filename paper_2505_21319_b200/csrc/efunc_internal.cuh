@@ -170,7 +170,6 @@ struct FitArgs {
   uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
   const uint32_t* iota;   // dense mode (cutoff_T = inf): 0 .. 2R^3-1, every key a candidate; else null
   int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
-  int pipe;               // 1: k_fit builds the next item's candidate ids during this item's backward
   float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
 };
 
