@@ -332,9 +332,20 @@ def run_ours(args, rank, world, local_rank, nccl):
     clk = ClockSampler(uuid)
     clk.start()
     time.sleep(0.3)
-    # soak so the sampler sees the loaded clock, then the timed region
-    t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 0.5:
+    # soak so the sampler sees the loaded clock, then the timed region. The soak length is a step
+    # count every rank agrees on (a step holds an all-reduce when N > 1: ranks must issue the same
+    # number of collectives)
+    torch.cuda.synchronize()
+    ts = time.perf_counter()
+    step(0)
+    step(0)
+    torch.cuda.synchronize()
+    n_soak = int(np.ceil(0.5 / max((time.perf_counter() - ts) / 2, 1e-5)))
+    if world > 1:
+        tn = torch.tensor([n_soak], dtype=torch.int64, device=f"cuda:{dev}")
+        dist.all_reduce(tn, op=dist.ReduceOp.MIN)
+        n_soak = int(tn[0])
+    for _ in range(min(n_soak, 5000)):
         step(0)
     torch.cuda.synchronize()
     launches0 = m.stats()["launches"]

@@ -65,14 +65,30 @@ typedef enum {
   EFUNC_ENOMEM = 5       /* device allocation failed */
 } efunc_status;
 
-typedef enum { EFUNC_VARIANT_COMBINED = 0 } efunc_variant; /* O^{+Delta}, 13 channels */
+/* Model families of Table 3:
+ *   COMBINED  O^{+Delta} (Eq. func-offset): fixed grid keys + learnable
+ *             offset keys k_n + Delta_n, one softmax over both banks (Table 3 Full-3/4);
+ *   GRID      O (Eq. func-interp) over the fixed grid keys (Table 3 G-5..G-8);
+ *   OFFSET    O^Delta (Eq. func-with-offset): learnable keys only (Full-1/2).
+ *             Without fixed keys the per-query exponent minimum has no lattice bound, so this
+ *             variant always evaluates every key (cutoff_T is forced to infinity, reading R-1).
+ * Parameter layout per node (efunc_channels gives the count): COMBINED with degree 0/1 is the
+ * 13-channel layout below; every other (variant, degree) uses, bank by bank (grid first),
+ *   grid bank   [s, c, g(3) if degree >= 1, H(6) if degree == 2]
+ *   offset bank [Delta(3), s, c, g(3) if degree >= 1, H(6) if degree == 2]
+ * with beta = exp(s), f(x) = c + g.x + 1/2 x^T H x, x = q - key (Eq. poly-func),
+ * H symmetric stored as (Hxx, Hyy, Hzz, Hxy, Hxz, Hyz): G-7 = GRID/2 = 11 channels, Full-1 =
+ * OFFSET/1 = 8, G-6 = GRID/1 = 5, COMBINED/2 = 25. */
+typedef enum { EFUNC_VARIANT_COMBINED = 0, EFUNC_VARIANT_GRID = 1, EFUNC_VARIANT_OFFSET = 2 } efunc_variant;
 
 typedef struct {
   int32_t R;              /* lattice resolution per axis, 2 <= R <= 256 */
-  int32_t degree;         /* polynomial degree of f: 1 (f = c + g.(q-k)) or 0 (f = c, Table 3 G-0:
-                             the g channels 2-4, 10-12 are held at 0 and AdamW skips them; their
-                             gradient entries are the degree-1 ones at g = 0 and carry no update) */
-  int32_t variant;        /* EFUNC_VARIANT_COMBINED */
+  int32_t degree;         /* polynomial degree of f: 1 (f = c + g.(q-k)), 2 (+ 1/2 (q-k)^T H (q-k)) or
+                             0 (f = c). COMBINED/0 keeps the 13-channel layout (Table 3 G-0): the g
+                             channels 2-4, 10-12 are held at 0 and AdamW skips them (their gradient
+                             entries are the degree-1 ones at g = 0). Degree 2 supports the MSE loss
+                             (no Eikonal terms) and no deterministic mode. */
+  int32_t variant;        /* efunc_variant */
   float cutoff_T;         /* certified cutoff in nats (20.0f default); <=0 or inf: dense */
   int32_t deterministic;  /* 1: gradients bitwise reproducible run to run (no float atomics) */
   int32_t device;         /* CUDA device ordinal */
@@ -119,7 +135,8 @@ typedef struct {
 /* efunc_create — allocate a handle on cfg->device and upload theta.
  *   theta_host: host float[R^3*13] in the layout above (NULL = all zeros); [n_shapes][R^3*13]
  *               for a batched handle.
- *   Returns EFUNC_EINVAL for R outside [2,256], degree not 0 or 1, variant != COMBINED. */
+ *   Returns EFUNC_EINVAL for R outside [2,256], an unsupported (variant, degree), or degree 2 with
+ *   deterministic mode. theta_host is [R^3][efunc_channels(variant, degree)]. */
 EFUNC_API efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efunc_t** out);
 EFUNC_API efunc_status efunc_destroy(efunc_t* h);
 
@@ -251,6 +268,9 @@ EFUNC_API efunc_status efunc_check(efunc_t* h, void* stream);
 
 EFUNC_API const char* efunc_last_error(const efunc_t* h); /* never NULL; h may be NULL */
 EFUNC_API int32_t efunc_abi_version(void);
+/* efunc_channels — parameter channels per node of a (variant, degree) (Table 3 "Ch"), or -1 if
+ * the pair is not supported. Every theta/grad/m/v array of a handle is [R^3][channels]. */
+EFUNC_API int32_t efunc_channels(int32_t variant, int32_t degree);
 
 #ifdef __cplusplus
 }

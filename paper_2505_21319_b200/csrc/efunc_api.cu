@@ -151,7 +151,44 @@ int bits_for(size_t nvals) {  // bits of the largest value nvals - 1
 // regardless of the Verlet skin.
 // degree 0 (Table 3 G-0: f = c): the g channels of both banks held at 0
 uint32_t g_channels(const efunc_t* h) {
-  return h->cfg.degree == 0 ? ((7u << 2) | (7u << 10)) : 0u;
+  return (!h->vmode && h->cfg.degree == 0) ? ((7u << 2) | (7u << 10)) : 0u;
+}
+
+// Variants (NEXT-4): the internal 13-channel theta (+ the degree-2 squares and their per-key
+// records) derived from the user's parameters; call before rebuild_keys
+void sync_internal_theta(efunc_t* h, cudaStream_t s) {
+  if (!h->vmode) return;
+  h->launches += launch_var_unpack(h->theta_v, h->n_nodes, h->vlay, h->theta, h->thetaH, s);
+  if (h->keyH) h->launches += launch_var_keyH(h->thetaH, h->n_nodes, h->keyH, s);
+}
+
+// channels of the user's parameter layout for a (variant, degree), or -1 (include/efunc.h)
+int variant_channels(int variant, int degree, ef::VarLayout* L) {
+  if (degree < 0 || degree > 2 || variant < 0 || variant > 2) return -1;
+  const int coef = degree == 0 ? 1 : (degree == 1 ? 4 : 10);
+  ef::VarLayout v{};
+  v.deg = degree;
+  v.grid = v.off = v.delta = -1;
+  if (variant == EFUNC_VARIANT_COMBINED && degree <= 1) {  // the 13-channel layout (Table 3 Full-4)
+    v.nch = EF_NCH;
+    v.grid = 0;
+    v.delta = 5;
+    v.off = 8;
+  } else {
+    int o = 0;
+    if (variant != EFUNC_VARIANT_OFFSET) {
+      v.grid = o;
+      o += 1 + coef;
+    }
+    if (variant != EFUNC_VARIANT_GRID) {
+      v.delta = o;
+      v.off = o + 3;
+      o += 4 + coef;
+    }
+    v.nch = o;
+  }
+  if (L) *L = v;
+  return v.nch;
 }
 
 efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
@@ -162,7 +199,7 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->keys_resort, force ? 1 : 0, sizeof(uint32_t), s));
   const float skin = SKIN_H * h->h;
-  h->launches += launch_prep_keys(h->theta, h->R, h->key_raw, h->key_cell, h->cell_count, h->key_ref,
+  h->launches += launch_prep_keys(h->theta, h->R, h->banks, h->key_raw, h->key_cell, h->cell_count, h->key_ref,
                                   skin * skin, SKIN_MU, h->ds, s);
   // the cell sort only when some offset key changed cell (k_prep_keys sets keys_resort)
   const uint32_t* gate = &h->ds->keys_resort;
@@ -257,6 +294,7 @@ void free_timing(efunc_t* h) {
 
 void free_all(efunc_t* h) {
   dfree(h->theta); dfree(h->m); dfree(h->v);
+  dfree(h->theta_v); dfree(h->m_v); dfree(h->v_v); dfree(h->thetaH); dfree(h->keyH); dfree(h->gint); dfree(h->gH);
   dfree(h->key_raw); dfree(h->key_sorted); dfree(h->kid); dfree(h->key_cell);
   dfree(h->cell_count); dfree(h->cell_start); dfree(h->cell_fill); dfree(h->key_tmp); dfree(h->key_order);
   dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad); dfree(h->rk); dfree(h->rh);
@@ -369,13 +407,20 @@ efunc_status do_forward(efunc_t* h, const float* q, const float* o, int64_t J, c
     return EFUNC_OK;
   }
   const float* o_used = (kind != EFUNC_LOSS_NONE) ? o : nullptr;
+  if (h->vk && kind == EFUNC_LOSS_MSE_EIKONAL)
+    return fail(h, EFUNC_EINVAL, "degree 2 / O^Delta only: the Eikonal loss is not supported (MSE or no loss)");
   FwdArgs a;
   RET(prep_queries(h, q, o_used, J, loss, a, s));
   const int64_t items = h->fwd_items_bound;
   const uint32_t* n_items = a.n_items;
   a.O = O;
   a.G = G;
-  h->launches += launch_forward(a, want_g, items, s);
+  if (h->vk) {  // NEXT-4 (k_var.cu): certified item lists (or every key), exact shift, O (+G)
+    if (!std::isinf(a.T_l)) h->launches += launch_item_lists(a, items, s);
+    h->launches += launch_var_forward(a, h->keyH, h->iota, h->iota_n, G != nullptr, items, s);
+  } else {
+    h->launches += launch_forward(a, want_g, items, s);
+  }
   if (kind != EFUNC_LOSS_NONE && loss_out) h->launches += launch_sum_partials(h->loss_part, n_items, 1, loss_out, s);
   else if (loss_out) CK(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   CK(cudaGetLastError());
@@ -451,6 +496,79 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
   return EFUNC_OK;
 }
 
+// the FwdArgs of the last forward (its sorted queries, items, records and candidate lists)
+FwdArgs saved_fwd_args(efunc_t* h) {
+  FwdArgs a{};
+  a.kv = keys_view(h);
+  a.qs = h->qs;
+  a.perm = h->perm;
+  a.J = h->fwd_J;
+  a.items = h->items;
+  a.n_items = h->item_off + (h->bg.n_codes + 1);
+  a.T_l = cutoff_log2(h->cfg);
+  a.rec = h->rec;
+  a.wl_pool = h->wl_pool;
+  a.wl_cap = h->wl_cap;
+  a.wl_off = h->wl_off;
+  a.wl_n = h->wl_n;
+  a.ds = h->ds;
+  return a;
+}
+
+// degree-2 backward (k_var.cu) into the internal gradient scratch (g13 += ..., gH += ...)
+efunc_status do_backward_var2(efunc_t* h, const float* dL_dO, const float* dL_dG, float* g13, float* gH,
+                              cudaStream_t s) {
+  if (!h->have_fwd) return fail(h, EFUNC_ESTATE, "backward without a valid forward (saved e_j missing)");
+  if (dL_dG) return fail(h, EFUNC_EINVAL, "degree 2: dL_dG (Eikonal terms) is not supported");
+  if (h->fwd_J == 0) return EFUNC_OK;
+  if (!dL_dO && h->fwd_loss_kind == EFUNC_LOSS_NONE)
+    return fail(h, EFUNC_EINVAL, "dL_dO is NULL and the forward had no fused loss");
+  const FwdArgs a = saved_fwd_args(h);
+  const int slot = timing_begin(h, s);
+  h->launches += launch_var_backward(a, h->keyH, h->iota, h->iota_n, dL_dO, g13, gH, h->fwd_items_bound, s);
+  timing_end(h, slot, s);
+  CK(cudaGetLastError());
+  return EFUNC_OK;
+}
+
+efunc_status zero_internal_grad(efunc_t* h, cudaStream_t s) {
+  CK(cudaMemsetAsync(h->gint, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, s));
+  if (h->gH) CK(cudaMemsetAsync(h->gH, 0, sizeof(float) * (size_t)h->n_nodes * 12, s));
+  return EFUNC_OK;
+}
+
+// backward in the user's layout (grad += dL/dtheta)
+efunc_status any_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad, cudaStream_t s) {
+  if (!h->vmode) return do_backward(h, dL_dO, dL_dG, grad, s);
+  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
+  RET(zero_internal_grad(h, s));
+  if (h->vk) RET(do_backward_var2(h, dL_dO, dL_dG, h->gint, h->gH, s));
+  else RET(do_backward(h, dL_dO, dL_dG, h->gint, s));
+  h->launches += launch_var_pack_grad(h->gint, h->gH, h->n_nodes, h->vlay, grad, s);
+  return EFUNC_OK;
+}
+
+efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                                 float* O, float* grad, float* loss_out, cudaStream_t s);
+
+efunc_status any_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
+                                  float* O, float* grad, float* loss_out, cudaStream_t s) {
+  if (!h->vmode) return do_forward_backward(h, q, o, J, loss, O, grad, loss_out, s);
+  if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
+  if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "forward_backward needs a loss");
+  RET(zero_internal_grad(h, s));
+  if (h->vk) {
+    RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
+    const efunc_status st = do_backward_var2(h, nullptr, nullptr, h->gint, h->gH, s);
+    h->have_fwd = 0;  // like the fused call: no saved state afterwards
+    RET(st);
+  } else {
+    RET(do_forward_backward(h, q, o, J, loss, O, h->gint, loss_out, s));
+  }
+  h->launches += launch_var_pack_grad(h->gint, h->gH, h->n_nodes, h->vlay, grad, s);
+  return EFUNC_OK;
+}
+
 // EFUNC_FIT_PRE=1: the items' candidate lists are built by k_fit_lists before k_fit (measured
 // slower than k_fit building them itself; kept for A/B runs)
 int fit_pre_off() {
@@ -468,7 +586,8 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   if (!grad) return fail(h, EFUNC_EINVAL, "grad is NULL");
   if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "forward_backward needs a loss");
   const int eik = loss->kind == EFUNC_LOSS_MSE_EIKONAL;
-  const int fused = !h->cfg.deterministic && !h->count_kept && !(eik && h->iota);  // (dense Eikonal: split)
+  const bool dense = std::isinf(cutoff_log2(h->cfg));
+  const int fused = !h->cfg.deterministic && !h->count_kept && !(eik && dense);  // (dense Eikonal: split)
   if (!fused || J == 0) {
     RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
     RET(do_backward(h, nullptr, nullptr, grad, s));
@@ -488,11 +607,12 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.f = a;
   f.gpad = h->gpad;
   f.scratch = h->scratch;
-  f.iota = h->iota;
+  f.iota = dense ? h->iota : nullptr;
+  f.iota_n = h->iota_n;
   f.item_o = h->item_o;
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
-  f.pre = (!eik && !h->iota && !fit_pre_off()) ? 1 : 0;
+  f.pre = (!eik && !dense && !fit_pre_off()) ? 1 : 0;
   const int slot = timing_begin(h, s);
   if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
   h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
@@ -530,7 +650,13 @@ efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cuda
   hc.weight_decay = hp->weight_decay;
   hc.decay_mask = hp->decay_mask;
   hc.frozen_mask = g_channels(h);
-  h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
+  hc.nch = h->pnch;
+  if (h->vmode) {  // NEXT-4: the update runs on the user's layout, then the internal theta follows
+    h->launches += launch_adamw(h->theta_v, grad, h->m_v, h->v_v, (int64_t)h->n_nodes * h->pnch, hc, h->ds, s);
+    sync_internal_theta(h, s);
+  } else {
+    h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
+  }
   CK(cudaGetLastError());
   return rebuild_keys(h, s);
 }
@@ -542,8 +668,8 @@ efunc_status fit_device_step(efunc_t* h, int slot, const float* qd, const float*
                              cudaStream_t s) {
   float* g = grad_ws ? grad_ws : h->fit_grad;
   auto device_work = [&](cudaStream_t st) -> efunc_status {
-    CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * EF_NCH, st));
-    RET(do_forward_backward(h, qd, od, J, loss, nullptr, g, lossd, st));
+    CK(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)h->n_nodes * h->pnch, st));
+    RET(any_forward_backward(h, qd, od, J, loss, nullptr, g, lossd, st));
     return do_adamw(h, g, hp, st);
   };
   efunc_t::FitKey key{};
@@ -684,6 +810,8 @@ extern "C" {
 
 int32_t efunc_abi_version(void) { return EFUNC_ABI_VERSION; }
 
+int32_t efunc_channels(int32_t variant, int32_t degree) { return variant_channels(variant, degree, nullptr); }
+
 const char* efunc_last_error(const efunc_t* h) {
   if (h && !h->err.empty()) return h->err.c_str();
   return g_err.c_str();
@@ -695,17 +823,23 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
   *out = nullptr;
   if (cfg->R < 2 || cfg->R > 256) return fail(nullptr, EFUNC_EINVAL, "R must be in [2, 256]");
   if (cfg->n_shapes < 0 || cfg->n_shapes > 4096) return fail(nullptr, EFUNC_EINVAL, "n_shapes must be in [0, 4096]");
+  ef::VarLayout vlay{};
+  const int pnch = variant_channels(cfg->variant, cfg->degree, &vlay);
+  if (pnch < 0) return fail(nullptr, EFUNC_EINVAL, "variant must be COMBINED, GRID or OFFSET and degree 0, 1 or 2");
+  if ((cfg->degree == 2 || cfg->variant == EFUNC_VARIANT_OFFSET) && cfg->deterministic)
+    return fail(nullptr, EFUNC_EINVAL, "degree 2 and O^Delta-only have no deterministic mode");
   if (cfg->n_shapes > 1) {  // C5: one single-shape handle per shape behind this one
     efunc_t* p = new (std::nothrow) efunc();
     if (!p) return fail(nullptr, EFUNC_ENOMEM, "host allocation failed");
     p->cfg = *cfg;
     p->R = cfg->R;
     p->n_nodes = cfg->R * cfg->R * cfg->R;
+    p->pnch = pnch;
     efunc_config c1 = *cfg;
     c1.n_shapes = 1;
     for (int k = 0; k < cfg->n_shapes; ++k) {
       efunc_t* kid = nullptr;
-      const efunc_status st = efunc_create(&c1, off(theta_host, p->n_nodes * (int64_t)EF_NCH, k), &kid);
+      const efunc_status st = efunc_create(&c1, off(theta_host, p->n_nodes * (int64_t)p->pnch, k), &kid);
       if (st != EFUNC_OK) {
         for (efunc_t* q : p->kids) efunc_destroy(q);
         delete p;
@@ -716,14 +850,21 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     *out = p;
     return EFUNC_OK;
   }
-  if (cfg->degree != 0 && cfg->degree != 1) return fail(nullptr, EFUNC_EINVAL, "degree must be 0 or 1");
-  if (cfg->variant != EFUNC_VARIANT_COMBINED) return fail(nullptr, EFUNC_EINVAL, "only the COMBINED variant");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(nullptr, EFUNC_ECUDA, "no CUDA device");
   if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, EFUNC_EINVAL, "bad device ordinal");
   h = new (std::nothrow) efunc();
   if (!h) return fail(nullptr, EFUNC_ENOMEM, "host allocation failed");
   h->cfg = *cfg;
+  // NEXT-4 variants: O^Delta alone has no fixed grid keys bounding each query's exponent minimum
+  // (reading R-1), so it evaluates every key (dense, cutoff_T = inf)
+  if (cfg->variant == EFUNC_VARIANT_OFFSET) h->cfg.cutoff_T = INFINITY;
+  h->vlay = vlay;
+  h->pnch = pnch;
+  h->vmode = !(cfg->variant == EFUNC_VARIANT_COMBINED && cfg->degree <= 1);
+  // degree 2 and O^Delta alone run the generic kernels of k_var.cu (exact per-query shift)
+  h->vk = cfg->degree == 2 || cfg->variant == EFUNC_VARIANT_OFFSET;
+  h->banks = cfg->variant == EFUNC_VARIANT_GRID ? 1 : (cfg->variant == EFUNC_VARIANT_OFFSET ? 2 : 3);
   DeviceGuard dg(cfg->device);
   h->R = cfg->R;
   h->n_nodes = h->R * h->R * h->R;
@@ -737,7 +878,21 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->theta, np));
     CK(dalloc(&h->m, np));
     CK(dalloc(&h->v, np));
-    CK(dalloc(&h->fit_grad, np));
+    CK(dalloc(&h->fit_grad, (size_t)h->n_nodes * std::max(h->pnch, EF_NCH)));
+    if (h->vmode) {
+      const size_t nv = (size_t)h->n_nodes * h->pnch;
+      CK(dalloc(&h->theta_v, nv));
+      CK(dalloc(&h->m_v, nv));
+      CK(dalloc(&h->v_v, nv));
+      CK(cudaMemset(h->m_v, 0, nv * sizeof(float)));
+      CK(cudaMemset(h->v_v, 0, nv * sizeof(float)));
+      CK(dalloc(&h->gint, np));
+      if (h->vk) {
+        CK(dalloc(&h->thetaH, (size_t)h->n_nodes * 12));
+        CK(dalloc(&h->gH, (size_t)h->n_nodes * 12));
+        CK(dalloc(&h->keyH, 2 * (size_t)h->n_keys));
+      }
+    }
     CK(dalloc(&h->key_raw, 2 * (size_t)h->n_keys));
     CK(dalloc(&h->key_sorted, 2 * (size_t)h->n_keys));
     CK(dalloc(&h->kid, h->n_keys));
@@ -749,9 +904,13 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->cell_fill, h->n_cells + 1));
     CK(dalloc(&h->ds, 1));
     CK(dalloc(&h->scratch, (size_t)SCRATCH_WARPS * SCRATCH_STRIDE));
-    if (std::isinf(cutoff_log2(h->cfg))) {  // dense mode: the fused kernel's all-keys list
-      std::vector<uint32_t> ids((size_t)h->n_keys);
-      for (size_t i = 0; i < ids.size(); ++i) ids[i] = (uint32_t)i;
+    if (std::isinf(cutoff_log2(h->cfg)) || h->vk) {
+      // every enabled key id: the dense fused kernel's candidate list; degree 2's list for items
+      // without a certified one
+      std::vector<uint32_t> ids;
+      for (int i = 0; i < h->n_keys; ++i)
+        if ((h->banks >> (i < h->n_nodes ? 0 : 1)) & 1) ids.push_back((uint32_t)i);
+      h->iota_n = (uint32_t)ids.size();
       CK(dalloc(&h->iota, ids.size()));
       CK(cudaMemcpy(h->iota, ids.data(), ids.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
@@ -777,8 +936,12 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(cudaMemset(h->ds, 0, sizeof(DevScalars)));
     RET(ensure_scan_tmp(h, h->n_cells + 1));
     RET(ensure_radix(h, (size_t)h->n_keys));
-    if (theta_host) CK(cudaMemcpy(h->theta, theta_host, np * sizeof(float), cudaMemcpyHostToDevice));
-    else CK(cudaMemset(h->theta, 0, np * sizeof(float)));
+    float* pdst = h->vmode ? h->theta_v : h->theta;
+    const size_t pn = (size_t)h->n_nodes * h->pnch;
+    if (theta_host) CK(cudaMemcpy(pdst, theta_host, pn * sizeof(float), cudaMemcpyHostToDevice));
+    else CK(cudaMemset(pdst, 0, pn * sizeof(float)));
+    if (h->vmode) CK(cudaMemset(h->theta, 0, np * sizeof(float)));
+    sync_internal_theta(h, 0);
     CK(cudaMemset(h->m, 0, np * sizeof(float)));
     CK(cudaMemset(h->v, 0, np * sizeof(float)));
     CK(dalloc(&h->key_ref, h->n_keys));
@@ -835,13 +998,13 @@ efunc_status efunc_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, 
     for (size_t k = 0; k < h->kids.size(); ++k) {
       const int64_t J = h->kids[k]->fwd_J;
       RET(kid_ok(h, k, efunc_backward(h->kids[k], off(dL_dO, J, k), off(dL_dG, 3 * J, k),
-                                      off(grad, h->kids[k]->n_nodes * (int64_t)EF_NCH, k), stream)));
+                                      off(grad, h->kids[k]->n_nodes * (int64_t)h->pnch, k), stream)));
     }
     return EFUNC_OK;
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
-  return do_backward(h, dL_dO, dL_dG, grad, (cudaStream_t)stream);
+  return any_backward(h, dL_dO, dL_dG, grad, (cudaStream_t)stream);
 }
 
 efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -851,13 +1014,13 @@ efunc_status efunc_forward_backward(efunc_t* h, const float* q, const float* o, 
     RET(kids_fork(h, (cudaStream_t)stream));
     for (size_t k = 0; k < h->kids.size(); ++k)
       RET(kid_ok(h, k, efunc_forward_backward(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, off(O, J, k),
-                                              off(grad, h->n_nodes * (int64_t)EF_NCH, k), off(loss_out, 1, k),
+                                              off(grad, h->n_nodes * (int64_t)h->pnch, k), off(loss_out, 1, k),
                                               h->kid_streams[k])));
     return kids_join(h, (cudaStream_t)stream);
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
-  return do_forward_backward(h, q, o, J, loss, O, grad, loss_out, (cudaStream_t)stream);
+  return any_forward_backward(h, q, o, J, loss, O, grad, loss_out, (cudaStream_t)stream);
 }
 
 efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* hp, void* stream) {
@@ -865,7 +1028,7 @@ efunc_status efunc_adamw_step(efunc_t* h, const float* grad, const efunc_adamw* 
     DeviceGuard dg(h->cfg.device);
     RET(kids_fork(h, (cudaStream_t)stream));
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_adamw_step(h->kids[k], off(grad, h->n_nodes * (int64_t)EF_NCH, k), hp,
+      RET(kid_ok(h, k, efunc_adamw_step(h->kids[k], off(grad, h->n_nodes * (int64_t)h->pnch, k), hp,
                                         h->kid_streams[k])));
     return kids_join(h, (cudaStream_t)stream);
   }
@@ -984,7 +1147,7 @@ efunc_status efunc_fit_step(efunc_t* h, const float* q, const float* o, int64_t 
   if (h && !h->kids.empty()) {
     for (size_t k = 0; k < h->kids.size(); ++k)
       RET(kid_ok(h, k, efunc_fit_step(h->kids[k], off(q, 3 * J, k), off(o, J, k), J, loss, hp,
-                                      off(grad_ws, h->n_nodes * (int64_t)EF_NCH, k), off(loss_out, 1, k), host_io,
+                                      off(grad_ws, h->n_nodes * (int64_t)h->pnch, k), off(loss_out, 1, k), host_io,
                                       stream)));
     return EFUNC_OK;
   }
@@ -1050,7 +1213,12 @@ efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, flo
   if (!(bandwidth > 0.0f)) return fail(h, EFUNC_EINVAL, "bandwidth must be > 0");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (!(h->banks & 2)) return fail(h, EFUNC_EINVAL, "mean shift initialises the offset bank; this variant has none");
   h->launches += launch_mean_shift(h->theta, h->R, surf, N, bandwidth, s);
+  if (h->vmode) {  // the offsets into the user's layout, then the internal theta from it
+    h->launches += launch_var_delta_out(h->theta, h->n_nodes, h->vlay, h->theta_v, s);
+    sync_internal_theta(h, s);
+  }
   CK(cudaGetLastError());
   return rebuild_keys(h, s, 1);
 }
@@ -1058,14 +1226,15 @@ efunc_status efunc_mean_shift_init(efunc_t* h, const float* surf, int64_t N, flo
 efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream) {
   if (h && !h->kids.empty() && dst) {
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_get_params(h->kids[k], off(dst, h->n_nodes * (int64_t)EF_NCH, k), on_device, stream)));
+      RET(kid_ok(h, k, efunc_get_params(h->kids[k], off(dst, h->n_nodes * (int64_t)h->pnch, k), on_device, stream)));
     return EFUNC_OK;
   }
   if (!h || !dst) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
-  CK(cudaMemcpyAsync(dst, h->theta, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * h->pnch;
+  CK(cudaMemcpyAsync(dst, h->vmode ? h->theta_v : h->theta, bytes,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return EFUNC_OK;
 }
@@ -1073,14 +1242,16 @@ efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* s
 efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, void* stream) {
   if (h && !h->kids.empty() && src) {
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_set_params(h->kids[k], off(src, h->n_nodes * (int64_t)EF_NCH, k), on_device, stream)));
+      RET(kid_ok(h, k, efunc_set_params(h->kids[k], off(src, h->n_nodes * (int64_t)h->pnch, k), on_device, stream)));
     return EFUNC_OK;
   }
   if (!h || !src) return fail(h, EFUNC_EINVAL, "NULL argument");
   DeviceGuard dg(h->cfg.device);
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
-  CK(cudaMemcpyAsync(h->theta, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * h->pnch;
+  CK(cudaMemcpyAsync(h->vmode ? h->theta_v : h->theta, src, bytes,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  sync_internal_theta(h, s);
   RET(rebuild_keys(h, s, 1));
   CK(cudaStreamSynchronize(s));
   return EFUNC_OK;
@@ -1089,16 +1260,16 @@ efunc_status efunc_set_params(efunc_t* h, const float* src, int32_t on_device, v
 efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int64_t* step) {
   if (h && !h->kids.empty()) {
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_get_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)EF_NCH, k),
-                                            off(v_host, h->n_nodes * (int64_t)EF_NCH, k), k == 0 ? step : nullptr)));
+      RET(kid_ok(h, k, efunc_get_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)h->pnch, k),
+                                            off(v_host, h->n_nodes * (int64_t)h->pnch, k), k == 0 ? step : nullptr)));
     return EFUNC_OK;
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   DeviceGuard dg(h->cfg.device);
-  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * h->pnch;
   CK(cudaDeviceSynchronize());
-  if (m_host) CK(cudaMemcpy(m_host, h->m, bytes, cudaMemcpyDeviceToHost));
-  if (v_host) CK(cudaMemcpy(v_host, h->v, bytes, cudaMemcpyDeviceToHost));
+  if (m_host) CK(cudaMemcpy(m_host, h->vmode ? h->m_v : h->m, bytes, cudaMemcpyDeviceToHost));
+  if (v_host) CK(cudaMemcpy(v_host, h->vmode ? h->v_v : h->v, bytes, cudaMemcpyDeviceToHost));
   if (step) {
     unsigned long long t = 0;
     CK(cudaMemcpy(&t, &h->ds->adam_t, sizeof(t), cudaMemcpyDeviceToHost));
@@ -1110,19 +1281,21 @@ efunc_status efunc_get_adam_state(efunc_t* h, float* m_host, float* v_host, int6
 efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, const float* v_host, int64_t step) {
   if (h && !h->kids.empty()) {
     for (size_t k = 0; k < h->kids.size(); ++k)
-      RET(kid_ok(h, k, efunc_set_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)EF_NCH, k),
-                                            off(v_host, h->n_nodes * (int64_t)EF_NCH, k), step)));
+      RET(kid_ok(h, k, efunc_set_adam_state(h->kids[k], off(m_host, h->n_nodes * (int64_t)h->pnch, k),
+                                            off(v_host, h->n_nodes * (int64_t)h->pnch, k), step)));
     return EFUNC_OK;
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   if (step < 0) return fail(h, EFUNC_EINVAL, "step < 0");
   DeviceGuard dg(h->cfg.device);
-  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * EF_NCH;
+  const size_t bytes = sizeof(float) * (size_t)h->n_nodes * h->pnch;
+  float* mm = h->vmode ? h->m_v : h->m;
+  float* vv = h->vmode ? h->v_v : h->v;
   CK(cudaDeviceSynchronize());
-  if (m_host) CK(cudaMemcpy(h->m, m_host, bytes, cudaMemcpyHostToDevice));
-  else CK(cudaMemset(h->m, 0, bytes));
-  if (v_host) CK(cudaMemcpy(h->v, v_host, bytes, cudaMemcpyHostToDevice));
-  else CK(cudaMemset(h->v, 0, bytes));
+  if (m_host) CK(cudaMemcpy(mm, m_host, bytes, cudaMemcpyHostToDevice));
+  else CK(cudaMemset(mm, 0, bytes));
+  if (v_host) CK(cudaMemcpy(vv, v_host, bytes, cudaMemcpyHostToDevice));
+  else CK(cudaMemset(vv, 0, bytes));
   const unsigned long long t = (unsigned long long)step;
   CK(cudaMemcpy(&h->ds->adam_t, &t, sizeof(t), cudaMemcpyHostToDevice));
   return EFUNC_OK;

@@ -168,7 +168,8 @@ struct FitArgs {
   FwdArgs f;
   float* gpad;            // [R^3][16] padded gradient accumulator
   uint32_t* scratch;      // per-warp candidate-id scratch: SCRATCH_WARPS slots of SCRATCH_STRIDE ids
-  const uint32_t* iota;   // dense mode (cutoff_T = inf): 0 .. 2R^3-1, every key a candidate; else null
+  const uint32_t* iota;   // dense mode (cutoff_T = inf): the enabled key ids, every key a candidate; else null
+  uint32_t iota_n;        // their count (2R^3 with both banks)
   int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
   float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
 };
@@ -184,8 +185,19 @@ struct BrickGeom {
   uint32_t qsub;  // query sub-bins per brick = (2B)^3, Morton ordered inside the brick
 };
 
+// Parameter layout of a Table 3 variant (k_var.cu; include/efunc.h efunc_channels): channel
+// offsets of the grid bank's s, the offset bank's s and Delta (-1: the bank is absent), the
+// polynomial degree, channels per node.
+struct VarLayout {
+  int nch;
+  int grid;   // [s, c, g(3) if deg >= 1, H(6) if deg >= 2] or -1
+  int off;    // same for the offset bank, or -1
+  int delta;  // offset bank's Delta(3), or -1
+  int deg;
+};
+
 // ---------------------------------------------------------------- launchers (host)
-int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s);
 int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, DevScalars* ds,
                          cudaStream_t s);
@@ -225,6 +237,7 @@ struct AdamWConst {  // the efunc_adamw hyper-parameters (doubles, like torch's 
   double lr, beta1, beta2, eps, weight_decay;
   uint32_t decay_mask;
   uint32_t frozen_mask;  // channels AdamW leaves untouched (degree 0: the g channels, held at 0)
+  int nch;               // channels per node of the parameter array (13, or the variant's)
 };
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,
                  DevScalars* ds, cudaStream_t s);
@@ -232,6 +245,16 @@ int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float b
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
 int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s);
+// NEXT-4 (k_var.cu): variant layouts and the degree-2 forward / backward
+int launch_var_unpack(const float* tv, int n, const VarLayout& L, float* t13, float* tH, cudaStream_t s);
+int launch_var_pack_grad(const float* g13, const float* gH, int n, const VarLayout& L, float* gv, cudaStream_t s);
+int launch_var_delta_out(const float* t13, int n, const VarLayout& L, float* tv, cudaStream_t s);
+int launch_var_keyH(const float* tH, int n, float4* keyH, cudaStream_t s);
+int launch_var_forward(const FwdArgs& a, const float4* keyH, const uint32_t* iota, uint32_t iota_n, int want_g,
+                       int64_t n_items, cudaStream_t s);
+int launch_var_backward(const FwdArgs& a, const float4* keyH, const uint32_t* iota, uint32_t iota_n,
+                        const float* dL_dO, float* g13, float* gH, int64_t n_items, cudaStream_t s);
+int launch_item_lists(const FwdArgs& a, int64_t n_items, cudaStream_t s);
 // NEXT-3 (k_mesh.cu): lattice queries, Marching Cubes, vertex normals
 cudaError_t mc_upload_table();
 int launch_lattice_q(int N, const float* lo, const float* step, int k0, int nk, float* q, cudaStream_t s);
@@ -252,6 +275,21 @@ struct efunc {
   float* theta = nullptr;
   float* m = nullptr;
   float* v = nullptr;
+  // Table 3 variants other than the 13-channel default (NEXT-4): parameters and AdamW moments in
+  // the user's layout; theta above (+ thetaH) is derived from them before every key rebuild
+  int vmode = 0;                    // 1: the user layout differs from the internal 13 channels
+  int vk = 0;                       // 1: degree 2 or O^Delta only: forward/backward in k_var.cu
+  int banks = 3;                    // 1 grid, 2 offset, 3 both
+  int pnch = EF_NCH;                // channels per node of the user's parameter arrays
+  ef::VarLayout vlay{};
+  float* theta_v = nullptr;
+  float* m_v = nullptr;
+  float* v_v = nullptr;
+  float* thetaH = nullptr;          // [R^3][12] degree-2 squares (grid, offset)
+  float4* keyH = nullptr;           // [2R^3][2] per key id
+  float* gint = nullptr;            // [R^3][13] internal gradient scratch (vmode)
+  float* gH = nullptr;              // [R^3][12] degree-2 gradient scratch
+  uint32_t iota_n = 0;
   // keys
   float4* key_raw = nullptr;
   float4* key_sorted = nullptr;

@@ -31,7 +31,7 @@ __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ gra
   const float decay = c[0], omb1 = c[1], b2 = c[2], omb2 = c[3], eps = c[4], step_size = c[5], sqrt_bc2 = c[6];
   const uint32_t mask = hc.decay_mask;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ch = (int)(i % EF_NCH);
+    const int ch = (int)(i % hc.nch);
     if ((hc.frozen_mask >> ch) & 1u) continue;  // degree 0: g channels stay exactly 0
     float p = theta[i];
     const float g = grad[i];

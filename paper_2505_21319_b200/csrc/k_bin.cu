@@ -18,7 +18,7 @@ __device__ __forceinline__ int cell_clamp(float p, float inv_h, int NC) {
 // ------------------------------------------------------------------------------ S0
 // Also checks the brick lists' Verlet skin: a key that moved more than skin from its position at
 // the last list build, or whose bl left [ref/(1+mu), ref*(1+mu)], invalidates the lists.
-__global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __restrict__ key_raw,
+__global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, float4* __restrict__ key_raw,
                             uint32_t* __restrict__ key_cell, uint32_t* __restrict__ cell_count,
                             const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
   const int N = R * R * R;
@@ -35,26 +35,36 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
     const float* t = theta + (size_t)n * EF_NCH;
     const float bl0 = expf(t[0]) * EF_LOG2E;
     const float bl1 = expf(t[8]) * EF_LOG2E;
-    const float px = kx + t[5], py = ky + t[6], pz = kz + t[7];
-    key_raw[2 * n] = make_float4(kx, ky, kz, bl0);
+    const bool on0 = banks & 1, on1 = banks & 2;
+    // a bank the variant does not have (NEXT-4: O only / O^Delta only): its keys sit far away
+    // (weight exactly 0) in the sentinel cell n_cells that no enumeration visits
+    constexpr float FAR = 1e15f;
+    const float px = on1 ? kx + t[5] : FAR, py = on1 ? ky + t[6] : FAR, pz = on1 ? kz + t[7] : FAR;
+    const float gx = on0 ? kx : FAR, gy = on0 ? ky : FAR, gz = on0 ? kz : FAR;
+    key_raw[2 * n] = make_float4(gx, gy, gz, bl0);
     key_raw[2 * n + 1] = make_float4(t[1], t[2], t[3], t[4]);
     key_raw[2 * (N + n)] = make_float4(px, py, pz, bl1);
     key_raw[2 * (N + n) + 1] = make_float4(t[9], t[10], t[11], t[12]);
-    const uint32_t c0 = (uint32_t)((cell_clamp(kz, inv_h, NC) * NC + cell_clamp(ky, inv_h, NC)) * NC +
-                                   cell_clamp(kx, inv_h, NC));
-    const uint32_t c1 = (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
-                                   cell_clamp(px, inv_h, NC));
+    const uint32_t nc3 = (uint32_t)(NC * NC * NC);
+    const uint32_t c0 = on0 ? (uint32_t)((cell_clamp(kz, inv_h, NC) * NC + cell_clamp(ky, inv_h, NC)) * NC +
+                                         cell_clamp(kx, inv_h, NC))
+                            : nc3;
+    const uint32_t c1 = on1 ? (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
+                                         cell_clamp(px, inv_h, NC))
+                            : nc3;
     resort |= key_cell[N + n] != c1;  // grid-bank cells never change
     key_cell[n] = c0;
     key_cell[N + n] = c1;
     atomicAdd(&cell_count[c0], 1u);
     atomicAdd(&cell_count[c1], 1u);
-    local_min = fminf(local_min, fminf(bl0, bl1));
+    local_min = fminf(local_min, fminf(on0 ? bl0 : INFINITY, on1 ? bl1 : INFINITY));
     const float4 r0 = key_ref[n], r1 = key_ref[N + n];
     const float ex = px - r1.x, ey = py - r1.y, ez = pz - r1.z;
-    moved |= fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > skin2;
-    moved |= !(bl0 <= r0.w * (1.0f + mu) && bl0 * (1.0f + mu) >= r0.w);
-    moved |= !(bl1 <= r1.w * (1.0f + mu) && bl1 * (1.0f + mu) >= r1.w);
+    if (on1) {
+      moved |= fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > skin2;
+      moved |= !(bl1 <= r1.w * (1.0f + mu) && bl1 * (1.0f + mu) >= r1.w);
+    }
+    if (on0) moved |= !(bl0 <= r0.w * (1.0f + mu) && bl0 * (1.0f + mu) >= r0.w);
   }
   // bl > 0: the IEEE bit pattern orders like the value
   for (int o = 16; o > 0; o >>= 1) local_min = fminf(local_min, __shfl_xor_sync(~0u, local_min, o));
@@ -64,12 +74,12 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, float4* __re
   if (__any_sync(~0u, resort) && (threadIdx.x & 31) == 0) atomicOr(&ds->keys_resort, 1u);
 }
 
-int launch_prep_keys(const float* theta, int R, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s) {
   const int N = R * R * R;
   int blocks = (N + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, key_raw, key_cell, cell_count, key_ref, skin2, mu, ds);
+  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, banks, key_raw, key_cell, cell_count, key_ref, skin2, mu, ds);
   return 1;
 }
 

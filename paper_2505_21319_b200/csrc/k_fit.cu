@@ -371,9 +371,9 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
   const uint32_t* L = Lw;  // the candidate ids the passes read
   // builds chunk c of the candidate ids into Lw (or points L at them); returns its length
   auto build = [&](const uint32_t c) -> uint32_t {
-    if (dense) {  // all 2R^3 keys in id order (coalesced record loads)
+    if (dense) {  // every enabled key in id order (coalesced record loads)
       L = F.iota;
-      total = 2u * (uint32_t)kv.n_nodes;
+      total = F.iota_n;
       return total;
     }
     uint32_t cnt = 0;
@@ -511,9 +511,9 @@ __device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint3
   __syncwarp();  // the previous item's readers of L are done
   wn = 0;
   L = Lw;
-  if (dense) {  // all 2R^3 keys in id order (coalesced record loads)
+  if (dense) {  // every enabled key in id order (coalesced record loads)
     L = F.iota;
-    wn = 2u * (uint32_t)kv.n_nodes;
+    wn = F.iota_n;
   } else {
     uint32_t cnt = 0;
     stream_list<4>(kv, kv.bl_pool + __ldg(&kv.bl_off[it.z]), nb, box, [&](bool pass, uint32_t id) {

@@ -419,6 +419,12 @@ int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s) {
   return 1;
 }
 
+int launch_item_lists(const FwdArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  k_item_lists<<<(unsigned)((n_items + IL_WARPS - 1) / IL_WARPS), 32 * IL_WARPS, 0, s>>>(a);
+  return 1;
+}
+
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   const unsigned blocks = (unsigned)((n_items + NWARP - 1) / NWARP);

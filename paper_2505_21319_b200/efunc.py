@@ -16,6 +16,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EFUNC_LIB_PATH") or os.path.join(_PKG, "lib", "libefunc.so")
 
 NCH = 13
+# model families of Table 3: include/efunc.h efunc_variant
+VARIANT_COMBINED, VARIANT_GRID, VARIANT_OFFSET = 0, 1, 2
 OK, EINVAL, ESTATE, ENONFINITE, ECUDA, ENOMEM = range(6)
 LOSS_NONE, LOSS_MSE, LOSS_MSE_EIKONAL = 0, 1, 2
 # default decay mask (reading R-10 / SPEC D15): polynomial coefficients c, g of both banks
@@ -26,7 +28,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
             "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
             "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_sync", "efunc_last_error",
-            "efunc_mesh",
+            "efunc_mesh", "efunc_channels",
             "efunc_abi_version"]
 
 
@@ -101,6 +103,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.efunc_last_error.restype = C.c_char_p
     lib.efunc_abi_version.argtypes = []
     lib.efunc_abi_version.restype = C.c_int32
+    lib.efunc_channels.argtypes = [C.c_int32, C.c_int32]
+    lib.efunc_channels.restype = C.c_int32
     _lib = lib
     return lib
 
@@ -145,18 +149,35 @@ class AdamW:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 1e-2
-    decay_mask: int = DEFAULT_DECAY_MASK
+    decay_mask: int | None = None  # None: the polynomial coefficients of the handle's layout (SPEC D15)
 
-    def c(self) -> AdamWParams:
-        return AdamWParams(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.decay_mask)
+    def c(self, default_mask: int = DEFAULT_DECAY_MASK) -> AdamWParams:
+        mask = default_mask if self.decay_mask is None else self.decay_mask
+        return AdamWParams(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, mask)
+
+
+def _coef_mask(variant: int, degree: int) -> int:
+    """Weight-decay mask of a layout (reading R-10, SPEC D15): the polynomial coefficients c, g (and H)
+    of every bank; scales s and offsets Delta are not decayed."""
+    if variant == VARIANT_COMBINED and degree <= 1:
+        return DEFAULT_DECAY_MASK
+    coef = {0: 1, 1: 4, 2: 10}[degree]
+    mask, o = 0, 0
+    if variant != VARIANT_OFFSET:
+        mask |= ((1 << coef) - 1) << (o + 1)
+        o += 1 + coef
+    if variant != VARIANT_GRID:
+        mask |= ((1 << coef) - 1) << (o + 4)
+    return mask
 
 
 class EFunc:
-    """One efunc grid (O^{+Delta}, degree 1, R^3 x 13) on one CUDA device."""
+    """One efunc grid on one CUDA device: O^{+Delta} with degree-1 polynomials (R^3 x 13) by default,
+    or another Table 3 family (variant, degree; R^3 x efunc_channels(variant, degree))."""
 
     def __init__(self, R: int, theta=None, cutoff_T: float = 20.0, device: int = 0,
                  deterministic: bool = False, sync_checks: bool = False, fit_graph: bool = True,
-                 n_shapes: int = 1, degree: int = 1):
+                 n_shapes: int = 1, degree: int = 1, variant: int = VARIANT_COMBINED):
         """n_shapes > 1: S independent grids in one handle (BASELINE config C5); theta, grads and
         the per-query arrays then carry a leading [S] axis and J counts queries per shape."""
         import torch
@@ -164,16 +185,20 @@ class EFunc:
         self.R = int(R)
         self.S = max(1, int(n_shapes))
         self.device = int(device)
-        self.n_params = self.S * self.R ** 3 * NCH
-        cfg = Config(self.R, int(degree), 0, float(cutoff_T), int(deterministic), self.device, int(sync_checks),
-                     int(fit_graph), self.S)
+        self.nch = int(self.lib.efunc_channels(int(variant), int(degree)))
+        if self.nch < 0:
+            raise ValueError(f"unsupported (variant, degree) = ({variant}, {degree})")
+        self.n_params = self.S * self.R ** 3 * self.nch
+        self.decay_mask = _coef_mask(int(variant), int(degree))
+        cfg = Config(self.R, int(degree), int(variant), float(cutoff_T), int(deterministic), self.device,
+                     int(sync_checks), int(fit_graph), self.S)
         th = None
         if theta is not None:
             if isinstance(theta, torch.Tensor):
                 theta = theta.detach().cpu().numpy()
             th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
             if th.size != self.n_params:
-                raise ValueError("theta must have n_shapes*R^3*13 elements")
+                raise ValueError(f"theta must have n_shapes*R^3*{self.nch} elements")
         h = C.c_void_p()
         st = self.lib.efunc_create(C.byref(cfg), None if th is None else th.ctypes.data, C.byref(h))
         if st != OK:
@@ -206,7 +231,7 @@ class EFunc:
         return self._torch.empty(*shape, dtype=self._torch.float32, device=f"cuda:{self.device}")
 
     def _grad_zeros(self):
-        shape = (self.R ** 3, NCH) if self.S == 1 else (self.S, self.R ** 3, NCH)
+        shape = (self.R ** 3, self.nch) if self.S == 1 else (self.S, self.R ** 3, self.nch)
         return self._torch.zeros(*shape, dtype=self._torch.float32, device=f"cuda:{self.device}")
 
     def _J(self, q):
@@ -214,7 +239,7 @@ class EFunc:
         return q.numel() // (3 * self.S)
 
     def _pshape(self):
-        return (self.R ** 3, NCH) if self.S == 1 else (self.S, self.R ** 3, NCH)
+        return (self.R ** 3, self.nch) if self.S == 1 else (self.S, self.R ** 3, self.nch)
 
     # ---------------------------------------------------------------- API
     def forward(self, q, o=None, loss: int = LOSS_NONE, eikonal_lambda: float = 0.1, J_global: int = 0,
@@ -260,7 +285,7 @@ class EFunc:
     def adamw_step(self, grad, hp: AdamW | None = None):
         hp = hp or AdamW()
         _check_dev(grad, "grad", self.n_params, self.device)
-        p = hp.c()
+        p = hp.c(self.decay_mask)
         self._ok(self.lib.efunc_adamw_step(self.h, _ptr(grad), C.byref(p), self._stream()))
 
     def eval_grad(self, q, want_O=True, want_G=True):
@@ -306,7 +331,7 @@ class EFunc:
         hp = hp or AdamW()
         J = self._J(q)
         lc = Loss(loss, eikonal_lambda, J_global)
-        p = hp.c()
+        p = hp.c(self.decay_mask)
         host = q.device.type == "cpu"
         _check_io(q, "q", 3 * J * self.S, self.device, host, pinned=host and pipelined)
         _check_io(o, "o", J * self.S, self.device, host, pinned=host and pipelined)

@@ -46,6 +46,22 @@ def test_abi_version_callable_without_gpu(lib):
     assert lib.efunc_abi_version() == 1
 
 
+def test_variant_channel_counts_without_gpu(lib):
+    """efunc_channels (NEXT-4) against Table 3's "Ch" column and the variant
+    oracle's layout."""
+    from oracle import variant_oracle as vo
+    lib.efunc_channels.restype = ctypes.c_int32
+    lib.efunc_channels.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    assert lib.efunc_channels(0, 1) == 13 and lib.efunc_channels(0, 0) == 13  # Full-4 / G-0 tie
+    assert lib.efunc_channels(1, 2) == 11   # G-7
+    assert lib.efunc_channels(1, 1) == 5    # G-6
+    assert lib.efunc_channels(1, 0) == 2    # G-5
+    assert lib.efunc_channels(2, 1) == 8    # Full-1
+    for v, banks in ((0, vo.BOTH), (1, vo.GRID), (2, vo.OFFSET)):
+        assert lib.efunc_channels(v, 2) == vo.n_channels(banks, 2)
+    assert lib.efunc_channels(3, 1) == -1 and lib.efunc_channels(0, 3) == -1
+
+
 def test_struct_sizes_match_header():
     """Compile a tiny C program against the header and compare sizeof with the ctypes mirrors."""
     from paper_2505_21319_b200 import efunc
