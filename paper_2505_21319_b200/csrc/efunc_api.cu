@@ -304,7 +304,7 @@ void free_all(efunc_t* h) {
   dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items); dfree(h->item_o);
-  dfree(h->scratch); dfree(h->iota);
+  dfree(h->scratch); dfree(h->iota); dfree(h->dn_zm); dfree(h->dn_dq);
   drop_fit_graph(h);
   free_timing(h);
   for (int k = 0; k < 2; ++k) {
@@ -613,10 +613,29 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
   f.pre = (!eik && !dense && !fit_pre_off()) ? 1 : 0;
-  const int slot = timing_begin(h, s);
-  if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
-  h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
-  timing_end(h, slot, s);
+  if (dense && !eik) {  // NEXT-2: key-sliced dense kernels (all warp slots busy at small J)
+    const int64_t nz = dense_zm_elems(h->fwd_items_bound, h->iota_n);
+    if (nz > h->dn_zm_cap) {
+      drop_fit_graph(h);
+      dfree(h->dn_zm);
+      CK(dalloc(&h->dn_zm, (size_t)nz));
+      h->dn_zm_cap = nz;
+    }
+    if (h->fwd_items_bound * 48 > h->dn_dq_cap) {
+      drop_fit_graph(h);
+      dfree(h->dn_dq);
+      CK(dalloc(&h->dn_dq, (size_t)h->fwd_items_bound * 48));
+      h->dn_dq_cap = h->fwd_items_bound * 48;
+    }
+    const int slot = timing_begin(h, s);
+    h->launches += launch_dense_fit(f, h->fwd_items_bound, h->dn_zm, h->dn_dq, s, nullptr);
+    timing_end(h, slot, s);
+  } else {
+    const int slot = timing_begin(h, s);
+    if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
+    h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
+    timing_end(h, slot, s);
+  }
   // items the fused kernel left (no brick list / shift-bound overflow): the split kernels
   h->fwd_J = J;
   h->launches += launch_forward_slow(a, eik, s);

@@ -228,6 +228,9 @@ int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s);
+// dense mode (cutoff_T = inf, MSE): key-sliced forward, combine, key-stationary backward (k_fit.cu)
+int64_t dense_zm_elems(int64_t n_items, uint32_t iota_n);
+int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, cudaStream_t s, int* fwd_launches);
 int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
@@ -290,6 +293,10 @@ struct efunc {
   float* gint = nullptr;            // [R^3][13] internal gradient scratch (vmode)
   float* gH = nullptr;              // [R^3][12] degree-2 gradient scratch
   uint32_t iota_n = 0;
+  float2* dn_zm = nullptr;          // dense mode: per (item, key slice) partial Z, M
+  int64_t dn_zm_cap = 0;
+  float4* dn_dq = nullptr;          // dense mode: per item packed query table for the backward
+  int64_t dn_dq_cap = 0;
   // keys
   float4* key_raw = nullptr;
   float4* key_sorted = nullptr;

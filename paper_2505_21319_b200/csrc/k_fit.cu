@@ -709,6 +709,213 @@ __global__ void __launch_bounds__(32 * FL_WARPS, 3) k_fit_lists(const FitArgs F)
   }
 }
 
+// ------------------------------------------------------------------ dense mode (cutoff_T = inf)
+// every (query, key) pair, the paper's own Table 4 setting.
+// With few queries (Table 4: J = 16384, ~550 work items) one warp per item leaves most of the 2368
+// warp slots idle, so the pass is split three ways:
+//   k_dense_fwd      (item, key slice) units: the slice's partial Z_j, M_j of the item's queries
+//                    (lanes = keys, the item-local expansion of k_fit's forward);
+//   k_dense_combine  per item: Z_j, M_j summed over the slices in slice order, O_j, the MSE loss,
+//                    rho_j = r_j / Z_j and the item's packed query table for the backward;
+//   k_dense_bwd      (block of 64 keys, group of items) units, key-stationary as Alg. 2
+//                    (PAPER.md:L540-568): two keys per lane accumulate over every query of the
+//                    group in registers (direct form, d = q - k), two red.v4 per key and group.
+constexpr int DN_WARPS = 4;
+
+__global__ void __launch_bounds__(32 * DN_WARPS) k_dense_fwd(const FitArgs F, float2* __restrict__ zm, int S,
+                                                             uint32_t ks) {
+  __shared__ FitSmem smem[DN_WARPS];
+  FitSmem& Sm = smem[threadIdx.x >> 5];
+  const FwdArgs& A = F.f;
+  const uint32_t u = blockIdx.x * DN_WARPS + (threadIdx.x >> 5);
+  const uint32_t item = u / (uint32_t)S, sl = u % (uint32_t)S;
+  if (item >= *A.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  const float4 q = act ? A.qs[js] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const Box box = warp_box(act, q.x, q.y, q.z, 0.0f);
+  const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
+  const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
+  const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;
+  {
+    const float xo = __shfl_xor_sync(~0u, qx, 1), yo = __shfl_xor_sync(~0u, qy, 1);
+    const float zo = __shfl_xor_sync(~0u, qz, 1), qo = __shfl_xor_sync(~0u, qq, 1);
+    if ((lane & 1) == 0) {
+      Sm.qa[lane >> 1] = make_float4(qx, xo, qy, yo);
+      Sm.qb[lane >> 1] = make_float4(qz, zo, qq, qo);
+    }
+  }
+  __syncwarp();
+  const uint32_t k0 = sl * ks;
+  const uint32_t wn = k0 < F.iota_n ? min(ks, F.iota_n - k0) : 0u;
+  float Z, M;
+  if (nact <= 16) fwd_sums_x<8>(A.kv, F.iota + k0, wn, nact, o, Sm.qa, Sm.qb, Z, M);
+  else fwd_sums_x<16>(A.kv, F.iota + k0, wn, nact, o, Sm.qa, Sm.qb, Z, M);
+  zm[(size_t)u * 32 + lane] = make_float2(Z, M);
+}
+
+__global__ void k_dense_combine(const FitArgs F, const float2* __restrict__ zm, int S, float4* __restrict__ dq) {
+  const FwdArgs& A = F.f;
+  const uint32_t item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= *A.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float Z = 0.f, M = 0.f;
+  for (int s = 0; s < S; ++s) {  // slice order: the sums do not depend on the schedule
+    const float2 v = zm[((size_t)item * S + s) * 32 + lane];
+    Z += v.x;
+    M += v.y;
+  }
+  const float4 q = act ? A.qs[js] : make_float4(1e6f, 1e6f, 1e6f, 0.f);
+  const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
+  const bool slow = __any_sync(~0u, bad);  // Z underflow: the split kernels shift exactly
+  float O = 0.f, rho = 0.f, lossj = 0.f;
+  if (act && !slow) {
+    const float iz = 1.0f / Z;
+    O = M * iz;
+    const float diff = O - q.w;
+    rho = 2.0f * diff * A.inv_J * iz;
+    lossj = diff * diff * A.inv_J;
+    if (A.O) A.O[A.perm[js]] = O;
+  }
+  for (int s = 16; s > 0; s >>= 1) lossj += __shfl_xor_sync(~0u, lossj, s);
+  if (lane == 0) {
+    if (slow) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    else A.loss_part[item] = lossj;
+    atomicAdd(&A.ds->cand_pairs, (unsigned long long)F.iota_n * (unsigned long long)nact);
+  }
+  // packed query pairs for the backward: {x0,x1,y0,y1}, {z0,z1,rho0,rho1}, {-O0,-O1,0,0}; an idle
+  // (or slow-path) slot is far away with rho = 0: it contributes exactly 0
+  const float x = (act && !slow) ? q.x : 1e6f, y = (act && !slow) ? q.y : 1e6f, z = (act && !slow) ? q.z : 1e6f;
+  const float xo = __shfl_xor_sync(~0u, x, 1), yo = __shfl_xor_sync(~0u, y, 1), zo = __shfl_xor_sync(~0u, z, 1);
+  const float ro = __shfl_xor_sync(~0u, rho, 1), Oo = __shfl_xor_sync(~0u, O, 1);
+  if ((lane & 1) == 0) {
+    float4* d = dq + (size_t)item * 48;
+    d[lane >> 1] = make_float4(x, xo, y, yo);
+    d[16 + (lane >> 1)] = make_float4(z, zo, rho, ro);
+    d[32 + (lane >> 1)] = make_float4(-O, -Oo, 0.f, 0.f);
+  }
+}
+
+// OFF: the block's keys are offset-bank keys (the Delta sums are needed; grid keys are fixed)
+template <bool OFF>
+__device__ __forceinline__ void dense_bwd_unit(const FitArgs& F, const float4* __restrict__ dq, float4* Q,
+                                               uint32_t kb, uint32_t i0, uint32_t i1) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t kA = kb * 64u + lane, kB = kA + 32u;
+  const uint32_t idA = kA < F.iota_n ? F.iota[kA] : 0u, idB = kB < F.iota_n ? F.iota[kB] : 0u;
+  float4 aA = far_a, bA = z4, aB = far_a, bB = z4;
+  if (kA < F.iota_n) ld_rec(&kv.grid_raw[2 * idA], aA, bA);
+  if (kB < F.iota_n) ld_rec(&kv.grid_raw[2 * idB], aB, bB);
+  float2 Sc[2], Sgx[2], Sgy[2], Sgz[2], Ss[2], Sdx[2], Sdy[2], Sdz[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) Sc[k] = Sgx[k] = Sgy[k] = Sgz[k] = Ss[k] = Sdx[k] = Sdy[k] = Sdz[k] = make_float2(0.f, 0.f);
+  auto pair = [&](const int k, const float4 a, const float4 b, const float4 QA, const float4 QB, const float4 QC) {
+    const float2 dx = __fadd2_rn(make_float2(QA.x, QA.y), make_float2(-a.x, -a.x));
+    const float2 dy = __fadd2_rn(make_float2(QA.z, QA.w), make_float2(-a.y, -a.y));
+    const float2 dz = __fadd2_rn(make_float2(QB.x, QB.y), make_float2(-a.z, -a.z));
+    float2 dd = __fmul2_rn(dz, dz);
+    dd = __ffma2_rn(dy, dy, dd);
+    dd = __ffma2_rn(dx, dx, dd);
+    const float2 e = __fmul2_rn(make_float2(-a.w, -a.w), dd);
+    const float2 t = __fmul2_rn(make_float2(QB.z, QB.w), make_float2(ex2f(e.x), ex2f(e.y)));
+    float2 f = __ffma2_rn(make_float2(b.y, b.y), dx, make_float2(b.x, b.x));
+    f = __ffma2_rn(make_float2(b.z, b.z), dy, f);
+    f = __ffma2_rn(make_float2(b.w, b.w), dz, f);
+    const float2 uu = __fmul2_rn(t, __fadd2_rn(f, make_float2(QC.x, QC.y)));
+    Sc[k] = __fadd2_rn(Sc[k], t);
+    Sgx[k] = __ffma2_rn(t, dx, Sgx[k]);
+    Sgy[k] = __ffma2_rn(t, dy, Sgy[k]);
+    Sgz[k] = __ffma2_rn(t, dz, Sgz[k]);
+    Ss[k] = __ffma2_rn(uu, dd, Ss[k]);
+    if (OFF) {
+      Sdx[k] = __ffma2_rn(uu, dx, Sdx[k]);
+      Sdy[k] = __ffma2_rn(uu, dy, Sdy[k]);
+      Sdz[k] = __ffma2_rn(uu, dz, Sdz[k]);
+    }
+  };
+  for (uint32_t item = i0; item < i1; ++item) {
+    const int npairs = (__ldg(&A.items[item].y) + 1) >> 1;
+    __syncwarp();
+    const float4* src = dq + (size_t)item * 48;
+    Q[lane] = __ldcg(&src[lane]);
+    if (lane < 16) Q[32 + lane] = __ldcg(&src[32 + lane]);
+    __syncwarp();
+    for (int p = 0; p < npairs; ++p) {
+      const float4 QA = Q[p], QB = Q[16 + p], QC = Q[32 + p];
+      pair(0, aA, bA, QA, QB, QC);
+      pair(1, aB, bB, QA, QB, QC);
+    }
+  }
+  auto fin = [&](const int k, MseSums& m) {
+    m.sc = Sc[k].x + Sc[k].y;
+    m.sgx = Sgx[k].x + Sgx[k].y; m.sgy = Sgy[k].x + Sgy[k].y; m.sgz = Sgz[k].x + Sgz[k].y;
+    m.ss = Ss[k].x + Ss[k].y;
+    m.sdx = Sdx[k].x + Sdx[k].y; m.sdy = Sdy[k].x + Sdy[k].y; m.sdz = Sdz[k].x + Sdz[k].y;
+  };
+  MseSums m0, m1;
+  fin(0, m0);
+  fin(1, m1);
+  if (i0 < i1) {
+    if (kA < F.iota_n) bwd_mse_red(m0, aA, bA, (int)idA, kv.n_nodes, F.gpad);
+    if (kB < F.iota_n) bwd_mse_red(m1, aB, bB, (int)idB, kv.n_nodes, F.gpad);
+  }
+}
+
+__global__ void __launch_bounds__(32 * DN_WARPS) k_dense_bwd(const FitArgs F, const float4* __restrict__ dq, int G) {
+  __shared__ float4 stage[DN_WARPS][48];
+  const uint32_t u = blockIdx.x * DN_WARPS + (threadIdx.x >> 5);
+  const uint32_t kb = u / (uint32_t)G, g = u % (uint32_t)G;
+  if (kb * 64u >= F.iota_n) return;
+  const uint32_t n_items = *F.f.n_items;
+  const uint32_t ipg = (n_items + G - 1) / G;
+  const uint32_t i0 = g * ipg, i1 = min(n_items, i0 + ipg);
+  // a block holds grid keys only or offset keys only unless it straddles the bank boundary
+  const uint32_t last = min(kb * 64u + 63u, F.iota_n - 1u);
+  if (F.iota[last] < (uint32_t)F.f.kv.n_nodes) dense_bwd_unit<false>(F, dq, stage[threadIdx.x >> 5], kb, i0, i1);
+  else dense_bwd_unit<true>(F, dq, stage[threadIdx.x >> 5], kb, i0, i1);
+}
+
+// work split of the three dense kernels for n_items items (a launch bound) and iota_n keys
+static void dense_split(int64_t n_items, uint32_t iota_n, int& S, uint32_t& ks, int& G) {
+  const int64_t target = 148 * 16 * 4;  // units: ~4 per warp slot
+  S = (int)std::max<int64_t>(1, std::min<int64_t>((target + n_items - 1) / std::max<int64_t>(n_items, 1),
+                                                    (iota_n + 255) / 256));
+  ks = ((iota_n + S - 1) / S + 31) & ~31u;
+  const int64_t kblocks = (iota_n + 63) / 64;
+  G = (int)std::max<int64_t>(1, std::min<int64_t>((target + kblocks - 1) / kblocks, n_items));
+}
+
+int64_t dense_zm_elems(int64_t n_items, uint32_t iota_n) {
+  int S, G;
+  uint32_t ks;
+  dense_split(n_items, iota_n, S, ks, G);
+  return n_items * S * 32;
+}
+
+int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, cudaStream_t s, int* fwd_launches) {
+  if (n_items <= 0) return 0;
+  int S, G;
+  uint32_t ks;
+  dense_split(n_items, a.iota_n, S, ks, G);
+  const int64_t ufwd = n_items * S;
+  k_dense_fwd<<<(unsigned)((ufwd + DN_WARPS - 1) / DN_WARPS), 32 * DN_WARPS, 0, s>>>(a, zm, S, ks);
+  k_dense_combine<<<(unsigned)((n_items + 3) / 4), 128, 0, s>>>(a, zm, S, dq);
+  const int64_t ubwd = ((a.iota_n + 63) / 64) * (int64_t)G;
+  k_dense_bwd<<<(unsigned)((ubwd + DN_WARPS - 1) / DN_WARPS), 32 * DN_WARPS, 0, s>>>(a, dq, G);
+  if (fwd_launches) *fwd_launches = 2;
+  return 3;
+}
+
 int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   k_fit_lists<<<(unsigned)((n_items + FL_WARPS - 1) / FL_WARPS), 32 * FL_WARPS, 0, s>>>(a);

@@ -15,9 +15,10 @@ p.add_argument("--R", type=int, default=32)
 p.add_argument("--J", type=int, default=1 << 20)
 p.add_argument("--eikonal", action="store_true")
 p.add_argument("--split", action="store_true", help="forward + backward instead of forward_backward")
+p.add_argument("--dense", action="store_true", help="cutoff_T = inf (every pair)")
 a = p.parse_args()
 tor = synth.Torus()
-m = ef.EFunc(a.R, synth.init_theta(a.R, 1234))
+m = ef.EFunc(a.R, synth.init_theta(a.R, 1234), cutoff_T=float("inf") if a.dense else 20.0)
 m.mean_shift_init(torch.as_tensor(synth.surface_points(tor, 16384, 1234)).cuda())
 q, o = synth.sample_batch(tor, a.J, seed=99)
 qd, od = torch.as_tensor(q).cuda(), torch.as_tensor(o).cuda()

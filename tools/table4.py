@@ -50,8 +50,16 @@ def main():
             fwd()
             t_b = timed(lambda: m.backward(grad=grad), reps)
             t_fb = timed(lambda: m.forward_backward(qd, od, grad=grad, want_loss=False), reps)
-            rows.append({"R": R, "T": T, "fwd_ms": t_f, "bwd_ms": t_b, "fused_fwd_bwd_ms": t_fb,
-                         "paper_fwd_ms": PAPER[R][0], "paper_bwd_ms": PAPER[R][1]})
+            row = {"R": R, "T": T, "fwd_ms": t_f, "bwd_ms": t_b, "fused_fwd_bwd_ms": t_fb,
+                   "paper_fwd_ms": PAPER[R][0], "paper_bwd_ms": PAPER[R][1]}
+            if T == float("inf"):
+                # every pair is evaluated: direct-form lane-ops 12 (forward) + 18 / 21 (MSE backward,
+                # grid / offset bank) per pair, measured FFMA peak 35.22 T lane-op/s
+                ops = a.J * R ** 3 * ((12 + 18) + (12 + 21))
+                row["dense_pairs"] = a.J * 2 * R ** 3
+                row["fused_Tlaneops_per_s"] = ops / (t_fb * 1e-3) / 1e12
+                row["fused_frac_fp32"] = row["fused_Tlaneops_per_s"] / 35.22
+            rows.append(row)
             print(json.dumps(rows[-1]), flush=True)
     lines = ["# Table 4 on B200 (J = 16384 queries; torus, paper init + mean-shift offsets)", "",
              "Paper: PAPER.md:L842-846 (Table 4), their CUDA kernels, GPU/variant unstated, dense global sums. "
@@ -59,12 +67,13 @@ def main():
              "times; forward = efunc_forward (O + MSE upstream), backward = efunc_backward (MSE), fused = "
              "efunc_forward_backward. T = inf evaluates every pair (the paper's definition); T = 20 is the "
              "certified cutoff (DESIGN.md R-1).", "",
-             "| I (per bank) | T | fwd ms | bwd ms | fused fwd+bwd ms | paper fwd ms | paper bwd ms | paper / ours (fwd+bwd) |",
-             "|---|---|---|---|---|---|---|---|"]
+             "| I (per bank) | T | fwd ms | bwd ms | fused fwd+bwd ms | paper fwd ms | paper bwd ms | paper / ours (fwd+bwd) | fused frac of FP32 peak (dense) |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         ours = min(r["fwd_ms"] + r["bwd_ms"], r["fused_fwd_bwd_ms"])
         lines.append(f"| {r['R']}^3 | {r['T']:g} | {r['fwd_ms']:.3f} | {r['bwd_ms']:.3f} | {r['fused_fwd_bwd_ms']:.3f} | "
-                     f"{r['paper_fwd_ms']} | {r['paper_bwd_ms']} | {(r['paper_fwd_ms'] + r['paper_bwd_ms']) / ours:.1f}x |")
+                     f"{r['paper_fwd_ms']} | {r['paper_bwd_ms']} | {(r['paper_fwd_ms'] + r['paper_bwd_ms']) / ours:.1f}x | "
+                     + (f"{r['fused_frac_fp32']:.2f} |" if "fused_frac_fp32" in r else "— |"))
     txt = "\n".join(lines) + "\n"
     print(txt)
     if a.out:
