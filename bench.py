@@ -82,7 +82,7 @@ def parse():
     p.add_argument("--eager", action="store_true", help="N=1: plain launches instead of a CUDA graph per step")
     p.add_argument("--split", action="store_true", help="efunc_forward + efunc_backward instead of the fused call")
     p.add_argument("--deterministic", action="store_true",
-                   help="deterministic mode (stable sorts, 64-bit fixed-point gradient sums; split path)")
+                   help="deterministic mode (stable sorts, 64-bit fixed-point gradient sums in the fused kernel)")
     return p.parse_args()
 
 
@@ -462,7 +462,7 @@ def run_ours(args, rank, world, local_rank, nccl):
         return
     # roofline of the dominant kernel: algorithmic lane-ops per launch / its time. k_fit (fused,
     # MSE) does the forward and the backward of every kept pair; k_backward only the backward.
-    fused = not (args.split or args.deterministic)
+    fused = not args.split
     kname = ("k_fit" if loss_kind == "mse" else "k_fit_eik") if fused else "k_backward"
     if loss_kind == "mse":
         ops = OPS_BWD_GRID * (kept - kept_off) + OPS_BWD_OFF * kept_off
@@ -514,7 +514,7 @@ def run_ours(args, rank, world, local_rank, nccl):
                                       "gloo all_reduce (shared-GPU code-path run, not a measurement)")
                                      if reduce_grad else None,
                        "deterministic": bool(args.deterministic),
-                       "path": "split forward/backward" if (args.split or args.deterministic) else
+                       "path": "split forward/backward" if args.split else
                                f"efunc_forward_backward (fused {'k_fit' if loss_kind == 'mse' else 'k_fit_eik'})",
                        "l2": f"inputs larger than L2: pool of {pool} batches x {n_pts * 16 / 1e6:.1f} MB cycled"},
             "roofline": roof, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,

@@ -587,7 +587,9 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   if (!loss || loss->kind == EFUNC_LOSS_NONE) return fail(h, EFUNC_EINVAL, "forward_backward needs a loss");
   const int eik = loss->kind == EFUNC_LOSS_MSE_EIKONAL;
   const bool dense = std::isinf(cutoff_log2(h->cfg));
-  const int fused = !h->cfg.deterministic && !h->count_kept && !(eik && dense);  // (dense Eikonal: split)
+  // deterministic mode: the fused MSE kernel with 64-bit fixed-point sums (cutoff mode); otherwise split
+  const int det = h->cfg.deterministic;
+  const int fused = !h->count_kept && !(eik && dense) && !(det && (eik || dense));
   if (!fused || J == 0) {
     RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
     RET(do_backward(h, nullptr, nullptr, grad, s));
@@ -610,9 +612,16 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.iota = dense ? h->iota : nullptr;
   f.iota_n = h->iota_n;
   f.item_o = h->item_o;
+  f.gfix = det ? h->gfix : nullptr;
+  f.umax = &h->ds->umax;
+  f.fix_overflow = &h->ds->fix_overflow;
+  if (det) {  // the fixed-point unit: an a-priori bound of max_j |r_j| (k_det_bound)
+    CK(cudaMemsetAsync(&h->ds->umax, 0, sizeof(float), s));
+    h->launches += launch_det_bound(h->theta, h->n_nodes, h->qs, J, a.inv_J, &h->ds->umax, s);
+  }
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
-  f.pre = (!eik && !dense && !fit_pre_off()) ? 1 : 0;
+  f.pre = (!eik && !dense && !det && !fit_pre_off()) ? 1 : 0;
   if (dense && !eik) {  // NEXT-2: key-sliced dense kernels (all warp slots busy at small J)
     const int64_t nz = dense_zm_elems(h->fwd_items_bound, h->iota_n);
     if (nz > h->dn_zm_cap) {
@@ -642,8 +651,14 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   BwdArgs b = bwd_args(h, nullptr, nullptr, grad, eik);
   b.list = h->slow_items;
   b.list_n = &h->ds->slow_n;
-  h->launches += launch_backward(b, h->fwd_items_bound, s);
-  h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+  CK(cudaMemsetAsync(&h->ds->bwd_next, 0, sizeof(uint32_t), s));
+  if (det) {  // fixed point with the unit k_det_bound set, then folded into grad
+    h->launches += launch_backward_list_det(b, s);
+    h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);
+  } else {
+    h->launches += launch_backward(b, h->fwd_items_bound, s);
+    h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+  }
   if (loss_out) h->launches += launch_sum_partials(h->loss_part, a.n_items, 1, loss_out, s);
   CK(cudaGetLastError());
   if (h->cfg.sync_checks) {

@@ -172,6 +172,11 @@ struct FitArgs {
   uint32_t iota_n;        // their count (2R^3 with both banks)
   int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
   float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
+  // deterministic mode: 64-bit fixed-point accumulation (BwdArgs::gfix) with the unit umax * 2^-FIX_BITS,
+  // umax an a-priori bound of max_j |r_j| (k_det_bound); null gfix: float reds into gpad
+  unsigned long long* gfix;
+  const float* umax;
+  uint32_t* fix_overflow;
 };
 
 constexpr int FIX_BITS = 36;  // resolution umax * 2^-36; range |partial| < umax * 2^26
@@ -228,6 +233,9 @@ int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s);
+int launch_det_bound(const float* theta, int n_nodes, const float4* qs, int64_t J, float inv_J, float* umax,
+                     cudaStream_t s);
+int launch_backward_list_det(const BwdArgs& a, cudaStream_t s);
 // dense mode (cutoff_T = inf, MSE): key-sliced forward, combine, key-stationary backward (k_fit.cu)
 int64_t dense_zm_elems(int64_t n_items, uint32_t iota_n);
 int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, cudaStream_t s, int* fwd_launches);

@@ -331,6 +331,46 @@ int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s) {
   return 2;
 }
 
+// Deterministic fused path: the fixed-point unit must be known before the fused kernel computes
+// the upstreams, so it comes from an a-priori bound of max_j |r_j| = 2 |O_j - o_j| / J: O_j is a
+// convex combination of key polynomials f_i(q_j) = c_i + g_i.(q_j - k_i) with |q_a - k_a| <= 2 +
+// |Delta_a| for in-domain queries, so |r_j| <= 2/J (max_i (|c_i| + |g_i|_1 (2 + |Delta_i|_inf))
+// + max_j |o_j|) <= 4/J max(...). A max is independent of the order the atomics land in.
+__global__ void k_det_bound(const float* __restrict__ theta, int n_nodes, const float4* __restrict__ qs, int64_t J,
+                            float inv_J, float* umax) {
+  float m = 0.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n_nodes + J;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n_nodes) {
+      const float* t = theta + (size_t)i * EF_NCH;
+      const float dm = fmaxf(fabsf(t[5]), fmaxf(fabsf(t[6]), fabsf(t[7])));
+      const float f0 = fabsf(t[1]) + (fabsf(t[2]) + fabsf(t[3]) + fabsf(t[4])) * 2.0f;
+      const float f1 = fabsf(t[9]) + (fabsf(t[10]) + fabsf(t[11]) + fabsf(t[12])) * (2.0f + dm);
+      m = fmaxf(m, fmaxf(f0, f1));
+    } else {
+      m = fmaxf(m, fabsf(qs[i - n_nodes].w));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(~0u, m, o));
+  m *= 4.0f * inv_J;
+  if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(umax), __float_as_uint(m));
+}
+
+int launch_det_bound(const float* theta, int n_nodes, const float4* qs, int64_t J, float inv_J, float* umax,
+                     cudaStream_t s) {
+  const int64_t n = (int64_t)n_nodes + J;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_det_bound<<<blocks, 256, 0, s>>>(theta, n_nodes, qs, J, inv_J, umax);
+  return 1;
+}
+
+// the deterministic backward of the items in a.list (the fused path's leftovers) with the unit in
+// *a.umax as set before the fused kernel
+int launch_backward_list_det(const BwdArgs& a, cudaStream_t s) {
+  k_backward<false, true><<<148u, 32 * BW_WARPS, 0, s>>>(a);
+  return 1;
+}
+
 // grad[n][13] += fixed-point sums * umax * 2^-FIX_BITS; zero the accumulator
 __global__ void k_fold_fix(unsigned long long* __restrict__ gfix, const float* __restrict__ umax,
                            float* __restrict__ grad, int n_nodes) {

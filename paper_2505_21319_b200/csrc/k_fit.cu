@@ -78,6 +78,38 @@ __device__ __forceinline__ KeyX key_x(const float4 a, const float4 b, const floa
   return k;
 }
 
+// The key's 5 / 8 channel gradients of one item: float reds (bwd_mse_red), or in deterministic mode
+// 64-bit fixed-point integer atomics (order-independent sums, reading R-D) in k_backward's layout.
+__device__ __forceinline__ void bwd_mse_out(const FitArgs& F, const MseSums& s, const float4 a, const float4 b,
+                                            const int id) {
+  const int n_nodes = F.f.kv.n_nodes;
+  if (!F.gfix) {
+    bwd_mse_red(s, a, b, id, n_nodes, F.gpad);
+    return;
+  }
+  const float um = *F.umax;
+  const float scale = um > 0.0f ? (float)(1ull << FIX_BITS) / um : 0.0f;
+  auto fix_add = [&](unsigned long long* p, float v) {
+    const float qv = v * scale;
+    if (fabsf(qv) < 4.0e18f) atomicAdd(p, (unsigned long long)(long long)rintf(qv));
+    else atomicOr(F.fix_overflow, 1u);
+  };
+  const float beta = a.w * EF_LN2;
+  const float dsv = -beta * s.ss;
+  if (id < n_nodes) {
+    unsigned long long* gp = F.gfix + (size_t)id * 16;
+    fix_add(gp + 0, dsv); fix_add(gp + 1, s.sc); fix_add(gp + 2, s.sgx); fix_add(gp + 3, s.sgy);
+    fix_add(gp + 4, s.sgz);
+  } else {
+    unsigned long long* gp = F.gfix + (size_t)(id - n_nodes) * 16 + 8;
+    fix_add(gp + 0, fmaf(-b.y, s.sc, 2.0f * beta * s.sdx));
+    fix_add(gp + 1, fmaf(-b.z, s.sc, 2.0f * beta * s.sdy));
+    fix_add(gp + 2, fmaf(-b.w, s.sc, 2.0f * beta * s.sdz));
+    fix_add(gp + 3, dsv);
+    fix_add(gp + 4, s.sc); fix_add(gp + 5, s.sgx); fix_add(gp + 6, s.sgy); fix_add(gp + 7, s.sgz);
+  }
+}
+
 // exponent (log2 units, <= 0) and polynomial value of one key at a packed query pair
 #define FX_EF(K, QA, QB, e, f)                                                   \
   float2 e = __ffma2_rn(make_float2(K.nbl, K.nbl), make_float2(QB.z, QB.w), make_float2(K.C, K.C)); \
@@ -308,11 +340,11 @@ __device__ __forceinline__ void bwd_pass_x(const FitArgs& F, const uint32_t* L, 
     if (base + 32 < wn) {  // warp-uniform: two keys per lane
       MseSums s0, s1;
       bwd_sums_x2(key_x(a0, b0, o), key_x(a1, b1, o), npairs, S.qa, S.qb, S.pc, s0, s1);
-      if (k < wn) bwd_mse_red(s0, a0, b0, (int)idA, kv.n_nodes, F.gpad);
-      if (k + 32 < wn) bwd_mse_red(s1, a1, b1, (int)idB, kv.n_nodes, F.gpad);
+      if (k < wn) bwd_mse_out(F, s0, a0, b0, (int)idA);
+      if (k + 32 < wn) bwd_mse_out(F, s1, a1, b1, (int)idB);
     } else if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a0, b0, o), npairs, S.qa, S.qb, S.pc);
-      bwd_mse_red(ms, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+      bwd_mse_out(F, ms, a0, b0, (int)idA);
     }
   }
 #else
@@ -332,7 +364,7 @@ __device__ __forceinline__ void bwd_pass_x(const FitArgs& F, const uint32_t* L, 
     }
     if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
-      bwd_mse_red(ms, a, b, (int)id, kv.n_nodes, F.gpad);
+      bwd_mse_out(F, ms, a, b, (int)id);
     }
   }
 #endif
@@ -612,11 +644,11 @@ __device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_
     if (base + 32 < wn) {  // warp-uniform: two keys per lane
       MseSums s0, s1;
       bwd_sums_x2(key_x(a0, b0, o), key_x(a1, b1, o), npairs, S.qa, S.qb, S.pc, s0, s1);
-      if (k < wn) bwd_mse_red(s0, a0, b0, (int)idA, kv.n_nodes, F.gpad);
-      if (k + 32 < wn) bwd_mse_red(s1, a1, b1, (int)idB, kv.n_nodes, F.gpad);
+      if (k < wn) bwd_mse_out(F, s0, a0, b0, (int)idA);
+      if (k + 32 < wn) bwd_mse_out(F, s1, a1, b1, (int)idB);
     } else if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a0, b0, o), npairs, S.qa, S.qb, S.pc);
-      bwd_mse_red(ms, a0, b0, (int)idA, kv.n_nodes, F.gpad);
+      bwd_mse_out(F, ms, a0, b0, (int)idA);
     }
   }
 #else
@@ -636,7 +668,7 @@ __device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_
     }
     if (k < wn) {
       const MseSums ms = bwd_sums_x(key_x(a, b, o), npairs, S.qa, S.qb, S.pc);
-      bwd_mse_red(ms, a, b, (int)id, kv.n_nodes, F.gpad);
+      bwd_mse_out(F, ms, a, b, (int)id);
     }
   }
 #endif
