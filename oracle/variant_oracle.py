@@ -185,3 +185,40 @@ def backward(theta, R: int, q, fwd: VForward, dL_dO, banks: int = BOTH, degree: 
         put(lay["off"], slice(o, o + n))
         grad[:, lay["delta"]:lay["delta"] + 3] = dk[o:o + n]
     return grad
+
+
+# ------------------------------------------------------------------ cosine-series stacks (§4.4)
+def cosine_weights(q, B: int):
+    """w_b(q) = cos(b pi x) cos(b pi y) cos(b pi z), b = 0 .. B-1, and their q-gradients
+    (Eq. cosine-series; reading R-C: the 3-D cosine of "cos(b pi q)" is the
+    separable product, and b runs over B terms so that B = 1 is Config G-6).
+    Returns (W [B, J], dW [B, J, 3])."""
+    q = np.asarray(q, dtype=np.float64).reshape(-1, 3)
+    W = np.zeros((B, q.shape[0])); dW = np.zeros((B, q.shape[0], 3))
+    for b in range(B):
+        c = np.cos(b * np.pi * q); s = np.sin(b * np.pi * q)
+        W[b] = c[:, 0] * c[:, 1] * c[:, 2]
+        dW[b, :, 0] = -b * np.pi * s[:, 0] * c[:, 1] * c[:, 2]
+        dW[b, :, 1] = -b * np.pi * c[:, 0] * s[:, 1] * c[:, 2]
+        dW[b, :, 2] = -b * np.pi * c[:, 0] * c[:, 1] * s[:, 2]
+    return W, dW
+
+
+def cosine_forward(thetas, R: int, q, banks: int = GRID, degree: int = 1):
+    """S(q) = sum_b w_b(q) O_b(q) and dS/dq = sum_b (dw_b O_b + w_b G_b), each O_b a model of the
+    given family. thetas: [B, R^3, nch]. Returns (S, GS, per-band VForward list)."""
+    q = np.asarray(q, dtype=np.float64).reshape(-1, 3)
+    B = len(thetas)
+    W, dW = cosine_weights(q, B)
+    fs = [forward(thetas[b], R, q, banks, degree) for b in range(B)]
+    S = sum(W[b] * fs[b].O for b in range(B))
+    GS = sum(dW[b] * fs[b].O[:, None] + W[b][:, None] * fs[b].G for b in range(B))
+    return S, GS, fs
+
+
+def cosine_backward(thetas, R: int, q, fs, dL_dS, banks: int = GRID, degree: int = 1):
+    """dL/dtheta_b = backward of band b with upstream w_b(q_j) dL/dS_j (chain rule). [B, R^3, nch]."""
+    q = np.asarray(q, dtype=np.float64).reshape(-1, 3)
+    W, _ = cosine_weights(q, len(thetas))
+    return np.stack([backward(thetas[b], R, q, fs[b], W[b] * np.asarray(dL_dS, np.float64), banks, degree)
+                     for b in range(len(thetas))])

@@ -366,7 +366,7 @@ class EFunc:
     def set_params(self, theta):
         th = np.ascontiguousarray(np.asarray(theta, dtype=np.float32).reshape(-1))
         if th.size != self.n_params:
-            raise ValueError("theta must have n_shapes*R^3*13 elements")
+            raise ValueError(f"theta must have n_shapes*R^3*{self.nch} elements")
         self._ok(self.lib.efunc_set_params(self.h, th.ctypes.data, 0, self._stream()))
 
     def get_adam_state(self):

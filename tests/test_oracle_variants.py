@@ -122,3 +122,42 @@ def test_mse_gradient_matches_central_differences(banks, degree):
         tm = th.copy(); tm[idx] -= eps
         fd[idx] = (loss(tp) - loss(tm)) / (2 * eps)
     np.testing.assert_allclose(g, fd, atol=1e-7 * max(1.0, np.abs(fd).max()))
+
+
+def test_cosine_stack_b1_is_g6_and_weights():
+    """Eq. cosine-series: B = 1 is Config G-6 (w_0 = 1); the weights are the
+    separable cosines (reading R-C): w_b(0) = 1, w_b at the lattice point (1, 0, 0) is (-1)^b."""
+    R = 3
+    th = rand_theta(R, vo.GRID, 1, 50)
+    q = synth.rng(51).uniform(-1, 1, size=(13, 3))
+    S, GS, fs = vo.cosine_forward([th], R, q)
+    f = vo.forward(th, R, q, vo.GRID, 1)
+    np.testing.assert_allclose(S, f.O, rtol=0, atol=0)
+    np.testing.assert_allclose(GS, f.G, rtol=0, atol=0)
+    W, _ = vo.cosine_weights(np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]]), 4)
+    np.testing.assert_allclose(W[:, 0], 1.0)
+    np.testing.assert_allclose(W[:, 1], [1.0, -1.0, 1.0, -1.0], atol=1e-15)
+
+
+def test_cosine_stack_gradients_match_central_differences():
+    R, B = 2, 3
+    ths = [rand_theta(R, vo.GRID, 1, 60 + b) for b in range(B)]
+    q = synth.rng(61).uniform(-0.9, 0.9, size=(7, 3))
+    o = synth.rng(62).normal(size=7)
+    S, GS, fs = vo.cosine_forward(ths, R, q)
+    eps = 1e-6
+    for ax in range(3):
+        dq = np.zeros(3); dq[ax] = eps
+        fd = (vo.cosine_forward(ths, R, q + dq)[0] - vo.cosine_forward(ths, R, q - dq)[0]) / (2 * eps)
+        np.testing.assert_allclose(GS[:, ax], fd, atol=1e-7 * max(1.0, np.abs(fd).max()))
+    dS = 2.0 * (S - o) / len(o)
+    g = vo.cosine_backward(ths, R, q, fs, dS)
+
+    def loss(tt):
+        return np.mean((vo.cosine_forward(tt, R, q)[0] - o) ** 2)
+    for b in range(B):
+        for idx in [(0, 0), (3, 1), (5, 2), (7, 4)]:
+            tp = [t.copy() for t in ths]; tm = [t.copy() for t in ths]
+            tp[b][idx] += eps; tm[b][idx] -= eps
+            fd = (loss(tp) - loss(tm)) / (2 * eps)
+            assert abs(g[b][idx] - fd) <= 1e-7 * max(1.0, abs(fd)), (b, idx, g[b][idx], fd)
