@@ -242,6 +242,23 @@ EFUNC_API efunc_status efunc_mesh(efunc_t* h, int32_t N, const float* lo3, const
                                   int64_t max_verts, int64_t max_tris, int64_t* n_verts, int64_t* n_tris,
                                   void* stream);
 
+/* Cosine-series stacks (§4.4, Eq. cosine-series):
+ *   S(q) = sum_{b=0}^{B-1} w_b(q) O_b(q),  w_b(q) = cos(b pi x) cos(b pi y) cos(b pi z)
+ * (reading R-C: the 3-D cosine of "cos(b pi q)" is the separable product; B terms, so B = 1 is
+ * Table 3 Config G-6). The bands O_b are an n_shapes = B handle (variant GRID,
+ * degree 1) evaluated on the same queries:
+ *   efunc_cosine_replicate: qr[b][j][:] = q[j][:] (dev float[B*J*3]) for that handle;
+ *   efunc_cosine_combine: from the band values O dev [B][J] (and G dev [B][J][3] or NULL) the
+ *     stack value S dev [J], its gradient GS dev [J][3] (needs G) = sum_b (dw_b O_b + w_b G_b), and
+ *     with targets o dev [J]: the MSE loss of S (loss dev [1], needs S) and the band upstreams
+ *     dL_dO dev [B][J] = w_b(q_j) 2 (S_j - o_j) / J_global for efunc_backward (chain rule).
+ *   q dev [J*3]. J_global <= 0 means J. Any output may be NULL. Stream-ordered; no handle.
+ *   Errors: EINVAL (B < 1, J < 0, NULL q/O, GS without G, dL_dO/loss without o, loss without S). */
+EFUNC_API efunc_status efunc_cosine_replicate(const float* q, int64_t J, int32_t B, float* qr, void* stream);
+EFUNC_API efunc_status efunc_cosine_combine(const float* q, int64_t J, int32_t B, const float* O, const float* G,
+                                            const float* o, int64_t J_global, float* S, float* GS, float* dL_dO,
+                                            float* loss, void* stream);
+
 /* Parameter / optimizer-state access. on_device=1: ptr is a device pointer, else host.
  * These synchronise the stream. set_params rebuilds keys and clears the saved state. */
 EFUNC_API efunc_status efunc_get_params(efunc_t* h, float* dst, int32_t on_device, void* stream);

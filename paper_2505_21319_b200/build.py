@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libefunc.so")
-SOURCES = ["efunc_api.cu", "k_bin.cu", "k_lists.cu", "k_forward.cu", "k_backward.cu", "k_fit.cu", "k_fit_eik.cu", "k_adamw.cu", "k_mesh.cu", "k_var.cu"]
+SOURCES = ["efunc_api.cu", "k_bin.cu", "k_lists.cu", "k_forward.cu", "k_backward.cu", "k_fit.cu", "k_fit_eik.cu", "k_adamw.cu", "k_mesh.cu", "k_var.cu", "k_cosine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -846,6 +846,29 @@ int32_t efunc_abi_version(void) { return EFUNC_ABI_VERSION; }
 
 int32_t efunc_channels(int32_t variant, int32_t degree) { return variant_channels(variant, degree, nullptr); }
 
+efunc_status efunc_cosine_replicate(const float* q, int64_t J, int32_t B, float* qr, void* stream) {
+  if (B < 1 || J < 0) return fail(nullptr, EFUNC_EINVAL, "cosine: B >= 1 and J >= 0 required");
+  if (J > 0 && (!q || !qr)) return fail(nullptr, EFUNC_EINVAL, "cosine: NULL q or qr");
+  if (J == 0) return EFUNC_OK;
+  launch_cos_replicate(q, J, B, qr, (cudaStream_t)stream);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EFUNC_OK : fail(nullptr, EFUNC_ECUDA, cudaGetErrorString(e));
+}
+
+efunc_status efunc_cosine_combine(const float* q, int64_t J, int32_t B, const float* O, const float* G, const float* o,
+                                  int64_t J_global, float* S, float* GS, float* dL_dO, float* loss, void* stream) {
+  if (B < 1 || J < 0) return fail(nullptr, EFUNC_EINVAL, "cosine: B >= 1 and J >= 0 required");
+  if (J > 0 && (!q || !O)) return fail(nullptr, EFUNC_EINVAL, "cosine: NULL q or O");
+  if (GS && !G) return fail(nullptr, EFUNC_EINVAL, "cosine: GS needs the band gradients G");
+  if ((dL_dO || loss) && !o) return fail(nullptr, EFUNC_EINVAL, "cosine: the loss needs targets o");
+  if (loss && !S) return fail(nullptr, EFUNC_EINVAL, "cosine: the loss needs S");
+  if (J == 0) return EFUNC_OK;
+  const float inv_J = (float)(1.0 / (double)(J_global > 0 ? J_global : J));
+  launch_cos_combine(q, J, B, O, G, o, inv_J, S, GS, dL_dO, loss, (cudaStream_t)stream);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EFUNC_OK : fail(nullptr, EFUNC_ECUDA, cudaGetErrorString(e));
+}
+
 const char* efunc_last_error(const efunc_t* h) {
   if (h && !h->err.empty()) return h->err.c_str();
   return g_err.c_str();

@@ -266,6 +266,10 @@ int launch_var_forward(const FwdArgs& a, const float4* keyH, const uint32_t* iot
 int launch_var_backward(const FwdArgs& a, const float4* keyH, const uint32_t* iota, uint32_t iota_n,
                         const float* dL_dO, float* g13, float* gH, int64_t n_items, cudaStream_t s);
 int launch_item_lists(const FwdArgs& a, int64_t n_items, cudaStream_t s);
+// NEXT-4 cosine-series stacks (k_cosine.cu)
+int launch_cos_replicate(const float* q, int64_t J, int B, float* qr, cudaStream_t s);
+int launch_cos_combine(const float* q, int64_t J, int B, const float* O, const float* G, const float* o, float inv_J,
+                       float* S, float* GS, float* dL_dO, float* loss, cudaStream_t s);
 // NEXT-3 (k_mesh.cu): lattice queries, Marching Cubes, vertex normals
 cudaError_t mc_upload_table();
 int launch_lattice_q(int N, const float* lo, const float* step, int k0, int nk, float* q, cudaStream_t s);

@@ -28,7 +28,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
             "efunc_eval_grad", "efunc_fit_step", "efunc_mean_shift_init", "efunc_get_params",
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
             "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_sync", "efunc_last_error",
-            "efunc_mesh", "efunc_channels",
+            "efunc_mesh", "efunc_channels", "efunc_cosine_replicate", "efunc_cosine_combine",
             "efunc_abi_version"]
 
 
@@ -94,6 +94,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_set_timing": [P, i32],
         "efunc_get_kernel_ms": [P, P, i32],
         "efunc_mesh": [P, i32, P, P, f32, P, P, P, P, i64, i64, C.POINTER(i64), C.POINTER(i64), P],
+        "efunc_cosine_replicate": [P, i64, i32, P, P],
+        "efunc_cosine_combine": [P, i64, i32, P, P, P, i64, P, P, P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -405,3 +407,50 @@ class EFunc:
 
     def check(self):
         self._ok(self.lib.efunc_check(self.h, self._stream()))
+
+
+class CosineStack:
+    """Cosine-series stack (§4.4, Eq. cosine-series): S(q) = sum_{b<B} w_b(q) O_b(q),
+    w_b(q) = cos(b pi x) cos(b pi y) cos(b pi z) (reading R-C), the B bands Config G-6 models
+    (variant GRID, degree 1) of one n_shapes = B handle. theta: [B, R^3, 5]."""
+
+    def __init__(self, R: int = 16, B: int = 4, theta=None, cutoff_T: float = 20.0, device: int = 0):
+        self.B = int(B)
+        self.bands = EFunc(R, theta, cutoff_T=cutoff_T, device=device, n_shapes=self.B, degree=1,
+                           variant=VARIANT_GRID)
+        self.lib = self.bands.lib
+        self.device = self.bands.device
+
+    def _rep(self, q):
+        J = q.numel() // 3
+        _check_dev(q, "q", 3 * J, self.device)
+        qr = self.bands._empty(J, 3)
+        self.bands._ok(self.lib.efunc_cosine_replicate(_ptr(q), J, self.B, _ptr(qr), self.bands._stream()))
+        return J, qr
+
+    def forward(self, q, o=None, want_G: bool = False, J_global: int = 0):
+        """Returns (S [J], GS [J,3] or None, loss or None); with targets o the band upstreams of the
+        MSE loss are kept for backward()."""
+        J, qr = self._rep(q)
+        O, G, _ = self.bands.forward(qr, want_G=want_G, want_loss=False)
+        torch = self.bands._torch
+        S = torch.empty(J, device=q.device)
+        GS = torch.empty(J, 3, device=q.device) if want_G else None
+        up = L = None
+        if o is not None:
+            _check_dev(o, "o", J, self.device)
+            up = torch.empty(self.B, J, device=q.device)
+            L = torch.empty(1, device=q.device)
+        self.bands._ok(self.lib.efunc_cosine_combine(_ptr(q), J, self.B, _ptr(O), _ptr(G), _ptr(o), int(J_global),
+                                                     _ptr(S), _ptr(GS), _ptr(up), _ptr(L), self.bands._stream()))
+        self._up = up
+        return S, GS, L
+
+    def backward(self, grad=None):
+        """dL/dtheta of every band [B, R^3, 5] (+= into grad) from the last forward's MSE upstreams."""
+        if getattr(self, "_up", None) is None:
+            raise RuntimeError("backward() needs a forward() with targets")
+        return self.bands.backward(dL_dO=self._up, grad=grad)
+
+    def adamw_step(self, grad, hp: AdamW | None = None):
+        self.bands.adamw_step(grad, hp)
