@@ -453,10 +453,19 @@ def run_ours(args, rank, world, local_rank, nccl):
             m.backward(grad=g4)
         fb_ms = tms(fb)
         fused_ms = tms(lambda: m.forward_backward(q4, o4, loss=loss, grad=g4, want_loss=False))
+        # the paper's own setting: dense global sums (cutoff_T = inf), same theta and batch
+        md = ef.EFunc(R, m.get_params(), device=dev, cutoff_T=float("inf"))
+        gd = md._grad_zeros()
+        dense_ms = tms(lambda: md.forward_backward(q4, o4, loss=loss, grad=gd, want_loss=False), reps=10)
+        dense_ops = nq * R ** 3 * ((OPS_FWD + OPS_BWD_GRID) + (OPS_FWD + OPS_BWD_OFF))
+        del md
         t4 = {"paper": PAPER_T4, "ours_fwd_ms": fwd_ms, "ours_bwd_ms": fb_ms - fwd_ms,
               "ours_fused_fwd_bwd_ms": fused_ms, "ours_fused_points_per_s": nq / (fused_ms * 1e-3),
+              "ours_dense_fused_fwd_bwd_ms": dense_ms,
+              "ours_dense_frac_of_fp32_peak": dense_ops / (dense_ms * 1e-3) / (fp32_peak()[0] * 1e12),
               "note": "ours: certified cutoff T = 20 (reading R-1), this batch's loss, eager launches incl. "
-                      "binning; the paper: dense global sums on an unstated GPU"}
+                      "binning; ours_dense: every pair (cutoff_T = inf, k_dense_* kernels), frac on "
+                      "direct-form lane-ops of all pairs; the paper: dense global sums on an unstated GPU"}
 
     if rank != 0:
         return

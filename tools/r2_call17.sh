@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2c17_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2c17_smoke.log
+timeout 1800 python -m pytest tests -m gpu -q --timeout 600 -rA > gpurun_out/r2c17_pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/r2c17_pytest_gpu.log
+timeout 400 python bench.py > gpurun_out/r2c17_bench_c2.json 2> gpurun_out/r2c17_bench_c2.err
+tail -3 gpurun_out/r2c17_pytest_gpu.log; tail -2 gpurun_out/r2c17_smoke.log; python -c "
+import json; d=json.loads(open('gpurun_out/r2c17_bench_c2.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['roofline']['frac'], d['paper_table4'])"
