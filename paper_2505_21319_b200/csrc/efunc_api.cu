@@ -87,9 +87,26 @@ BrickGeom brick_geom(const efunc_config& cfg, int NC, float h) {
   g.bits = 0;
   while ((1 << g.bits) < g.nb) ++g.bits;
   g.n_codes = 1u << (3 * g.bits);
-  g.sub_bits = 0;
-  while ((1 << g.sub_bits) < 2 * g.B) ++g.sub_bits;
-  g.qsub = 1u << (3 * g.sub_bits);
+  // work items are balanced runs of the Morton-sorted queries of one brick: sorting them by
+  // quarter-cell (rather than half-cell) sub-bins makes the items' boxes tighter (fewer candidate
+  // keys) while the bin arrays stay small (<= 8M bins); EF_SUBDIV overrides for experiments
+  g.sdiv = 4;
+#ifdef EF_SUBDIV
+  g.sdiv = EF_SUBDIV;
+#endif
+  auto set_sub = [&]() {
+    g.sub_bits = 0;
+    while ((1 << g.sub_bits) < g.sdiv * g.B) ++g.sub_bits;
+    g.qsub = 1u << (3 * g.sub_bits);
+  };
+  set_sub();
+#ifndef EF_BIN_CAP
+#define EF_BIN_CAP (8u << 20)
+#endif
+  while ((uint64_t)g.n_codes * g.qsub > EF_BIN_CAP && g.sdiv > 2) {
+    g.sdiv /= 2;
+    set_sub();
+  }
   return g;
 }
 
@@ -329,19 +346,22 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   const int kind = loss ? loss->kind : EFUNC_LOSS_NONE;
   RET(ensure_queries(h, J));
   const uint32_t nb = h->bg.n_codes;             // bricks
-  const uint32_t nbins = nb * h->bg.qsub + 1;    // half-cell bins + the out-of-domain bin
+  const uint32_t nbins = nb * h->bg.qsub + 1;    // sub-cell bins + the out-of-domain bin
   CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
-  CK(cudaMemsetAsync(h->bin_fill, 0, sizeof(uint32_t) * (nbins + 1), s));
+  // fused path: each query's rank inside its bin comes from the histogram's atomic (no fill
+  // counters, no second atomic pass); the other paths sort stably instead
+  const bool ranked = with_mh && !h->cfg.deterministic;
   static_assert(offsetof(DevScalars, kept_pairs_offset) + sizeof(unsigned long long) == sizeof(DevScalars),
                 "the per-forward counters end DevScalars");
   CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(DevScalars) - offsetof(DevScalars, overflow_items), s));
-  h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count, h->ds, s);
+  h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count,
+                                   ranked ? h->q_tmp : nullptr, h->ds, s);
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
   if (with_mh && !h->cfg.deterministic) {
     // fused path: the atomic scatter order inside a bin is kept (only deterministic mode needs the
     // stable rank); the gather then runs in sorted order, so the shift bounds' key loads of
     // neighbouring threads hit the same cells
-    h->launches += launch_scatter_only(h->q_bin, (uint32_t)J, h->bin_start, h->bin_fill, h->q_order, s);
+    h->launches += launch_scatter_ranked(h->q_bin, h->q_tmp, (uint32_t)J, h->bin_start, h->q_order, s);
     h->launches += launch_gather_queries_mh(keys_view(h), h->q_order, q, o_used, J, h->qs, h->perm, h->qmh,
                                             with_mh == 2 ? h->qf0 : nullptr, s);
   } else {

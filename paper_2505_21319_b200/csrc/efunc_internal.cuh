@@ -186,8 +186,9 @@ struct BrickGeom {
   int nb;         // bricks per axis
   int bits;       // Morton bits per axis (2^bits >= nb)
   uint32_t n_codes;  // 2^(3 bits)
-  int sub_bits;   // query sub-bins per brick edge = 2^sub_bits = 2B (half-cells)
-  uint32_t qsub;  // query sub-bins per brick = (2B)^3, Morton ordered inside the brick
+  int sdiv;       // query sub-bins per lattice cell edge (2: half-cells, 4: quarter-cells)
+  int sub_bits;   // query sub-bins per brick edge = 2^sub_bits = sdiv B
+  uint32_t qsub;  // query sub-bins per brick = (sdiv B)^3, Morton ordered inside the brick
 };
 
 // Parameter layout of a Table 3 variant (k_var.cu; include/efunc.h efunc_channels): channel
@@ -217,8 +218,10 @@ int launch_brick_lists(const KeysView& kv, const BrickGeom& bg, float T_l, uint3
                        uint32_t pool_cap, uint32_t* off, uint32_t* n, DevScalars* ds, uint32_t* scratch,
                        cudaStream_t s);
 int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom& bg, int NC,
-                      float inv_h, uint32_t* bins, uint32_t* count, DevScalars* ds,
+                      float inv_h, uint32_t* bins, uint32_t* count, uint32_t* rank, DevScalars* ds,
                       cudaStream_t s);
+int launch_scatter_ranked(const uint32_t* bin, const uint32_t* rank, uint32_t n, const uint32_t* bin_start,
+                          uint32_t* out_idx, cudaStream_t s);
 int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
                           float4* qs, int* perm, cudaStream_t s);
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,

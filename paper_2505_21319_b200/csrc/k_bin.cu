@@ -353,10 +353,10 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every 3
 // non-finite) go to the last bin, whose items enumerate keys directly instead of a brick list.
 __global__ void k_query_bins(const float* __restrict__ q, const float* __restrict__ o, int64_t J, BrickGeom bg,
                              int NC, float inv_h, uint32_t* __restrict__ bins, uint32_t* __restrict__ count,
-                             DevScalars* ds) {
+                             uint32_t* __restrict__ rank, DevScalars* ds) {
   const uint32_t outside = bg.n_codes * bg.qsub;
-  const float sub_scale = 2.0f * inv_h;  // half-cells
-  const int ns = 2 * bg.B;
+  const float sub_scale = (float)bg.sdiv * inv_h;  // sub-cells (half or quarter cells)
+  const int ns = bg.sdiv * bg.B;
   bool bad = false;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
     const float x = q[3 * j], y = q[3 * j + 1], z = q[3 * j + 2];
@@ -368,7 +368,7 @@ __global__ void k_query_bins(const float* __restrict__ q, const float* __restric
       const int bx = cell_clamp(x, inv_h, NC) / bg.B;
       const int by = cell_clamp(y, inv_h, NC) / bg.B;
       const int bz = cell_clamp(z, inv_h, NC) / bg.B;
-      // half-cell of the query inside its brick (Morton order): a brick's sub-bins stay contiguous
+      // sub-cell of the query inside its brick (Morton order): a brick's sub-bins stay contiguous
       const int sx = min(max((int)floorf((x + 1.0f) * sub_scale) - ns * bx, 0), ns - 1);
       const int sy = min(max((int)floorf((y + 1.0f) * sub_scale) - ns * by, 0), ns - 1);
       const int sz = min(max((int)floorf((z + 1.0f) * sub_scale) - ns * bz, 0), ns - 1);
@@ -376,15 +376,29 @@ __global__ void k_query_bins(const float* __restrict__ q, const float* __restric
           (spread3(sx) | (spread3(sy) << 1) | (spread3(sz) << 2));
     }
     bins[j] = b;
-    atomicAdd(&count[b], 1u);
+    const uint32_t r = atomicAdd(&count[b], 1u);
+    if (rank) rank[j] = r;  // position inside the bin (any order is valid outside deterministic mode)
   }
   if (__any_sync(~0u, bad) && (threadIdx.x & 31) == 0) atomicOr(&ds->nonfinite, 1u);
 }
 
 int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom& bg, int NC, float inv_h,
-                      uint32_t* bins, uint32_t* count, DevScalars* ds, cudaStream_t s) {
+                      uint32_t* bins, uint32_t* count, uint32_t* rank, DevScalars* ds, cudaStream_t s) {
   if (J == 0) return 0;
-  k_query_bins<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(q, o, J, bg, NC, inv_h, bins, count, ds);
+  k_query_bins<<<grid_for((uint32_t)J, 256), 256, 0, s>>>(q, o, J, bg, NC, inv_h, bins, count, rank, ds);
+  return 1;
+}
+
+__global__ void k_scatter_ranked(const uint32_t* __restrict__ bin, const uint32_t* __restrict__ rank, uint32_t n,
+                                 const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ out_idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out_idx[bin_start[bin[i]] + rank[i]] = i;
+}
+
+int launch_scatter_ranked(const uint32_t* bin, const uint32_t* rank, uint32_t n, const uint32_t* bin_start,
+                          uint32_t* out_idx, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_scatter_ranked<<<grid_for(n, 256), 256, 0, s>>>(bin, rank, n, bin_start, out_idx);
   return 1;
 }
 

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_configs.py -q -x --timeout 600 > gpurun_out/r2c19_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r2c19_pytest.log
+bash tools/variants.sh --no-cpu-baseline --no-e2e > gpurun_out/r2c19_variants.txt 2>&1
+bash tools/variants.sh --config c3 --no-cpu-baseline --no-e2e >> gpurun_out/r2c19_variants.txt 2>&1
+bash tools/variants.sh --config c5 --no-cpu-baseline --no-e2e >> gpurun_out/r2c19_variants.txt 2>&1
+tail -2 gpurun_out/r2c19_pytest.log; cat gpurun_out/r2c19_variants.txt
