@@ -47,7 +47,10 @@ namespace ef {
 constexpr int FT_WARPS = 4;
 constexpr int FT_BLOCKS = 148 * (FT_MIN_WARPS / FT_WARPS);
 static_assert(FT_BLOCKS * FT_WARPS <= SCRATCH_WARPS, "one scratch slot per warp");
-constexpr float FT_ZMIN = 7.8886e-31f;  // 2^-100: smaller Z_j -> exact-shift split path
+// 2^-97: smaller Z_j (m_j > 97 log2 units) -> the exact-shift split path. The unshifted weights
+// 2^-a_ij then stay normal floats (>= 2^-126, ex2.approx.ftz flushes below) for every pair within
+// the certified cutoff a_ij - m_j <= T = 20 nats = 28.85 log2 units (reading R-1)
+constexpr float FT_ZMIN = 6.3109e-30f;
 
 struct FitSmem {
   float4 qa[QW / 2], qb[QW / 2];              // {x'0,x'1,y'0,y'1}, {z'0,z'1,qq0,qq1}
@@ -110,6 +113,14 @@ __device__ __forceinline__ void bwd_mse_out(const FitArgs& F, const MseSums& s, 
   }
 }
 
+// Dense kernels: the origin's w is the item's exponent shift max_j mh_j (log2 units), so the
+// weights are 2^(shift - a_ij): Z_j >= 1 and no pair is flushed to zero however large m_j is.
+__device__ __forceinline__ KeyX key_x(const float4 a, const float4 b, const float4 o) {
+  KeyX k = key_x(a, b, make_float3(o.x, o.y, o.z));
+  k.C += o.w;
+  return k;
+}
+
 // exponent (log2 units, <= 0) and polynomial value of one key at a packed query pair
 #define FX_EF(K, QA, QB, e, f)                                                   \
   float2 e = __ffma2_rn(make_float2(K.nbl, K.nbl), make_float2(QB.z, QB.w), make_float2(K.C, K.C)); \
@@ -123,9 +134,9 @@ __device__ __forceinline__ void bwd_mse_out(const FitArgs& F, const MseSums& s, 
 // Forward sums, lanes = keys: one round = 32 candidate keys (records one round ahead, ids two),
 // every lane walks the item's query pairs; Z, M per query pair in registers; one transpose-
 // reduction per item returns Z_j, M_j to lane j. NPM = query pairs held (8: <= 16 queries).
-template <int NPM>
+template <int NPM, class OT>
 __device__ __forceinline__ void fwd_accum_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
-                                            const int nact, const float3 o, const float4* sQA,
+                                            const int nact, const OT o, const float4* sQA,
                                             const float4* sQB, float2 (&Z)[NPM], float2 (&M)[NPM]) {
   const int lane = threadIdx.x & 31;
   const int npairs = (nact + 1) >> 1;
@@ -201,9 +212,9 @@ __device__ __forceinline__ void fwd_reduce_x(const float2 (&Z)[NPM], const float
   }
 }
 
-template <int NPM>
+template <int NPM, class OT>
 __device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L, const uint32_t wn,
-                                           const int nact, const float3 o, const float4* sQA,
+                                           const int nact, const OT o, const float4* sQA,
                                            const float4* sQB, float& Zj, float& Mj) {
   float2 Z[NPM], M[NPM];
 #pragma unroll
@@ -211,7 +222,7 @@ __device__ __forceinline__ void fwd_sums_x(const KeysView& kv, const uint32_t* L
     Z[pp] = make_float2(0.f, 0.f);
     M[pp] = make_float2(0.f, 0.f);
   }
-  fwd_accum_x<NPM>(kv, L, wn, nact, o, sQA, sQB, Z, M);
+  fwd_accum_x<NPM, OT>(kv, L, wn, nact, o, sQA, sQB, Z, M);
   fwd_reduce_x<NPM>(Z, M, Zj, Mj);
 }
 
@@ -753,6 +764,9 @@ __global__ void __launch_bounds__(32 * FL_WARPS, 3) k_fit_lists(const FitArgs F)
 //                    (PAPER.md:L540-568): two keys per lane accumulate over every query of the
 //                    group in registers (direct form, d = q - k), two red.v4 per key and group.
 constexpr int DN_WARPS = 4;
+// item box diagonal^2 above which the dense forward uses the direct form: the expansion about the
+// box centre rounds the exponent by ~eps bl D^2 (2e-5 log2 units at D = 0.6, beta = e^7)
+constexpr float DN_LOCAL2 = 0.36f;
 
 __global__ void __launch_bounds__(32 * DN_WARPS) k_dense_fwd(const FitArgs F, float2* __restrict__ zm, int S,
                                                              uint32_t ks) {
@@ -768,8 +782,31 @@ __global__ void __launch_bounds__(32 * DN_WARPS) k_dense_fwd(const FitArgs F, fl
   const bool act = lane < nact;
   const int64_t js = (int64_t)it.x + lane;
   const float4 q = act ? A.qs[js] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const Box box = warp_box(act, q.x, q.y, q.z, 0.0f);
-  const float3 o = make_float3(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz));
+  const float mh = act ? A.qmh[js] : -INFINITY;
+  const Box box = warp_box(act, q.x, q.y, q.z, mh);
+  const float4 o = make_float4(0.5f * (box.lx + box.hx), 0.5f * (box.ly + box.hy), 0.5f * (box.lz + box.hz), box.thr);
+  const uint32_t k0 = sl * ks;
+  const uint32_t wn = k0 < F.iota_n ? min(ks, F.iota_n - k0) : 0u;
+  float Z, M;
+  const float ex = box.hx - box.lx, ey = box.hy - box.ly, ez = box.hz - box.lz;
+  if (fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > DN_LOCAL2) {
+    // a spread item (small J: a Morton run of the whole domain): the expansion about its centre
+    // would round the exponent by ~eps bl |q - o|^2, so the direct form d = q - k (k_pair.cuh)
+    {
+      const float xo = __shfl_xor_sync(~0u, q.x, 1), yo = __shfl_xor_sync(~0u, q.y, 1);
+      const float zo = __shfl_xor_sync(~0u, q.z, 1);
+      const float sh = act ? o.w : -INFINITY, so = __shfl_xor_sync(~0u, sh, 1);
+      if ((lane & 1) == 0) {
+        Sm.qa[lane >> 1] = make_float4(q.x, xo, q.y, yo);
+        Sm.qb[lane >> 1] = make_float4(q.z, zo, sh, so);
+      }
+    }
+    __syncwarp();
+    if (nact <= 16) fwd_keys_sums<8>(A.kv, F.iota + k0, wn, nact, Sm.qa, Sm.qb, Z, M);
+    else fwd_keys_sums<16>(A.kv, F.iota + k0, wn, nact, Sm.qa, Sm.qb, Z, M);
+    zm[(size_t)u * 32 + lane] = make_float2(Z, M);
+    return;
+  }
   const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
   const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;
   {
@@ -781,9 +818,6 @@ __global__ void __launch_bounds__(32 * DN_WARPS) k_dense_fwd(const FitArgs F, fl
     }
   }
   __syncwarp();
-  const uint32_t k0 = sl * ks;
-  const uint32_t wn = k0 < F.iota_n ? min(ks, F.iota_n - k0) : 0u;
-  float Z, M;
   if (nact <= 16) fwd_sums_x<8>(A.kv, F.iota + k0, wn, nact, o, Sm.qa, Sm.qb, Z, M);
   else fwd_sums_x<16>(A.kv, F.iota + k0, wn, nact, o, Sm.qa, Sm.qb, Z, M);
   zm[(size_t)u * 32 + lane] = make_float2(Z, M);
@@ -806,7 +840,13 @@ __global__ void k_dense_combine(const FitArgs F, const float2* __restrict__ zm, 
   }
   const float4 q = act ? A.qs[js] : make_float4(1e6f, 1e6f, 1e6f, 0.f);
   const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
-  const bool slow = __any_sync(~0u, bad);  // Z underflow: the split kernels shift exactly
+  // Z underflow or out-of-domain queries (their item box is not local): the split kernels shift
+  // exactly in the direct form
+  const bool slow = __any_sync(~0u, bad) || it.z < 0;
+  // the item's exponent shift (k_dense_fwd: max_j mh_j), for the backward's weights
+  const float mh = act ? A.qmh[js] : -INFINITY;
+  float shift = mh;
+  for (int s2 = 16; s2 > 0; s2 >>= 1) shift = fmaxf(shift, __shfl_xor_sync(~0u, shift, s2));
   float O = 0.f, rho = 0.f, lossj = 0.f;
   if (act && !slow) {
     const float iz = 1.0f / Z;
@@ -822,7 +862,7 @@ __global__ void k_dense_combine(const FitArgs F, const float2* __restrict__ zm, 
     else A.loss_part[item] = lossj;
     atomicAdd(&A.ds->cand_pairs, (unsigned long long)F.iota_n * (unsigned long long)nact);
   }
-  // packed query pairs for the backward: {x0,x1,y0,y1}, {z0,z1,rho0,rho1}, {-O0,-O1,0,0}; an idle
+  // packed query pairs for the backward: {x0,x1,y0,y1}, {z0,z1,rho0,rho1}, {-O0,-O1,s,s}; an idle
   // (or slow-path) slot is far away with rho = 0: it contributes exactly 0
   const float x = (act && !slow) ? q.x : 1e6f, y = (act && !slow) ? q.y : 1e6f, z = (act && !slow) ? q.z : 1e6f;
   const float xo = __shfl_xor_sync(~0u, x, 1), yo = __shfl_xor_sync(~0u, y, 1), zo = __shfl_xor_sync(~0u, z, 1);
@@ -831,7 +871,7 @@ __global__ void k_dense_combine(const FitArgs F, const float2* __restrict__ zm, 
     float4* d = dq + (size_t)item * 48;
     d[lane >> 1] = make_float4(x, xo, y, yo);
     d[16 + (lane >> 1)] = make_float4(z, zo, rho, ro);
-    d[32 + (lane >> 1)] = make_float4(-O, -Oo, 0.f, 0.f);
+    d[32 + (lane >> 1)] = make_float4(-O, -Oo, shift, shift);
   }
 }
 
@@ -858,7 +898,7 @@ __device__ __forceinline__ void dense_bwd_unit(const FitArgs& F, const float4* _
     float2 dd = __fmul2_rn(dz, dz);
     dd = __ffma2_rn(dy, dy, dd);
     dd = __ffma2_rn(dx, dx, dd);
-    const float2 e = __fmul2_rn(make_float2(-a.w, -a.w), dd);
+    const float2 e = __ffma2_rn(make_float2(-a.w, -a.w), dd, make_float2(QC.z, QC.w));  // shift - a
     const float2 t = __fmul2_rn(make_float2(QB.z, QB.w), make_float2(ex2f(e.x), ex2f(e.y)));
     float2 f = __ffma2_rn(make_float2(b.y, b.y), dx, make_float2(b.x, b.x));
     f = __ffma2_rn(make_float2(b.z, b.z), dy, f);
