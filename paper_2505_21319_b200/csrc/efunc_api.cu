@@ -609,7 +609,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   const bool dense = std::isinf(cutoff_log2(h->cfg));
   // deterministic mode: the fused MSE kernel with 64-bit fixed-point sums (cutoff mode); otherwise split
   const int det = h->cfg.deterministic;
-  const int fused = !h->count_kept && !(eik && dense) && !(det && (eik || dense));
+  const int fused = !h->count_kept && !(det && (eik || dense));
   if (!fused || J == 0) {
     RET(do_forward(h, q, o, J, loss, O, nullptr, loss_out, 1, s));
     RET(do_backward(h, nullptr, nullptr, grad, s));
@@ -642,22 +642,30 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   // MSE, cutoff mode: the items' candidate lists are built first by k_fit_lists (latency-bound list
   // stream at full occupancy), then k_fit computes; the timed "dominant kernel" spans both
   f.pre = (!eik && !dense && !det && !fit_pre_off()) ? 1 : 0;
-  if (dense && !eik) {  // NEXT-2: key-sliced dense kernels (all warp slots busy at small J)
-    const int64_t nz = dense_zm_elems(h->fwd_items_bound, h->iota_n);
-    if (nz > h->dn_zm_cap) {
+  if (dense) {  // NEXT-2: key-sliced dense kernels (all warp slots busy at small J)
+    const int64_t nz = eik ? dense_eik_part_elems(h->fwd_items_bound, h->iota_n)
+                           : dense_zm_elems(h->fwd_items_bound, h->iota_n);
+    // dn_zm holds float2 (MSE: Z, M per query and slice) or the Eikonal path's 11 floats per query
+    // and slice (half as many float2); dn_dq a packed query table per item (48 / 80 float4)
+    const int64_t nz2 = eik ? (nz + 1) / 2 : nz;
+    if (nz2 > h->dn_zm_cap) {
       drop_fit_graph(h);
       dfree(h->dn_zm);
-      CK(dalloc(&h->dn_zm, (size_t)nz));
-      h->dn_zm_cap = nz;
+      CK(dalloc(&h->dn_zm, (size_t)nz2));
+      h->dn_zm_cap = nz2;
     }
-    if (h->fwd_items_bound * 48 > h->dn_dq_cap) {
+    const int64_t ndq = h->fwd_items_bound * (eik ? 80 : 48);
+    if (ndq > h->dn_dq_cap) {
       drop_fit_graph(h);
       dfree(h->dn_dq);
-      CK(dalloc(&h->dn_dq, (size_t)h->fwd_items_bound * 48));
-      h->dn_dq_cap = h->fwd_items_bound * 48;
+      CK(dalloc(&h->dn_dq, (size_t)ndq));
+      h->dn_dq_cap = ndq;
     }
     const int slot = timing_begin(h, s);
-    h->launches += launch_dense_fit(f, h->fwd_items_bound, h->dn_zm, h->dn_dq, s, nullptr);
+    if (eik)
+      h->launches += launch_dense_fit_eik(f, h->fwd_items_bound, reinterpret_cast<float*>(h->dn_zm), h->dn_dq, s);
+    else
+      h->launches += launch_dense_fit(f, h->fwd_items_bound, h->dn_zm, h->dn_dq, s, nullptr);
     timing_end(h, slot, s);
   } else {
     const int slot = timing_begin(h, s);

@@ -241,6 +241,9 @@ int launch_det_bound(const float* theta, int n_nodes, const float4* qs, int64_t 
 int launch_backward_list_det(const BwdArgs& a, cudaStream_t s);
 // dense mode (cutoff_T = inf, MSE): key-sliced forward, combine, key-stationary backward (k_fit.cu)
 int64_t dense_zm_elems(int64_t n_items, uint32_t iota_n);
+void dense_split_dims(int64_t n_items, uint32_t iota_n, int& S, uint32_t& ks, int& G);
+int64_t dense_eik_part_elems(int64_t n_items, uint32_t iota_n);
+int launch_dense_fit_eik(const FitArgs& a, int64_t n_items, float* part, float4* dq, cudaStream_t s);
 int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, cudaStream_t s, int* fwd_launches);
 int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);

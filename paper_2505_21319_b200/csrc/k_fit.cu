@@ -860,7 +860,8 @@ __global__ void k_dense_combine(const FitArgs F, const float2* __restrict__ zm, 
   if (lane == 0) {
     if (slow) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
     else A.loss_part[item] = lossj;
-    atomicAdd(&A.ds->cand_pairs, (unsigned long long)F.iota_n * (unsigned long long)nact);
+    if (!slow)  // the split kernels count the slow items' pairs
+      atomicAdd(&A.ds->cand_pairs, (unsigned long long)F.iota_n * (unsigned long long)nact);
   }
   // packed query pairs for the backward: {x0,x1,y0,y1}, {z0,z1,rho0,rho1}, {-O0,-O1,s,s}; an idle
   // (or slow-path) slot is far away with rho = 0: it contributes exactly 0
@@ -958,7 +959,7 @@ __global__ void __launch_bounds__(32 * DN_WARPS) k_dense_bwd(const FitArgs F, co
 }
 
 // work split of the three dense kernels for n_items items (a launch bound) and iota_n keys
-static void dense_split(int64_t n_items, uint32_t iota_n, int& S, uint32_t& ks, int& G) {
+void dense_split_dims(int64_t n_items, uint32_t iota_n, int& S, uint32_t& ks, int& G) {
   const int64_t target = 148 * 16 * 4;  // units: ~4 per warp slot
   S = (int)std::max<int64_t>(1, std::min<int64_t>((target + n_items - 1) / std::max<int64_t>(n_items, 1),
                                                     (iota_n + 255) / 256));
@@ -970,7 +971,7 @@ static void dense_split(int64_t n_items, uint32_t iota_n, int& S, uint32_t& ks, 
 int64_t dense_zm_elems(int64_t n_items, uint32_t iota_n) {
   int S, G;
   uint32_t ks;
-  dense_split(n_items, iota_n, S, ks, G);
+  dense_split_dims(n_items, iota_n, S, ks, G);
   return n_items * S * 32;
 }
 
@@ -978,7 +979,7 @@ int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, 
   if (n_items <= 0) return 0;
   int S, G;
   uint32_t ks;
-  dense_split(n_items, a.iota_n, S, ks, G);
+  dense_split_dims(n_items, a.iota_n, S, ks, G);
   const int64_t ufwd = n_items * S;
   k_dense_fwd<<<(unsigned)((ufwd + DN_WARPS - 1) / DN_WARPS), 32 * DN_WARPS, 0, s>>>(a, zm, S, ks);
   k_dense_combine<<<(unsigned)((n_items + 3) / 4), 128, 0, s>>>(a, zm, S, dq);

@@ -353,6 +353,210 @@ __global__ void __launch_bounds__(32 * FE_WARPS, FE_MIN_WARPS / FE_WARPS) k_fit_
   }
 }
 
+// ------------------------------------------------------------------ dense mode (cutoff_T = inf)
+// The MSE + Eikonal loss with every (query, key) pair, split like the MSE
+// dense path (k_fit.cu) so that small batches fill the GPU:
+//   k_dense_eik_fwd      (item, key slice) units, lanes = queries: the slice's 11 partial sums of
+//                        eik_fwd_round (Z, M, S_g, S_u, S_uf; each query's own shift mh_j and f0);
+//   k_dense_eik_combine  per item: the sums over the slices in slice order, then O, G, u, both
+//                        losses and upstreams (the epilogue of eik_item) -> the item's packed table;
+//   k_dense_eik_bwd      (64-key block, item group) units, key-stationary: two keys per lane
+//                        accumulate the second-order sums over every query of the group.
+constexpr int DE_WARPS = 4;
+constexpr int DE_NSUM = 11;
+
+__global__ void __launch_bounds__(32 * DE_WARPS) k_dense_eik_fwd(const FitArgs F, float* __restrict__ part, int S,
+                                                                uint32_t ks) {
+  __shared__ EikSmem smem[DE_WARPS];
+  EikSmem& Sm = smem[threadIdx.x >> 5];
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const uint32_t u = blockIdx.x * DE_WARPS + (threadIdx.x >> 5);
+  const uint32_t item = u / (uint32_t)S, sl = u % (uint32_t)S;
+  if (item >= *A.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const bool act = lane < it.y;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = INFINITY, f0 = 0.f;
+  if (act) {
+    q = A.qs[js];
+    mh = A.qmh[js];
+    f0 = A.qf0[js];
+  }
+  const uint32_t k0 = sl * ks;
+  const uint32_t wn = k0 < F.iota_n ? min(ks, F.iota_n - k0) : 0u;
+  EikFwd fa;
+  fa.Z = fa.M = fa.sgx = fa.sgy = fa.sgz = fa.sux = fa.suy = fa.suz = fa.sfx = fa.sfy = fa.sfz = make_float2(0.f, 0.f);
+  const float sh = act ? mh : -INFINITY;
+  const float2 qx = make_float2(q.x, q.x), qy = make_float2(q.y, q.y), qz = make_float2(q.z, q.z);
+  const float2 sh2 = make_float2(sh, sh), nf0 = make_float2(-f0, -f0);
+  const int hi = lane & 1, slot = lane >> 1;
+  for (uint32_t base = 0; base < wn; base += 32) {
+    const uint32_t k = base + lane;
+    float4 a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < wn) ld_rec(&kv.grid_raw[2 * F.iota[k0 + k]], a, b);
+    __syncwarp();
+    Sm.kA[slot][hi] = a.x; Sm.kA[slot][2 + hi] = a.y;
+    Sm.kB[slot][hi] = a.z; Sm.kB[slot][2 + hi] = a.w;
+    Sm.kC[slot][hi] = b.x; Sm.kC[slot][2 + hi] = b.y;
+    Sm.kD[slot][hi] = b.z; Sm.kD[slot][2 + hi] = b.w;
+    __syncwarp();
+    const int npk = ((int)min(wn - base, 32u) + 1) >> 1;
+    eik_fwd_round(Sm, npk, qx, qy, qz, sh2, nf0, fa);
+  }
+  float* d = part + (size_t)u * DE_NSUM * 32 + lane;
+  d[0] = hsum(fa.Z); d[32] = hsum(fa.M);
+  d[64] = hsum(fa.sgx); d[96] = hsum(fa.sgy); d[128] = hsum(fa.sgz);
+  d[160] = hsum(fa.sux); d[192] = hsum(fa.suy); d[224] = hsum(fa.suz);
+  d[256] = hsum(fa.sfx); d[288] = hsum(fa.sfy); d[320] = hsum(fa.sfz);
+}
+
+__global__ void k_dense_eik_combine(const FitArgs F, const float* __restrict__ part, int S, float4* __restrict__ dq) {
+  const FwdArgs& A = F.f;
+  const uint32_t item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= *A.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const int4 it = A.items[item];
+  const bool act = lane < it.y;
+  const int64_t js = (int64_t)it.x + lane;
+  float v[DE_NSUM];
+#pragma unroll
+  for (int c = 0; c < DE_NSUM; ++c) v[c] = 0.f;
+  for (int s = 0; s < S; ++s) {  // slice order: the sums do not depend on the schedule
+    const float* p = part + ((size_t)item * S + s) * DE_NSUM * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < DE_NSUM; ++c) v[c] += p[32 * c];
+  }
+  const float Z = v[0], M = v[1];
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mh = 0.f, f0 = 0.f;
+  if (act) {
+    q = A.qs[js];
+    mh = A.qmh[js];
+    f0 = A.qf0[js];
+  }
+  const bool bad = act && !(isfinite(Z) && isfinite(M) && Z > 0.0f);
+  const bool slow = __any_sync(~0u, bad) || it.z < 0;  // the split kernels (exact shift, direct form)
+  float lossj = 0.f, rh = 0.f, Oj = 0.f, hx = 0.f, hy = 0.f, hz = 0.f, Tj = 0.f, nlam = -INFINITY;
+  if (act && !slow) {  // the epilogue of eik_item (Eq. func-normal; Eq. loss; reading R-12)
+    const float iz = 1.0f / Z;
+    Oj = f0 + M * iz;
+    nlam = mh - log2f(Z);
+    const float c2 = 2.0f * EF_LN2 * iz;
+    const float Of = M * iz;
+    const float Gx = fmaf(v[2], iz, c2 * fmaf(Of, v[5], -v[8]));
+    const float Gy = fmaf(v[3], iz, c2 * fmaf(Of, v[6], -v[9]));
+    const float Gz = fmaf(v[4], iz, c2 * fmaf(Of, v[7], -v[10]));
+    const float ux = c2 * v[5], uy = c2 * v[6], uz = c2 * v[7];
+    const float diff = Oj - q.w;
+    const float r = 2.0f * diff * A.inv_J;
+    lossj = diff * diff * A.inv_J;
+    const float nrm = sqrtf(fmaf(Gx, Gx, fmaf(Gy, Gy, Gz * Gz)));
+    lossj = fmaf(A.eik_lambda * (nrm - 1.0f) * (nrm - 1.0f), A.inv_J, lossj);
+    const float sc = nrm > 0.0f ? 2.0f * A.eik_lambda * (nrm - 1.0f) / nrm * A.inv_J : 0.0f;
+    hx = sc * Gx; hy = sc * Gy; hz = sc * Gz;
+    rh = r + (hx * ux + hy * uy + hz * uz);
+    Tj = hx * Gx + hy * Gy + hz * Gz;
+    const int ju = A.perm[js];
+    if (A.O) A.O[ju] = Oj;
+    if (A.G) {
+      A.G[3 * (size_t)ju] = Gx;
+      A.G[3 * (size_t)ju + 1] = Gy;
+      A.G[3 * (size_t)ju + 2] = Gz;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) lossj += __shfl_xor_sync(~0u, lossj, o);
+  if (lane == 0) {
+    if (slow) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    else A.loss_part[item] = lossj;
+    if (!slow)  // the split kernels count the slow items' pairs
+      atomicAdd(&A.ds->cand_pairs, (unsigned long long)F.iota_n * (unsigned long long)it.y);
+  }
+  // the item's table as packed pairs {x,y}, {z,w}, {r + h.u, O}, {hx, hy}, {hz, T}; an idle (or
+  // slow-path) slot has w = -inf and zero upstreams: it contributes exactly 0
+  float4* d = dq + (size_t)item * 80;
+  const float vals[10] = {q.x, q.y, q.z, nlam, rh, Oj, hx, hy, hz, Tj};
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const float a0 = vals[2 * c], a1 = vals[2 * c + 1];
+    const float o0 = __shfl_xor_sync(~0u, a0, 1), o1 = __shfl_xor_sync(~0u, a1, 1);
+    if ((lane & 1) == 0) d[16 * c + (lane >> 1)] = make_float4(a0, o0, a1, o1);
+  }
+}
+
+template <bool OFF>
+__device__ __forceinline__ void dense_eik_unit(const FitArgs& F, const float4* __restrict__ dq, EikSmem& S,
+                                               uint32_t kb, uint32_t i0, uint32_t i1) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31;
+  const uint32_t kA = kb * 64u + lane, kB = kA + 32u;
+  const bool hA = kA < F.iota_n, hB = kB < F.iota_n;
+  const uint32_t idA = hA ? F.iota[kA] : 0u, idB = hB ? F.iota[kB] : 0u;
+  float4 aA = make_float4(1e18f, 1e18f, 1e18f, 1.0f), bA = make_float4(0.f, 0.f, 0.f, 0.f), aB = aA, bB = bA;
+  if (hA) ld_rec(&kv.grid_raw[2 * idA], aA, bA);
+  if (hB) ld_rec(&kv.grid_raw[2 * idB], aB, bB);
+  const float beta2A = 2.0f * aA.w * EF_LN2, beta2B = 2.0f * aB.w * EF_LN2;
+  EikBwd s0, s1;
+  s0.sc = s0.sgx = s0.sgy = s0.sgz = s0.phx = s0.phy = s0.phz = s0.ss = s0.sdx = s0.sdy = s0.sdz = s0.pdx =
+      s0.pdy = s0.pdz = make_float2(0.f, 0.f);
+  s1 = s0;
+  float4* const tab = reinterpret_cast<float4*>(S.pA);  // pA..pE are contiguous: 5 x 16 float4
+  for (uint32_t item = i0; item < i1; ++item) {
+    const int np2 = (((__ldg(&A.items[item].y) + 1) >> 1) + 1) & ~1;
+    __syncwarp();
+    const float4* src = dq + (size_t)item * 80;
+    tab[lane] = __ldcg(&src[lane]);
+    tab[32 + lane] = __ldcg(&src[32 + lane]);
+    if (lane < 16) tab[64 + lane] = __ldcg(&src[64 + lane]);
+    __syncwarp();
+    for (int jp = 0; jp < np2; ++jp) {
+      const float4 QA = S.pA[jp], QB = S.pB[jp], QC = S.pC[jp], QD = S.pD[jp], QE = S.pE[jp];
+      eik_bwd_pair<OFF>(aA, bA, beta2A, QA, QB, QC, QD, QE, s0);
+      eik_bwd_pair<OFF>(aB, bB, beta2B, QA, QB, QC, QD, QE, s1);
+    }
+  }
+  if (i0 < i1) {
+    if (hA) eik_red<OFF>(s0, aA, bA, (int)idA, kv.n_nodes, F.gpad);
+    if (hB) eik_red<OFF>(s1, aB, bB, (int)idB, kv.n_nodes, F.gpad);
+  }
+}
+
+__global__ void __launch_bounds__(32 * DE_WARPS) k_dense_eik_bwd(const FitArgs F, const float4* __restrict__ dq, int G) {
+  __shared__ EikSmem smem[DE_WARPS];
+  const uint32_t u = blockIdx.x * DE_WARPS + (threadIdx.x >> 5);
+  const uint32_t kb = u / (uint32_t)G, g = u % (uint32_t)G;
+  if (kb * 64u >= F.iota_n) return;
+  const uint32_t n_items = *F.f.n_items;
+  const uint32_t ipg = (n_items + G - 1) / G;
+  const uint32_t i0 = g * ipg, i1 = min(n_items, i0 + ipg);
+  const uint32_t last = min(kb * 64u + 63u, F.iota_n - 1u);
+  if (F.iota[last] < (uint32_t)F.f.kv.n_nodes) dense_eik_unit<false>(F, dq, smem[threadIdx.x >> 5], kb, i0, i1);
+  else dense_eik_unit<true>(F, dq, smem[threadIdx.x >> 5], kb, i0, i1);
+}
+
+int64_t dense_eik_part_elems(int64_t n_items, uint32_t iota_n) {
+  int S, G;
+  uint32_t ks;
+  dense_split_dims(n_items, iota_n, S, ks, G);
+  return n_items * S * DE_NSUM * 32;
+}
+
+int launch_dense_fit_eik(const FitArgs& a, int64_t n_items, float* part, float4* dq, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  int S, G;
+  uint32_t ks;
+  dense_split_dims(n_items, a.iota_n, S, ks, G);
+  const int64_t ufwd = n_items * S;
+  k_dense_eik_fwd<<<(unsigned)((ufwd + DE_WARPS - 1) / DE_WARPS), 32 * DE_WARPS, 0, s>>>(a, part, S, ks);
+  k_dense_eik_combine<<<(unsigned)((n_items + 3) / 4), 128, 0, s>>>(a, part, S, dq);
+  const int64_t ubwd = ((a.iota_n + 63) / 64) * (int64_t)G;
+  k_dense_eik_bwd<<<(unsigned)((ubwd + DE_WARPS - 1) / DE_WARPS), 32 * DE_WARPS, 0, s>>>(a, dq, G);
+  return 3;
+}
+
 int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   const unsigned blocks = (unsigned)std::min<int64_t>((n_items + FE_WARPS - 1) / FE_WARPS, FE_BLOCKS);

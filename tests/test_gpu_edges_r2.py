@@ -128,3 +128,25 @@ def test_mesh_without_surface_and_minimal_lattice():
     assert lat.shape == (8, 8, 8)
     v2, t2, _, _ = m.mesh(2, lo=(-0.1, -0.1, -0.1), hi=(0.9, 0.9, 0.9))  # one cube across the sphere
     assert v2.shape[0] >= 3 and t2.shape[0] >= 1
+
+
+@pytest.mark.parametrize("R,J", [(8, 2000), (16, 3000)])
+def test_dense_eikonal_fused_parity(R, J):
+    """cutoff_T = inf with the MSE + Eikonal loss: the key-sliced dense kernels (k_dense_eik_*)
+    against the oracle's global sums: O, G via eval, the loss and all 13 gradient channels; a few
+    out-of-domain queries take the split kernels."""
+    tor = synth.Torus()
+    th = synth.fitted_like_theta(R, tor, 71)
+    q, o = synth.sample_batch(tor, J, seed=72)
+    q[:20] = synth.rng(73).uniform(1.02, 1.2, size=(20, 3)) * np.sign(q[:20])
+    o = tor.sdf(q.astype(np.float64)).astype(np.float32)
+    m = ef.EFunc(R, th, cutoff_T=float("inf"))
+    g, O, L = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE_EIKONAL, eikonal_lambda=0.1, want_O=True)
+    torch.cuda.synchronize()
+    f = orc.forward(th, R, q)
+    Lm, r = orc.mse_loss(f.O, o)
+    Le, h = orc.eikonal_loss(f.G, 0.1)
+    assert nw(O.cpu().numpy(), f.O) <= 1e-5
+    assert abs(float(L.item()) - (Lm + Le)) <= 1e-5 * (Lm + Le)
+    check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r, h))
+    assert m.stats()["candidate_pairs"] == J * 2 * R ** 3

@@ -59,6 +59,12 @@ def main():
                 row["dense_pairs"] = a.J * 2 * R ** 3
                 row["fused_Tlaneops_per_s"] = ops / (t_fb * 1e-3) / 1e12
                 row["fused_frac_fp32"] = row["fused_Tlaneops_per_s"] / 35.22
+            if T == float("inf"):  # the MSE + Eikonal loss (C3's), every pair
+                t_eik = timed(lambda: m.forward_backward(qd, od, loss=ef.LOSS_MSE_EIKONAL, grad=grad,
+                                                         want_loss=False), reps)
+                ops_e = a.J * R ** 3 * ((23 + 33) + (23 + 42))
+                row["eikonal_fused_fwd_bwd_ms"] = t_eik
+                row["eikonal_fused_frac_fp32"] = ops_e / (t_eik * 1e-3) / 1e12 / 35.22
             rows.append(row)
             print(json.dumps(rows[-1]), flush=True)
     lines = ["# Table 4 on B200 (J = 16384 queries; torus, paper init + mean-shift offsets)", "",
@@ -67,13 +73,15 @@ def main():
              "times; forward = efunc_forward (O + MSE upstream), backward = efunc_backward (MSE), fused = "
              "efunc_forward_backward. T = inf evaluates every pair (the paper's definition); T = 20 is the "
              "certified cutoff (DESIGN.md R-1).", "",
-             "| I (per bank) | T | fwd ms | bwd ms | fused fwd+bwd ms | paper fwd ms | paper bwd ms | paper / ours (fwd+bwd) | fused frac of FP32 peak (dense) |",
-             "|---|---|---|---|---|---|---|---|---|"]
+             "| I (per bank) | T | fwd ms | bwd ms | fused fwd+bwd ms | paper fwd ms | paper bwd ms | paper / ours (fwd+bwd) | fused frac of FP32 peak (dense) | + Eikonal fused ms (frac) |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         ours = min(r["fwd_ms"] + r["bwd_ms"], r["fused_fwd_bwd_ms"])
         lines.append(f"| {r['R']}^3 | {r['T']:g} | {r['fwd_ms']:.3f} | {r['bwd_ms']:.3f} | {r['fused_fwd_bwd_ms']:.3f} | "
                      f"{r['paper_fwd_ms']} | {r['paper_bwd_ms']} | {(r['paper_fwd_ms'] + r['paper_bwd_ms']) / ours:.1f}x | "
-                     + (f"{r['fused_frac_fp32']:.2f} |" if "fused_frac_fp32" in r else "— |"))
+                     + (f"{r['fused_frac_fp32']:.2f} |" if "fused_frac_fp32" in r else "— |")
+                     + (f" {r['eikonal_fused_fwd_bwd_ms']:.3f} ({r['eikonal_fused_frac_fp32']:.2f}) |"
+                        if "eikonal_fused_fwd_bwd_ms" in r else " — |"))
     txt = "\n".join(lines) + "\n"
     print(txt)
     if a.out:
