@@ -766,7 +766,10 @@ __global__ void __launch_bounds__(32 * FL_WARPS, 3) k_fit_lists(const FitArgs F)
 constexpr int DN_WARPS = 4;
 // item box diagonal^2 above which the dense forward uses the direct form: the expansion about the
 // box centre rounds the exponent by ~eps bl D^2 (2e-5 log2 units at D = 0.6, beta = e^7)
-constexpr float DN_LOCAL2 = 0.36f;
+#ifndef DN_LOCAL2_V
+#define DN_LOCAL2_V 0.36f
+#endif
+constexpr float DN_LOCAL2 = DN_LOCAL2_V;
 
 __global__ void __launch_bounds__(32 * DN_WARPS) k_dense_fwd(const FitArgs F, float2* __restrict__ zm, int S,
                                                              uint32_t ks) {
@@ -944,7 +947,10 @@ __device__ __forceinline__ void dense_bwd_unit(const FitArgs& F, const float4* _
   }
 }
 
-__global__ void __launch_bounds__(32 * DN_WARPS) k_dense_bwd(const FitArgs F, const float4* __restrict__ dq, int G) {
+#ifndef DN_BWD_MINB
+#define DN_BWD_MINB 1  // resident CTAs per SM the dense backward is compiled for
+#endif
+__global__ void __launch_bounds__(32 * DN_WARPS, DN_BWD_MINB) k_dense_bwd(const FitArgs F, const float4* __restrict__ dq, int G) {
   __shared__ float4 stage[DN_WARPS][48];
   const uint32_t u = blockIdx.x * DN_WARPS + (threadIdx.x >> 5);
   const uint32_t kb = u / (uint32_t)G, g = u % (uint32_t)G;
