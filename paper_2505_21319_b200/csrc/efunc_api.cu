@@ -164,6 +164,10 @@ int bits_for(size_t nvals) {  // bits of the largest value nvals - 1
   return b;
 }
 
+#ifndef EF_ITEMS_FUSED_MAX
+#define EF_ITEMS_FUSED_MAX 0u  // the single-CTA item pass measured slower at C2 (32k bricks): off
+#endif
+
 // S0 + key binning + brick lists. force = 1: theta was replaced wholesale, rebuild the lists
 // regardless of the Verlet skin.
 // degree 0 (Table 3 G-0: f = c): the g channels of both banks held at 0
@@ -211,12 +215,12 @@ int variant_channels(int variant, int degree, ef::VarLayout* L) {
 efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
   if (force) h->launches += launch_zero_channels(h->theta, h->n_nodes, g_channels(h), s);
   CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
-  CK(cudaMemsetAsync(h->cell_fill, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
   if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->keys_resort, force ? 1 : 0, sizeof(uint32_t), s));
   const float skin = SKIN_H * h->h;
-  h->launches += launch_prep_keys(h->theta, h->R, h->banks, h->key_raw, h->key_cell, h->cell_count, h->key_ref,
+  h->launches += launch_prep_keys(h->theta, h->R, h->banks, h->key_raw, h->key_cell,
+                                  h->cfg.deterministic ? nullptr : h->key_rank, h->cell_count, h->key_ref,
                                   skin * skin, SKIN_MU, h->ds, s);
   // the cell sort only when some offset key changed cell (k_prep_keys sets keys_resort)
   const uint32_t* gate = &h->ds->keys_resort;
@@ -227,7 +231,7 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
     h->launches += launch_stable_sort(h->key_cell, h->n_keys, bits_for((size_t)h->n_cells + 1), h->rk, h->rh,
                                       h->scan_tmp, h->key_tmp, h->key_order, s, gate);
   else
-    h->launches += launch_scatter_only(h->key_cell, h->n_keys, h->cell_start, h->cell_fill, h->key_order, s, gate);
+    h->launches += launch_scatter_ranked(h->key_cell, h->key_rank, h->n_keys, h->cell_start, h->key_order, s, gate);
   h->launches += launch_gather_keys(h->key_order, h->key_raw, h->key_sorted, h->kid, h->n_keys, s);
   // per-brick candidate lists for the next forward/backward (query independent)
   h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
@@ -313,7 +317,7 @@ void free_all(efunc_t* h) {
   dfree(h->theta); dfree(h->m); dfree(h->v);
   dfree(h->theta_v); dfree(h->m_v); dfree(h->v_v); dfree(h->thetaH); dfree(h->keyH); dfree(h->gint); dfree(h->gH);
   dfree(h->key_raw); dfree(h->key_sorted); dfree(h->kid); dfree(h->key_cell);
-  dfree(h->cell_count); dfree(h->cell_start); dfree(h->cell_fill); dfree(h->key_tmp); dfree(h->key_order);
+  dfree(h->cell_count); dfree(h->cell_start); dfree(h->cell_fill); dfree(h->key_tmp); dfree(h->key_rank); dfree(h->key_order);
   dfree(h->scan_tmp); dfree(h->ds); dfree(h->fit_grad); dfree(h->rk); dfree(h->rh);
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
@@ -374,9 +378,13 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
       h->launches += launch_gather_queries(h->q_order, q, o_used, J, h->qs, h->perm, s);
   }
   // work items: balanced runs of <= QW sorted queries of one brick
-  h->launches += launch_items_count(h->bin_start, nb, h->bg.qsub, h->item_cnt, s);
-  h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
-  h->launches += launch_items_write(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
+  if (nb + 2 <= EF_ITEMS_FUSED_MAX) {  // one single-CTA pass
+    h->launches += launch_items_fused(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
+  } else {
+    h->launches += launch_items_count(h->bin_start, nb, h->bg.qsub, h->item_cnt, s);
+    h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
+    h->launches += launch_items_write(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
+  }
   const int64_t items = (J + IQ - 1) / IQ + nb + 1;  // launch bound; kernels read the count
   h->fwd_items_bound = items;
   a = FwdArgs{};
@@ -983,6 +991,7 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->kid, h->n_keys));
     CK(dalloc(&h->key_cell, h->n_keys));
     CK(dalloc(&h->key_tmp, h->n_keys));
+    CK(dalloc(&h->key_rank, h->n_keys));
     CK(dalloc(&h->key_order, h->n_keys));
     CK(dalloc(&h->cell_count, h->n_cells + 1));
     CK(dalloc(&h->cell_start, h->n_cells + 1));

@@ -203,7 +203,8 @@ struct VarLayout {
 };
 
 // ---------------------------------------------------------------- launchers (host)
-int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* key_rank,
+                     uint32_t* cell_count,
                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s);
 int launch_list_snapshot(const float4* key_raw, float4* key_ref, int n_keys, DevScalars* ds,
                          cudaStream_t s);
@@ -221,7 +222,7 @@ int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom
                       float inv_h, uint32_t* bins, uint32_t* count, uint32_t* rank, DevScalars* ds,
                       cudaStream_t s);
 int launch_scatter_ranked(const uint32_t* bin, const uint32_t* rank, uint32_t n, const uint32_t* bin_start,
-                          uint32_t* out_idx, cudaStream_t s);
+                          uint32_t* out_idx, cudaStream_t s, const uint32_t* gate = nullptr);
 int launch_gather_queries(const uint32_t* order, const float* q, const float* o, int64_t J,
                           float4* qs, int* perm, cudaStream_t s);
 int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const float* q, const float* o, int64_t J,
@@ -229,6 +230,8 @@ int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const fl
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
                         uint32_t* out_idx, cudaStream_t s, const uint32_t* gate = nullptr);
 int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s);
+int launch_items_fused(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* item_off, int4* items,
+                       cudaStream_t s);
 int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
                        cudaStream_t s);
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
@@ -324,6 +327,7 @@ struct efunc {
   uint32_t* cell_start = nullptr;   // n_cells + 1
   uint32_t* cell_fill = nullptr;
   uint32_t* key_tmp = nullptr;
+  uint32_t* key_rank = nullptr;     // each key's position in its cell (ranked scatter)
   uint32_t* key_order = nullptr;
   uint32_t* scan_tmp = nullptr;     // block sums for scans
   size_t scan_tmp_cap = 0;

@@ -19,7 +19,8 @@ __device__ __forceinline__ int cell_clamp(float p, float inv_h, int NC) {
 // Also checks the brick lists' Verlet skin: a key that moved more than skin from its position at
 // the last list build, or whose bl left [ref/(1+mu), ref*(1+mu)], invalidates the lists.
 __global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, float4* __restrict__ key_raw,
-                            uint32_t* __restrict__ key_cell, uint32_t* __restrict__ cell_count,
+                            uint32_t* __restrict__ key_cell, uint32_t* __restrict__ key_rank,
+                            uint32_t* __restrict__ cell_count,
                             const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
   const int N = R * R * R;
   const int NC = R - 1;
@@ -55,8 +56,11 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, f
     resort |= key_cell[N + n] != c1;  // grid-bank cells never change
     key_cell[n] = c0;
     key_cell[N + n] = c1;
-    atomicAdd(&cell_count[c0], 1u);
-    atomicAdd(&cell_count[c1], 1u);
+    const uint32_t rk0 = atomicAdd(&cell_count[c0], 1u), rk1 = atomicAdd(&cell_count[c1], 1u);
+    if (key_rank) {  // positions inside the cells for the ranked scatter (non-deterministic mode)
+      key_rank[n] = rk0;
+      key_rank[N + n] = rk1;
+    }
     local_min = fminf(local_min, fminf(on0 ? bl0 : INFINITY, on1 ? bl1 : INFINITY));
     const float4 r0 = key_ref[n], r1 = key_ref[N + n];
     const float ex = px - r1.x, ey = py - r1.y, ez = pz - r1.z;
@@ -74,12 +78,14 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, f
   if (__any_sync(~0u, resort) && (threadIdx.x & 31) == 0) atomicOr(&ds->keys_resort, 1u);
 }
 
-int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* cell_count,
+int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* key_rank,
+                     uint32_t* cell_count,
                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s) {
   const int N = R * R * R;
   int blocks = (N + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, banks, key_raw, key_cell, cell_count, key_ref, skin2, mu, ds);
+  k_prep_keys<<<blocks, 256, 0, s>>>(theta, R, banks, key_raw, key_cell, key_rank, cell_count, key_ref, skin2, mu,
+                                     ds);
   return 1;
 }
 
@@ -390,15 +396,17 @@ int launch_query_bins(const float* q, const float* o, int64_t J, const BrickGeom
 }
 
 __global__ void k_scatter_ranked(const uint32_t* __restrict__ bin, const uint32_t* __restrict__ rank, uint32_t n,
-                                 const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ out_idx) {
+                                 const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ out_idx,
+                                 const uint32_t* gate) {
+  GATED;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out_idx[bin_start[bin[i]] + rank[i]] = i;
 }
 
 int launch_scatter_ranked(const uint32_t* bin, const uint32_t* rank, uint32_t n, const uint32_t* bin_start,
-                          uint32_t* out_idx, cudaStream_t s) {
+                          uint32_t* out_idx, cudaStream_t s, const uint32_t* gate) {
   if (n == 0) return 0;
-  k_scatter_ranked<<<grid_for(n, 256), 256, 0, s>>>(bin, rank, n, bin_start, out_idx);
+  k_scatter_ranked<<<grid_for(n, 256), 256, 0, s>>>(bin, rank, n, bin_start, out_idx, gate);
   return 1;
 }
 
@@ -469,6 +477,39 @@ __global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t n
       items[o + i] = make_int4((int)(s + a), (int)(b - a), brick, 0);
     }
   }
+}
+
+// count + exclusive scan + write of the work items in one single-CTA pass (small brick counts):
+// three launches and a three-kernel scan become one
+__global__ void __launch_bounds__(1024) k_items_fused(const uint32_t* __restrict__ bin_start, uint32_t nb,
+                                                     uint32_t qsub, uint32_t* __restrict__ item_off,
+                                                     int4* __restrict__ items) {
+  __shared__ uint32_t s_w[33];
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 <= nb + 1; c0 += 1024) {
+    const uint32_t c = c0 + threadIdx.x;
+    uint32_t st = 0, n = 0, m = 0;
+    if (c <= nb) {
+      brick_range(bin_start, c, nb, qsub, st, n);
+      m = (n + IQ - 1) / IQ;
+    }
+    uint32_t total;
+    const uint32_t off = block_excl_scan_1024(m, s_w, &total) + carry;
+    if (c <= nb + 1) item_off[c] = off;  // item_off[nb + 1]: the number of items
+    const int brick = (c == nb) ? -1 : (int)c;
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint32_t a = (uint32_t)(((uint64_t)i * n) / m), b = (uint32_t)(((uint64_t)(i + 1) * n) / m);
+      items[off + i] = make_int4((int)(st + a), (int)(b - a), brick, 0);
+    }
+    carry += total;
+    __syncthreads();
+  }
+}
+
+int launch_items_fused(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* item_off, int4* items,
+                       cudaStream_t s) {
+  k_items_fused<<<1, 1024, 0, s>>>(bin_start, nb, qsub, item_off, items);
+  return 1;
 }
 
 int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s) {
