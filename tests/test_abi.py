@@ -92,3 +92,24 @@ def test_create_fails_cleanly_without_gpu(lib):
     st = L.efunc_create(ctypes.byref(cfg), None, ctypes.byref(h))
     assert st in (efunc.ECUDA, efunc.EINVAL)
     assert L.efunc_last_error(None)
+
+
+def test_default_decay_mask_covers_polynomial_coefficients_only():
+    """The binding's default AdamW decay mask (reading R-10, SPEC D15) decays the polynomial
+    coefficients c, g (and H) of every bank of a layout and never the scales s or offsets Delta."""
+    from oracle import variant_oracle as vo
+    from paper_2505_21319_b200 import efunc
+    for variant, banks in ((efunc.VARIANT_GRID, vo.GRID), (efunc.VARIANT_OFFSET, vo.OFFSET),
+                           (efunc.VARIANT_COMBINED, vo.BOTH)):
+        for degree in (0, 1, 2):
+            lay = vo.layout(banks, degree)
+            want = 0
+            for key in ("grid", "off"):
+                if lay[key] is not None:
+                    for c in range(1, 1 + vo.NCOEF[degree]):
+                        want |= 1 << (lay[key] + c)
+            got = efunc._coef_mask(variant, degree)
+            if variant == efunc.VARIANT_COMBINED and degree == 0:
+                assert got == efunc.DEFAULT_DECAY_MASK  # the 13-channel tie keeps its mask
+            else:
+                assert got == want, (variant, degree, bin(got), bin(want))
