@@ -17,7 +17,11 @@
  *   the smallest exponent of query j (reading R-1). cutoff_T = INFINITY
  *   (or <= 0) evaluates every pair (the paper's dense definition).
  *
- * Parameter layout (theta, gradients, AdamW moments): float32 [R^3][13],
+ * Beyond the default model the library covers the other Table 3 families (efunc_variant and
+ * degree 0/1/2, parameter layouts by efunc_channels), cosine-series stacks (efunc_cosine_*),
+ * and inference to a mesh (efunc_mesh: lattice O, Marching Cubes, vertex normals).
+ *
+ * Parameter layout (theta, gradients, AdamW moments) of the default model: float32 [R^3][13],
  *   node n = x + R*(y + R*z), lattice k_n = float32(-1 + 2*x/(R-1), ...) on [-1,1]^3,
  *   channels (Table 3 row Full-4):
  *     0 s0 | 1 c0 | 2..4 g0 | 5..7 Delta | 8 s1 | 9 c1 | 10..12 g1
