@@ -510,7 +510,7 @@ __device__ __forceinline__ void fit_item_enum(const FitArgs& F, const uint32_t i
 }
 
 // Item types the list builder hands on
-constexpr uint32_t IT_NORMAL = 0, IT_ENUM = 1, IT_SKIP = 2, IT_END = 3;
+constexpr uint32_t IT_NORMAL = 0, IT_ENUM = 1, IT_SKIP = 2;
 
 // Part 1 of a work item: the box and its candidate ids (into Lw, or the all-keys list in dense
 // mode). Returns IT_NORMAL with L, wn, o set; IT_ENUM for an overflowed brick (fit_item_enum

@@ -386,21 +386,61 @@ __global__ void __launch_bounds__(32 * FK_WARPS, FK_MIN_BLOCKS / FK_WARPS) k_for
 }
 
 // S1 gather for the fused path: sorted {x,y,z,o}, the permutation, and each query's shift bound
-// mh_j >= m_j (k_common.cuh shift_bound), one query per thread: the latency-bound corner and
-// own-cell key loads run here at full occupancy instead of inside the FP32-bound k_fit.
+// mh_j >= m_j, one query per thread at full occupancy instead of inside the FP32-bound k_fit. The
+// bound is shift_bound's (same keys, same visit order, same strict minimum), with the candidates'
+// records loaded together (8 corners, then the own cell's keys 4 at a time) and the argmin key's
+// polynomial record read once at the end.
 __global__ void k_gather_queries_mh(const KeysView kv, const uint32_t* __restrict__ order, const float* __restrict__ q,
                                     const float* __restrict__ o, int64_t J, float4* __restrict__ qs,
                                     int* __restrict__ perm, float* __restrict__ qmh, float* __restrict__ qf0) {
+  const int R = kv.R, NC = kv.NC;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < J; p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t j = order[p];
     const float4 v = make_float4(q[3 * (size_t)j], q[3 * (size_t)j + 1], q[3 * (size_t)j + 2], o ? o[j] : 0.0f);
     qs[p] = v;
     perm[p] = (int)j;
-    float mh, f0;
-    float3 g0;
-    shift_bound(kv, v, mh, f0, g0);
+    const int cx = cellc(v.x, kv.inv_h, NC), cy = cellc(v.y, kv.inv_h, NC), cz = cellc(v.z, kv.inv_h, NC);
+    const int cid = (cz * NC + cy) * NC + cx;
+    const uint32_t s0 = __ldg(&kv.cell_start[cid]);
+    const uint32_t s1 = min(__ldg(&kv.cell_start[cid + 1]), s0 + 32u);
+    float4 ka[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      ka[c] = __ldg(&kv.grid_raw[2 * ((cx + (c & 1)) + R * ((cy + ((c >> 1) & 1)) + R * (cz + (c >> 2))))]);
+    float mh = INFINITY;
+    const float4* best = kv.grid_raw;
+    float4 bk = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float e = exponent(v, ka[c]);
+      if (e < mh) {
+        mh = e;
+        best = &kv.grid_raw[2 * ((cx + (c & 1)) + R * ((cy + ((c >> 1) & 1)) + R * (cz + (c >> 2))))];
+        bk = ka[c];
+      }
+    }
+    for (uint32_t k0 = s0; k0 < s1; k0 += 4) {
+      float4 kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kk[u] = (k0 + u < s1) ? __ldg(&kv.ks[2 * (k0 + u)]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < s1) {
+          const float e = exponent(v, kk[u]);
+          if (e < mh) {
+            mh = e;
+            best = &kv.ks[2 * (k0 + u)];
+            bk = kk[u];
+          }
+        }
+      }
+    }
     qmh[p] = mh;
-    if (qf0) qf0[p] = f0;
+    if (qf0) {
+      const float4 b = __ldg(best + 1);
+      const float dx = v.x - bk.x, dy = v.y - bk.y, dz = v.z - bk.z;
+      qf0[p] = (mh < INFINITY) ? fmaf(b.w, dz, fmaf(b.z, dy, fmaf(b.y, dx, b.x))) : 0.0f;
+    }
   }
 }
 

@@ -78,7 +78,7 @@ static void mc_build_table(McTable& T) {
     int next[12];
     for (int e = 0; e < 12; ++e) next[e] = -1;
     for (int f = 0; f < 6; ++f) {
-      int ex[2], en[2], nx = 0, nn = 0, order[4], type[4], m = 0;
+      int order[4], type[4], m = 0;
       for (int k = 0; k < 4; ++k) {
         const int c0 = face[f][k], c1 = face[f][(k + 1) % 4];
         if (in(c0) != in(c1)) {
@@ -87,7 +87,6 @@ static void mc_build_table(McTable& T) {
           ++m;
         }
       }
-      (void)ex; (void)en; (void)nx; (void)nn;
       // pair every exit with the cyclically preceding enter (separates inside corners)
       for (int k = 0; k < m; ++k) {
         if (type[k] != 1) continue;
