@@ -607,6 +607,16 @@ int fit_pre_off() {
   return off;
 }
 
+// EFUNC_FIT_TC=0/1: the MSE fused fit step on k_fit (FP32 pair loops) or k_fit_tc (tensor-core
+// pair loops, 3xTF32)
+int fit_tc_on() {
+  static const int on = [] {
+    const char* e = std::getenv("EFUNC_FIT_TC");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return on;
+}
+
 // efunc_forward_backward: the fused fit kernel for the MSE loss (k_fit.cu), the split kernels for
 // its leftover items; forward + backward otherwise.
 efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int64_t J, const efunc_loss* loss,
@@ -678,7 +688,9 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   } else {
     const int slot = timing_begin(h, s);
     if (f.pre) h->launches += launch_fit_lists(f, h->fwd_items_bound, s);
-    h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s) : launch_fit(f, h->fwd_items_bound, s);
+    h->launches += eik ? launch_fit_eik(f, h->fwd_items_bound, s)
+                       : (fit_tc_on() && !f.pre) ? launch_fit_tc(f, h->fwd_items_bound, s)
+                                                 : launch_fit(f, h->fwd_items_bound, s);
     timing_end(h, slot, s);
   }
   // items the fused kernel left (no brick list / shift-bound overflow): the split kernels

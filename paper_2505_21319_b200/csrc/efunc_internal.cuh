@@ -238,6 +238,7 @@ int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s
 int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s);
+int launch_fit_tc(const FitArgs& a, int64_t n_items, cudaStream_t s);  // tensor-core pair loops
 int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_det_bound(const float* theta, int n_nodes, const float4* qs, int64_t J, float inv_J, float* umax,
                      cudaStream_t s);

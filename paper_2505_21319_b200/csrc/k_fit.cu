@@ -1001,6 +1001,339 @@ int launch_fit_lists(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   return 1;
 }
 
+// ------------------------------------------------------------------ tensor-core pair loops (k_fit_tc)
+// The same work items, lists and outputs as k_fit, with the per-pair contractions on the tensor
+// cores (warp-level mma.sync m16n8k8, TF32 inputs, FP32 accumulation):
+//   exponent   e_ij = phi_j . E_i,  phi_j = [qq_j, x'_j, y'_j, z'_j, 1],  E_i = [-bl_i, A_i, C_i]
+//   polynomial f_ij = phi_j . P_i,  P_i = [0, g_i, c'_i]      (the item-local expansion of k_fit)
+//   backward   sum_j t_ij X_j = sum_j p_ij (rho_j X_j),  sum_j u_ij X_j = sum_j (p_ij del_ij)(rho_j X_j)
+//              with p_ij = 2^e_ij, del_ij = f_ij - O_j, X_j in {1, q'_j} (t) and {1, q'_j, qq_j} (u)
+// (Alg. 1 PAPER.md:L505-518 and Alg. 2 L540-568 as contractions over a 5-term feature axis and the
+// item's query axis). Every contraction runs as three TF32 products (3xTF32: hi*hi + hi*lo + lo*hi
+// with hi = the top 11 significand bits, lo = x - hi), which keeps ~2^-21 relative accuracy per
+// product, so the exponent of a kept pair (|terms| <= ~50 log2 units) carries ~2e-5 log2 units of
+// error, well inside the 1e-5 value / 1e-4 gradient tolerances (DESIGN.md R-T, R-TC).
+// The CUDA cores keep what is not a contraction: 2^e (MUFU.EX2), the forward's Z and M sums, f - O,
+// p del and the hi/lo splits. One warp per item as in k_fit; the forward's M dimension is the
+// item's queries (two 16-query tiles), the backward's the round's 32 candidate keys (two tiles).
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t a0, const uint32_t a1, const uint32_t a2,
+                                         const uint32_t a3, const uint32_t b0, const uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float tf_hi(const float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ uint32_t fu(const float x) { return __float_as_uint(x); }
+
+// K axis (16) of every exponent / polynomial contraction: positions 0-4 the hi parts of both sides,
+// 5-9 query hi x key lo, 10-14 query lo x key hi, 15 zero. A thread (g = lane/4, t = lane%4) of an
+// m16n8k8 fragment holds K positions {t, t+4} (k-step 0) and {8+t, 12+t} (k-step 1) of its rows /
+// columns, stored as one float4 per (row, t).
+__device__ __forceinline__ void tc_query_rec(float4* rec, const float* v) {  // query side (v: 5 features)
+  float h[5], l[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    h[i] = tf_hi(v[i]);
+    l[i] = v[i] - h[i];
+  }
+  rec[0] = make_float4(h[0], h[4], h[3], l[2]);
+  rec[1] = make_float4(h[1], h[0], h[4], l[3]);
+  rec[2] = make_float4(h[2], h[1], l[0], l[4]);
+  rec[3] = make_float4(h[3], h[2], l[1], 0.f);
+}
+__device__ __forceinline__ void tc_key_rec(float4* rec, const float* v) {  // key side
+  float h[5], l[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    h[i] = tf_hi(v[i]);
+    l[i] = v[i] - h[i];
+  }
+  rec[0] = make_float4(h[0], h[4], l[3], h[2]);
+  rec[1] = make_float4(h[1], l[0], l[4], h[3]);
+  rec[2] = make_float4(h[2], l[1], h[0], h[4]);
+  rec[3] = make_float4(h[3], l[2], h[1], 0.f);
+}
+
+struct TcSmem {
+  float4 qrec[QW][4];  // per query and t: phi_j on the query side of the K axis
+  union {
+    float4 krec[32 * 9];  // per round key and (type, t): E_i (type 0) / P_i (type 1), index 9 key + 4 type + t
+    float sx[32][12];     // backward: the round's per-key sums (after the A fragments are loaded)
+  };
+  float4 yrec[4][2][32];  // backward B fragments per 8-query tile: [tile][t-sums / u-sums][lane]
+  float nO[QW];           // -O_j
+};
+
+// the round's key lane -> its E / P records (far keys: E = -huge, P = 0: weight exactly 0)
+__device__ __forceinline__ void tc_key_prep(TcSmem& S, const KeyX& K, const int lane) {
+  const float E[5] = {K.nbl, K.Ax, K.Ay, K.Az, K.C};
+  const float P[5] = {0.f, K.gx, K.gy, K.gz, K.c};
+  tc_key_rec(&S.krec[9 * lane], E);
+  tc_key_rec(&S.krec[9 * lane + 4], P);
+}
+
+__device__ __forceinline__ void fit_item_tc(const FitArgs& F, const uint32_t item, TcSmem& S, const uint32_t* L,
+                                            const uint32_t wn, const float3 o) {
+  const FwdArgs& A = F.f;
+  const KeysView& kv = A.kv;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int4 it = A.items[item];
+  const int nact = it.y;
+  const bool act = lane < nact;
+  const int64_t js = (int64_t)it.x + lane;
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (act) q = A.qs[js];
+  __syncwarp();  // the previous item's readers of S are done
+  const float qx = q.x - o.x, qy = q.y - o.y, qz = q.z - o.z;
+  const float qq = act ? fmaf(qx, qx, fmaf(qy, qy, qz * qz)) : 1e30f;  // idle slot: weight exactly 0
+  {
+    const float phi[5] = {qq, qx, qy, qz, 1.0f};
+    tc_query_rec(S.qrec[lane], phi);
+  }
+  const float4 far_a = make_float4(1e18f, 1e18f, 1e18f, 1.0f), z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // ---- forward: M = queries (tiles of 16), N = 4 keys x {e, f} per group, 8 groups per round
+  __syncwarp();
+  const bool two_q = nact > 16;
+  const float4 qa0 = S.qrec[g][t], qa1 = S.qrec[g + 8][t], qa2 = S.qrec[16 + g][t], qa3 = S.qrec[24 + g][t];
+  float2 Z0 = make_float2(0.f, 0.f), M0 = Z0, Z1 = Z0, M1 = Z0;
+  {
+    uint32_t id1 = ((uint32_t)lane < wn) ? L[lane] : 0u;
+    uint32_t id2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+    float4 a1 = far_a, b1 = z4;
+    if ((uint32_t)lane < wn) ld_rec(&kv.grid_raw[2 * id1], a1, b1);
+    for (uint32_t base = 0; base < wn; base += 32) {
+      const uint32_t k = base + lane;
+      const float4 ka = a1, kb = b1;
+      id1 = id2;
+      id2 = (k + 64 < wn) ? L[k + 64] : 0u;
+      a1 = far_a;
+      b1 = z4;
+      if (k + 32 < wn) ld_rec(&kv.grid_raw[2 * id1], a1, b1);
+      tc_key_prep(S, key_x(ka, kb, o), lane);
+      __syncwarp();
+      const uint32_t left = wn - base;
+#pragma unroll
+      for (int G = 0; G < 8; ++G) {
+        if ((uint32_t)(4 * G) < left) {
+          const float4 B = S.krec[36 * G + lane + (lane >> 3)];
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          mma_tf32(d, fu(qa0.x), fu(qa1.x), fu(qa0.y), fu(qa1.y), fu(B.x), fu(B.y));
+          mma_tf32(d, fu(qa0.z), fu(qa1.z), fu(qa0.w), fu(qa1.w), fu(B.z), fu(B.w));
+          const float2 w = make_float2(ex2f(d[0]), ex2f(d[2]));
+          Z0 = __fadd2_rn(Z0, w);
+          M0 = __ffma2_rn(w, make_float2(d[1], d[3]), M0);
+          if (two_q) {
+            float d1[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_tf32(d1, fu(qa2.x), fu(qa3.x), fu(qa2.y), fu(qa3.y), fu(B.x), fu(B.y));
+            mma_tf32(d1, fu(qa2.z), fu(qa3.z), fu(qa2.w), fu(qa3.w), fu(B.z), fu(B.w));
+            const float2 w1 = make_float2(ex2f(d1[0]), ex2f(d1[2]));
+            Z1 = __fadd2_rn(Z1, w1);
+            M1 = __ffma2_rn(w1, make_float2(d1[1], d1[3]), M1);
+          }
+        }
+      }
+      __syncwarp();  // krec readers done before the next round's records
+    }
+  }
+  // sum over the quad (t holds keys t mod 4 of every group), then lane j takes query j's totals:
+  // query 16 mt + 8 h + g sits in lane 4g, component h of tile mt
+#pragma unroll
+  for (int o2 = 1; o2 <= 2; o2 <<= 1) {
+    Z0.x += __shfl_xor_sync(~0u, Z0.x, o2); Z0.y += __shfl_xor_sync(~0u, Z0.y, o2);
+    M0.x += __shfl_xor_sync(~0u, M0.x, o2); M0.y += __shfl_xor_sync(~0u, M0.y, o2);
+    Z1.x += __shfl_xor_sync(~0u, Z1.x, o2); Z1.y += __shfl_xor_sync(~0u, Z1.y, o2);
+    M1.x += __shfl_xor_sync(~0u, M1.x, o2); M1.y += __shfl_xor_sync(~0u, M1.y, o2);
+  }
+  float Z, M;
+  {
+    const int src = 4 * (lane & 7), sel = lane >> 3;
+    const float za = __shfl_sync(~0u, Z0.x, src), zb = __shfl_sync(~0u, Z0.y, src);
+    const float zc = __shfl_sync(~0u, Z1.x, src), zd = __shfl_sync(~0u, Z1.y, src);
+    const float ma = __shfl_sync(~0u, M0.x, src), mb = __shfl_sync(~0u, M0.y, src);
+    const float mc = __shfl_sync(~0u, M1.x, src), md = __shfl_sync(~0u, M1.y, src);
+    Z = sel == 0 ? za : sel == 1 ? zb : sel == 2 ? zc : zd;
+    M = sel == 0 ? ma : sel == 1 ? mb : sel == 2 ? mc : md;
+  }
+  const bool bad = act && !(Z >= FT_ZMIN && isfinite(Z) && isfinite(M));
+  if (__any_sync(~0u, bad)) {  // Z underflow (far queries): the split kernels shift exactly
+    if (lane == 0) A.slow_items[atomicAdd(&A.ds->slow_n, 1u)] = item;
+    return;
+  }
+  float O = 0.f, rho = 0.f, lossj = 0.f;
+  if (act) {
+    const float iz = 1.0f / Z;
+    O = M * iz;
+    const float diff = O - q.w;
+    const float r = 2.0f * diff * A.inv_J;
+    rho = r * iz;  // t_ij = r_j p_ij = (r_j / Z_j) 2^(-a_ij log2 e)
+    lossj = diff * diff * A.inv_J;
+    if (A.O) A.O[A.perm[js]] = O;
+  }
+  for (int s2 = 16; s2 > 0; s2 >>= 1) lossj += __shfl_xor_sync(~0u, lossj, s2);
+  if (lane == 0) {
+    A.loss_part[item] = lossj;
+    atomicAdd(&A.ds->cand_pairs, (unsigned long long)wn * (unsigned long long)nact);
+  }
+  // ---- backward: B fragments of the query side. Tile nt holds queries 8 nt .. 8 nt + 7, its K
+  // (query) order pairs query 8 nt + 2t with A column t and 8 nt + 2t + 1 with column t + 4, so the
+  // exponent MMA's accumulator is the accumulation MMA's A fragment as it stands.
+  {
+    S.nO[lane] = -O;
+    const int nt = lane >> 3, tt = (lane >> 1) & 3, h = lane & 1;
+    const float Y[5] = {rho, rho * qx, rho * qy, rho * qz, rho * (act ? qq : 0.f)};
+    float* yt = reinterpret_cast<float*>(&S.yrec[nt][0][0]);
+    float* yu = reinterpret_cast<float*>(&S.yrec[nt][1][0]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float v = c < 5 ? Y[c] : 0.f;
+      const float hi = tf_hi(v), lo = v - hi;
+      if (c < 4) {
+        yt[(4 * c + tt) * 4 + h] = hi;
+        yt[(4 * c + tt) * 4 + 2 + h] = lo;
+      } else {
+        yt[(4 * c + tt) * 4 + h] = 0.f;
+        yt[(4 * c + tt) * 4 + 2 + h] = 0.f;
+      }
+      yu[(4 * c + tt) * 4 + h] = hi;
+      yu[(4 * c + tt) * 4 + 2 + h] = lo;
+    }
+  }
+  __syncwarp();
+  const int ntiles = (nact + 7) >> 3;
+  uint32_t iA = ((uint32_t)lane < wn) ? L[lane] : 0u;
+  uint32_t iA2 = ((uint32_t)lane + 32 < wn) ? L[lane + 32] : 0u;
+  float4 aA = far_a, bA = z4;
+  if ((uint32_t)lane < wn) ld_rec(&kv.grid_raw[2 * iA], aA, bA);
+  for (uint32_t base = 0; base < wn; base += 32) {
+    const uint32_t k = base + lane;
+    const uint32_t id = iA;
+    const float4 a0 = aA, b0 = bA;
+    iA = iA2;
+    iA2 = (k + 64 < wn) ? L[k + 64] : 0u;
+    aA = far_a;
+    bA = z4;
+    if (k + 32 < wn) ld_rec(&kv.grid_raw[2 * iA], aA, bA);
+    const KeyX K = key_x(a0, b0, o);
+    tc_key_prep(S, K, lane);
+    __syncwarp();
+    const bool two_k = base + 16 < wn;
+    // A fragments of the round's two 16-key tiles (E and P records)
+    uint32_t ae[2][8], ap[2][8];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const float4 u = S.krec[9 * (16 * mt + g) + t], v = S.krec[9 * (16 * mt + g + 8) + t];
+      const float4 up = S.krec[9 * (16 * mt + g) + 4 + t], vp = S.krec[9 * (16 * mt + g + 8) + 4 + t];
+      ae[mt][0] = fu(u.x); ae[mt][1] = fu(v.x); ae[mt][2] = fu(u.y); ae[mt][3] = fu(v.y);
+      ae[mt][4] = fu(u.z); ae[mt][5] = fu(v.z); ae[mt][6] = fu(u.w); ae[mt][7] = fu(v.w);
+      ap[mt][0] = fu(up.x); ap[mt][1] = fu(vp.x); ap[mt][2] = fu(up.y); ap[mt][3] = fu(vp.y);
+      ap[mt][4] = fu(up.z); ap[mt][5] = fu(vp.z); ap[mt][6] = fu(up.w); ap[mt][7] = fu(vp.w);
+    }
+    float dt[2][4], du[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dt[mt][c] = du[mt][c] = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      if (nt < ntiles) {
+        const float4 Bq = S.qrec[8 * nt + g][t];
+        const float4 Yt = S.yrec[nt][0][lane], Yu = S.yrec[nt][1][lane];
+        const float2 nO = *reinterpret_cast<const float2*>(&S.nO[8 * nt + 2 * t]);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          if (mt == 0 || two_k) {
+            float de[4] = {0.f, 0.f, 0.f, 0.f}, df[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_tf32(de, ae[mt][0], ae[mt][1], ae[mt][2], ae[mt][3], fu(Bq.x), fu(Bq.y));
+            mma_tf32(de, ae[mt][4], ae[mt][5], ae[mt][6], ae[mt][7], fu(Bq.z), fu(Bq.w));
+            mma_tf32(df, ap[mt][0], ap[mt][1], ap[mt][2], ap[mt][3], fu(Bq.x), fu(Bq.y));
+            mma_tf32(df, ap[mt][4], ap[mt][5], ap[mt][6], ap[mt][7], fu(Bq.z), fu(Bq.w));
+            // de/df: (key g, q 2t), (key g, q 2t+1), (key g+8, q 2t), (key g+8, q 2t+1)
+            const float2 p01 = make_float2(ex2f(de[0]), ex2f(de[1])), p23 = make_float2(ex2f(de[2]), ex2f(de[3]));
+            const float2 u01 = __fmul2_rn(p01, __fadd2_rn(make_float2(df[0], df[1]), nO));
+            const float2 u23 = __fmul2_rn(p23, __fadd2_rn(make_float2(df[2], df[3]), nO));
+            const float ph0 = tf_hi(p01.x), ph1 = tf_hi(p01.y), ph2 = tf_hi(p23.x), ph3 = tf_hi(p23.y);
+            const float2 pl01 = __fadd2_rn(p01, make_float2(-ph0, -ph1)), pl23 = __fadd2_rn(p23, make_float2(-ph2, -ph3));
+            const float uh0 = tf_hi(u01.x), uh1 = tf_hi(u01.y), uh2 = tf_hi(u23.x), uh3 = tf_hi(u23.y);
+            const float2 ul01 = __fadd2_rn(u01, make_float2(-uh0, -uh1)), ul23 = __fadd2_rn(u23, make_float2(-uh2, -uh3));
+            // A fragment: a0 = (key g, col t) = q 2t, a1 = (key g+8, q 2t), a2 = (key g, q 2t+1), a3 = (key g+8, q 2t+1)
+            mma_tf32(dt[mt], fu(ph0), fu(ph2), fu(ph1), fu(ph3), fu(Yt.x), fu(Yt.y));
+            mma_tf32(dt[mt], fu(pl01.x), fu(pl23.x), fu(pl01.y), fu(pl23.y), fu(Yt.x), fu(Yt.y));
+            mma_tf32(dt[mt], fu(ph0), fu(ph2), fu(ph1), fu(ph3), fu(Yt.z), fu(Yt.w));
+            mma_tf32(du[mt], fu(uh0), fu(uh2), fu(uh1), fu(uh3), fu(Yu.x), fu(Yu.y));
+            mma_tf32(du[mt], fu(ul01.x), fu(ul23.x), fu(ul01.y), fu(ul23.y), fu(Yu.x), fu(Yu.y));
+            mma_tf32(du[mt], fu(uh0), fu(uh2), fu(uh1), fu(uh3), fu(Yu.z), fu(Yu.w));
+          }
+        }
+      }
+    }
+    __syncwarp();  // every lane's krec reads are done: sx aliases krec
+    // dt/du: (key 16mt+g, feature 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1); t-sums in features 0-3,
+    // u-sums in 0-4
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      if (t < 2) {
+        *reinterpret_cast<float2*>(&S.sx[16 * mt + g][2 * t]) = make_float2(dt[mt][0], dt[mt][1]);
+        *reinterpret_cast<float2*>(&S.sx[16 * mt + g + 8][2 * t]) = make_float2(dt[mt][2], dt[mt][3]);
+      }
+      if (t < 3) {
+        *reinterpret_cast<float2*>(&S.sx[16 * mt + g][4 + 2 * t]) = make_float2(du[mt][0], du[mt][1]);
+        *reinterpret_cast<float2*>(&S.sx[16 * mt + g + 8][4 + 2 * t]) = make_float2(du[mt][2], du[mt][3]);
+      }
+    }
+    __syncwarp();
+    if (k < wn) {
+      const float4 s0 = *reinterpret_cast<const float4*>(&S.sx[lane][0]);
+      const float4 s1 = *reinterpret_cast<const float4*>(&S.sx[lane][4]);
+      const float suq = S.sx[lane][8];
+      // q' sums -> d = q' - k' sums (as k_fit's bwd_sums_x)
+      const float sc = s0.x, su = s1.x;
+      MseSums ms;
+      ms.sc = sc;
+      ms.sgx = fmaf(-K.kx, sc, s0.y);
+      ms.sgy = fmaf(-K.ky, sc, s0.z);
+      ms.sgz = fmaf(-K.kz, sc, s0.w);
+      ms.ss = fmaf(K.kk, su, fmaf(-2.0f * K.kx, s1.y, fmaf(-2.0f * K.ky, s1.z, fmaf(-2.0f * K.kz, s1.w, suq))));
+      ms.sdx = fmaf(-K.kx, su, s1.y);
+      ms.sdy = fmaf(-K.ky, su, s1.z);
+      ms.sdz = fmaf(-K.kz, su, s1.w);
+      bwd_mse_out(F, ms, a0, b0, (int)id);
+    }
+    __syncwarp();  // sx readers done before the next round's krec
+  }
+}
+
+__device__ __forceinline__ void fit_item_tc_any(const FitArgs& F, const uint32_t item, TcSmem& S, FitSmem& S2,
+                                                uint32_t* Lw) {
+  const uint32_t* L;
+  uint32_t wn;
+  float3 o;
+  const uint32_t ty = fit_item_build(F, item, Lw, L, wn, o);
+  if (ty == IT_ENUM) fit_item_enum(F, item, S2, Lw);
+  else if (ty == IT_NORMAL) fit_item_tc(F, item, S, L, wn, o);
+}
+
+#ifndef TC_MIN_BLOCKS
+#define TC_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(32 * FT_WARPS, TC_MIN_BLOCKS) k_fit_tc(const FitArgs F) {
+  __shared__ TcSmem smem[FT_WARPS];
+  __shared__ FitSmem smem2[FT_WARPS];  // the overflowed-brick path (fit_item_enum)
+  const int w = threadIdx.x >> 5;
+  uint32_t* L = F.scratch + (size_t)(blockIdx.x * FT_WARPS + w) * SCRATCH_STRIDE;
+  for (;;) {
+    const int64_t item = fetch_item(&F.f.ds->fit_next, F.f.n_items, nullptr, nullptr);
+    if (item < 0) break;
+    fit_item_tc_any(F, (uint32_t)item, smem[w], smem2[w], L);
+  }
+}
+
+int launch_fit_tc(const FitArgs& a, int64_t n_items, cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n_items + FT_WARPS - 1) / FT_WARPS, 148 * TC_MIN_BLOCKS);
+  k_fit_tc<<<blocks, 32 * FT_WARPS, 0, s>>>(a);
+  return 1;
+}
+
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
   const unsigned blocks = (unsigned)std::min<int64_t>((n_items + FT_WARPS - 1) / FT_WARPS, FT_BLOCKS);
