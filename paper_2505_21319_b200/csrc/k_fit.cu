@@ -1336,6 +1336,12 @@ int launch_fit_tc(const FitArgs& a, int64_t n_items, cudaStream_t s) {
 
 int launch_fit(const FitArgs& a, int64_t n_items, cudaStream_t s) {
   if (n_items <= 0) return 0;
+#ifdef FT_CARVEOUT
+  static const bool carve = [] {  // shared-memory carveout (percent of the max) for A/B runs
+    return cudaFuncSetAttribute(k_fit, cudaFuncAttributePreferredSharedMemoryCarveout, FT_CARVEOUT) == cudaSuccess;
+  }();
+  (void)carve;
+#endif
   const unsigned blocks = (unsigned)std::min<int64_t>((n_items + FT_WARPS - 1) / FT_WARPS, FT_BLOCKS);
   k_fit<<<blocks, 32 * FT_WARPS, 0, s>>>(a);
   return 1;
