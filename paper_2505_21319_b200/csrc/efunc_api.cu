@@ -212,16 +212,25 @@ int variant_channels(int variant, int degree, ef::VarLayout* L) {
   return v.nch;
 }
 
-efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0) {
-  if (force) h->launches += launch_zero_channels(h->theta, h->n_nodes, g_channels(h), s);
+// the per-rebuild counters k_prep_keys / k_adamw_keys accumulate into
+efunc_status reset_key_counters(efunc_t* h, cudaStream_t s, int force) {
   CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
   CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
   if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
   CK(cudaMemsetAsync(&h->ds->keys_resort, force ? 1 : 0, sizeof(uint32_t), s));
-  const float skin = SKIN_H * h->h;
-  h->launches += launch_prep_keys(h->theta, h->R, h->banks, h->key_raw, h->key_cell,
-                                  h->cfg.deterministic ? nullptr : h->key_rank, h->cell_count, h->key_ref,
-                                  skin * skin, SKIN_MU, h->ds, s);
+  return EFUNC_OK;
+}
+
+// prepped: the key records were written by k_adamw_keys (AdamW and S0 in one pass)
+efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0, int prepped = 0) {
+  if (!prepped) {
+    if (force) h->launches += launch_zero_channels(h->theta, h->n_nodes, g_channels(h), s);
+    RET(reset_key_counters(h, s, force));
+    const float skin = SKIN_H * h->h;
+    h->launches += launch_prep_keys(h->theta, h->R, h->banks, h->key_raw, h->key_cell,
+                                    h->cfg.deterministic ? nullptr : h->key_rank, h->cell_count, h->key_ref,
+                                    skin * skin, SKIN_MU, h->ds, s);
+  }
   // the cell sort only when some offset key changed cell (k_prep_keys sets keys_resort)
   const uint32_t* gate = &h->ds->keys_resort;
   h->launches += launch_scan_u32(h->cell_count, h->cell_start, h->n_cells + 1, h->scan_tmp, s, gate);
@@ -736,8 +745,14 @@ efunc_status do_adamw(efunc_t* h, const float* grad, const efunc_adamw* hp, cuda
   if (h->vmode) {  // NEXT-4: the update runs on the user's layout, then the internal theta follows
     h->launches += launch_adamw(h->theta_v, grad, h->m_v, h->v_v, (int64_t)h->n_nodes * h->pnch, hc, h->ds, s);
     sync_internal_theta(h, s);
-  } else {
-    h->launches += launch_adamw(h->theta, grad, h->m, h->v, (int64_t)h->n_nodes * EF_NCH, hc, h->ds, s);
+  } else {  // AdamW and the key records of the updated theta in one pass (S6 + S0)
+    RET(reset_key_counters(h, s, 0));
+    const float skin = SKIN_H * h->h;
+    h->launches += launch_adamw_keys(h->theta, grad, h->m, h->v, hc, h->R, h->banks, h->key_raw, h->key_cell,
+                                     h->cfg.deterministic ? nullptr : h->key_rank, h->cell_count, h->key_ref,
+                                     skin * skin, SKIN_MU, h->ds, s);
+    CK(cudaGetLastError());
+    return rebuild_keys(h, s, 0, 1);
   }
   CK(cudaGetLastError());
   return rebuild_keys(h, s);

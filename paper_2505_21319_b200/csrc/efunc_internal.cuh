@@ -262,6 +262,39 @@ struct AdamWConst {  // the efunc_adamw hyper-parameters (doubles, like torch's 
 };
 int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamWConst& hc,
                  DevScalars* ds, cudaStream_t s);
+// S6 + S0 in one pass (13-channel layout): AdamW of each node's channels, then its two key records
+// from the updated theta (k_bin.cu k_adamw_keys; the same arithmetic as k_adamw + k_prep_keys)
+int launch_adamw_keys(float* theta, const float* grad, float* m, float* v, const AdamWConst& hc, int R, int banks,
+                      float4* key_raw, uint32_t* key_cell, uint32_t* key_rank, uint32_t* cell_count,
+                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s);
+
+// AdamW scalars for step t (torch's single-tensor AdamW; derived in double, rounded to fp32 once)
+struct AdamWScal {
+  float decay, omb1, b2, omb2, eps, step_size, sqrt_bc2;
+};
+__device__ __forceinline__ AdamWScal adamw_scal(const AdamWConst& hc, const unsigned long long t) {
+  const double bc1 = 1.0 - pow(hc.beta1, (double)t);
+  const double bc2 = 1.0 - pow(hc.beta2, (double)t);
+  AdamWScal c;
+  c.decay = (float)(1.0 - hc.lr * hc.weight_decay);
+  c.omb1 = (float)(1.0 - hc.beta1);
+  c.b2 = (float)hc.beta2;
+  c.omb2 = (float)(1.0 - hc.beta2);
+  c.eps = (float)hc.eps;
+  c.step_size = (float)(hc.lr / bc1);
+  c.sqrt_bc2 = (float)sqrt(bc2);
+  return c;
+}
+// one element: p *= decay (masked); m += (1-b1)(g-m); v = v b2 + (1-b2) g^2;
+// p += -step_size m / (sqrt(v)/sqrt(bc2) + eps)
+__device__ __forceinline__ float adamw_elem(float p, const float g, float& mi, float& vi, const bool dec,
+                                            const AdamWScal& c) {
+  if (dec) p *= c.decay;
+  mi = fmaf(c.omb1, g - mi, mi);
+  vi = fmaf(c.omb2, g * g, vi * c.b2);
+  const float denom = __fdiv_rn(__fsqrt_rn(vi), c.sqrt_bc2) + c.eps;
+  return fmaf(-c.step_size, __fdiv_rn(mi, denom), p);
+}
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);

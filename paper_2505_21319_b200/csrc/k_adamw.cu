@@ -12,37 +12,20 @@ namespace ef {
 // captured CUDA graph replays correct bias corrections.
 __global__ void k_adamw(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
                         float* __restrict__ v, int64_t n, const AdamWConst hc, DevScalars* ds) {
-  __shared__ float c[8];
+  __shared__ AdamWScal c;
   __shared__ unsigned long long t_next;
   if (threadIdx.x == 0) {
-    const unsigned long long t = ds->adam_t + 1;
-    const double bc1 = 1.0 - pow(hc.beta1, (double)t);
-    const double bc2 = 1.0 - pow(hc.beta2, (double)t);
-    c[0] = (float)(1.0 - hc.lr * hc.weight_decay);  // decay
-    c[1] = (float)(1.0 - hc.beta1);                  // 1 - b1
-    c[2] = (float)hc.beta2;
-    c[3] = (float)(1.0 - hc.beta2);                  // 1 - b2
-    c[4] = (float)hc.eps;
-    c[5] = (float)(hc.lr / bc1);                     // step_size
-    c[6] = (float)sqrt(bc2);
-    t_next = t;
+    t_next = ds->adam_t + 1;
+    c = adamw_scal(hc, t_next);
   }
   __syncthreads();
-  const float decay = c[0], omb1 = c[1], b2 = c[2], omb2 = c[3], eps = c[4], step_size = c[5], sqrt_bc2 = c[6];
+  const AdamWScal cs = c;
   const uint32_t mask = hc.decay_mask;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % hc.nch);
     if ((hc.frozen_mask >> ch) & 1u) continue;  // degree 0: g channels stay exactly 0
-    float p = theta[i];
-    const float g = grad[i];
-    if ((mask >> ch) & 1u) p *= decay;
-    float mi = m[i];
-    mi = fmaf(omb1, g - mi, mi);
-    float vi = v[i];
-    vi = fmaf(omb2, g * g, vi * b2);
-    const float denom = __fdiv_rn(__fsqrt_rn(vi), sqrt_bc2) + eps;
-    p = fmaf(-step_size, __fdiv_rn(mi, denom), p);
-    theta[i] = p;
+    float mi = m[i], vi = v[i];
+    theta[i] = adamw_elem(theta[i], grad[i], mi, vi, (mask >> ch) & 1u, cs);
     m[i] = mi;
     v[i] = vi;
   }

@@ -18,64 +18,142 @@ __device__ __forceinline__ int cell_clamp(float p, float inv_h, int NC) {
 // ------------------------------------------------------------------------------ S0
 // Also checks the brick lists' Verlet skin: a key that moved more than skin from its position at
 // the last list build, or whose bl left [ref/(1+mu), ref*(1+mu)], invalidates the lists.
+struct PrepOut {
+  float local_min = INFINITY;
+  bool moved = false, resort = false;
+};
+
+// node n's two key records from its 13 channels t (S0; see k_prep_keys)
+__device__ __forceinline__ void prep_key_node(const int n, const float* t, const int R, const int banks,
+                                              float4* __restrict__ key_raw, uint32_t* __restrict__ key_cell,
+                                              uint32_t* __restrict__ key_rank, uint32_t* __restrict__ cell_count,
+                                              const float4* __restrict__ key_ref, const float skin2, const float mu,
+                                              PrepOut& po) {
+  const int N = R * R * R;
+  const int NC = R - 1;
+  const float inv_h = (float)((R - 1) / 2.0);
+  const int x = n % R, y = (n / R) % R, z = n / (R * R);
+  // lattice k(i) = float32(-1 + 2 i/(R-1))  (reading R-2), evaluated in double
+  const float kx = (float)(-1.0 + 2.0 * x / (double)(R - 1));
+  const float ky = (float)(-1.0 + 2.0 * y / (double)(R - 1));
+  const float kz = (float)(-1.0 + 2.0 * z / (double)(R - 1));
+  const float bl0 = expf(t[0]) * EF_LOG2E;
+  const float bl1 = expf(t[8]) * EF_LOG2E;
+  const bool on0 = banks & 1, on1 = banks & 2;
+  // a bank the variant does not have (NEXT-4: O only / O^Delta only): its keys sit far away
+  // (weight exactly 0) in the sentinel cell n_cells that no enumeration visits
+  constexpr float FAR = 1e15f;
+  const float px = on1 ? kx + t[5] : FAR, py = on1 ? ky + t[6] : FAR, pz = on1 ? kz + t[7] : FAR;
+  const float gx = on0 ? kx : FAR, gy = on0 ? ky : FAR, gz = on0 ? kz : FAR;
+  key_raw[2 * n] = make_float4(gx, gy, gz, bl0);
+  key_raw[2 * n + 1] = make_float4(t[1], t[2], t[3], t[4]);
+  key_raw[2 * (N + n)] = make_float4(px, py, pz, bl1);
+  key_raw[2 * (N + n) + 1] = make_float4(t[9], t[10], t[11], t[12]);
+  const uint32_t nc3 = (uint32_t)(NC * NC * NC);
+  const uint32_t c0 = on0 ? (uint32_t)((cell_clamp(kz, inv_h, NC) * NC + cell_clamp(ky, inv_h, NC)) * NC +
+                                       cell_clamp(kx, inv_h, NC))
+                          : nc3;
+  const uint32_t c1 = on1 ? (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
+                                       cell_clamp(px, inv_h, NC))
+                          : nc3;
+  po.resort |= key_cell[N + n] != c1;  // grid-bank cells never change
+  key_cell[n] = c0;
+  key_cell[N + n] = c1;
+  const uint32_t rk0 = atomicAdd(&cell_count[c0], 1u), rk1 = atomicAdd(&cell_count[c1], 1u);
+  if (key_rank) {  // positions inside the cells for the ranked scatter (non-deterministic mode)
+    key_rank[n] = rk0;
+    key_rank[N + n] = rk1;
+  }
+  po.local_min = fminf(po.local_min, fminf(on0 ? bl0 : INFINITY, on1 ? bl1 : INFINITY));
+  const float4 r0 = key_ref[n], r1 = key_ref[N + n];
+  const float ex = px - r1.x, ey = py - r1.y, ez = pz - r1.z;
+  if (on1) {
+    po.moved |= fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > skin2;
+    po.moved |= !(bl1 <= r1.w * (1.0f + mu) && bl1 * (1.0f + mu) >= r1.w);
+  }
+  if (on0) po.moved |= !(bl0 <= r0.w * (1.0f + mu) && bl0 * (1.0f + mu) >= r0.w);
+}
+
+__device__ __forceinline__ void prep_key_flush(const PrepOut& po, DevScalars* ds) {
+  float local_min = po.local_min;
+  // bl > 0: the IEEE bit pattern orders like the value
+  for (int o = 16; o > 0; o >>= 1) local_min = fminf(local_min, __shfl_xor_sync(~0u, local_min, o));
+  if ((threadIdx.x & 31) == 0 && local_min < INFINITY)
+    atomicMin(reinterpret_cast<unsigned int*>(&ds->bl_min), __float_as_uint(local_min));
+  if (__any_sync(~0u, po.moved) && (threadIdx.x & 31) == 0) atomicOr(&ds->lists_invalid, 1u);
+  if (__any_sync(~0u, po.resort) && (threadIdx.x & 31) == 0) atomicOr(&ds->keys_resort, 1u);
+}
+
 __global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, float4* __restrict__ key_raw,
                             uint32_t* __restrict__ key_cell, uint32_t* __restrict__ key_rank,
                             uint32_t* __restrict__ cell_count,
                             const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
   const int N = R * R * R;
-  const int NC = R - 1;
-  const float inv_h = (float)((R - 1) / 2.0);
-  float local_min = INFINITY;
-  bool moved = false, resort = false;
+  PrepOut po;
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    const int x = n % R, y = (n / R) % R, z = n / (R * R);
-    // lattice k(i) = float32(-1 + 2 i/(R-1))  (reading R-2), evaluated in double
-    const float kx = (float)(-1.0 + 2.0 * x / (double)(R - 1));
-    const float ky = (float)(-1.0 + 2.0 * y / (double)(R - 1));
-    const float kz = (float)(-1.0 + 2.0 * z / (double)(R - 1));
-    const float* t = theta + (size_t)n * EF_NCH;
-    const float bl0 = expf(t[0]) * EF_LOG2E;
-    const float bl1 = expf(t[8]) * EF_LOG2E;
-    const bool on0 = banks & 1, on1 = banks & 2;
-    // a bank the variant does not have (NEXT-4: O only / O^Delta only): its keys sit far away
-    // (weight exactly 0) in the sentinel cell n_cells that no enumeration visits
-    constexpr float FAR = 1e15f;
-    const float px = on1 ? kx + t[5] : FAR, py = on1 ? ky + t[6] : FAR, pz = on1 ? kz + t[7] : FAR;
-    const float gx = on0 ? kx : FAR, gy = on0 ? ky : FAR, gz = on0 ? kz : FAR;
-    key_raw[2 * n] = make_float4(gx, gy, gz, bl0);
-    key_raw[2 * n + 1] = make_float4(t[1], t[2], t[3], t[4]);
-    key_raw[2 * (N + n)] = make_float4(px, py, pz, bl1);
-    key_raw[2 * (N + n) + 1] = make_float4(t[9], t[10], t[11], t[12]);
-    const uint32_t nc3 = (uint32_t)(NC * NC * NC);
-    const uint32_t c0 = on0 ? (uint32_t)((cell_clamp(kz, inv_h, NC) * NC + cell_clamp(ky, inv_h, NC)) * NC +
-                                         cell_clamp(kx, inv_h, NC))
-                            : nc3;
-    const uint32_t c1 = on1 ? (uint32_t)((cell_clamp(pz, inv_h, NC) * NC + cell_clamp(py, inv_h, NC)) * NC +
-                                         cell_clamp(px, inv_h, NC))
-                            : nc3;
-    resort |= key_cell[N + n] != c1;  // grid-bank cells never change
-    key_cell[n] = c0;
-    key_cell[N + n] = c1;
-    const uint32_t rk0 = atomicAdd(&cell_count[c0], 1u), rk1 = atomicAdd(&cell_count[c1], 1u);
-    if (key_rank) {  // positions inside the cells for the ranked scatter (non-deterministic mode)
-      key_rank[n] = rk0;
-      key_rank[N + n] = rk1;
-    }
-    local_min = fminf(local_min, fminf(on0 ? bl0 : INFINITY, on1 ? bl1 : INFINITY));
-    const float4 r0 = key_ref[n], r1 = key_ref[N + n];
-    const float ex = px - r1.x, ey = py - r1.y, ez = pz - r1.z;
-    if (on1) {
-      moved |= fmaf(ex, ex, fmaf(ey, ey, ez * ez)) > skin2;
-      moved |= !(bl1 <= r1.w * (1.0f + mu) && bl1 * (1.0f + mu) >= r1.w);
-    }
-    if (on0) moved |= !(bl0 <= r0.w * (1.0f + mu) && bl0 * (1.0f + mu) >= r0.w);
+    float t[EF_NCH];
+#pragma unroll
+    for (int c = 0; c < EF_NCH; ++c) t[c] = theta[(size_t)n * EF_NCH + c];
+    prep_key_node(n, t, R, banks, key_raw, key_cell, key_rank, cell_count, key_ref, skin2, mu, po);
   }
-  // bl > 0: the IEEE bit pattern orders like the value
-  for (int o = 16; o > 0; o >>= 1) local_min = fminf(local_min, __shfl_xor_sync(~0u, local_min, o));
-  if ((threadIdx.x & 31) == 0 && local_min < INFINITY)
-    atomicMin(reinterpret_cast<unsigned int*>(&ds->bl_min), __float_as_uint(local_min));
-  if (__any_sync(~0u, moved) && (threadIdx.x & 31) == 0) atomicOr(&ds->lists_invalid, 1u);
-  if (__any_sync(~0u, resort) && (threadIdx.x & 31) == 0) atomicOr(&ds->keys_resort, 1u);
+  prep_key_flush(po, ds);
+}
+
+// S6 + S0 fused (13-channel layout): thread per node, AdamW over its channels (adamw_elem: the
+// op order of k_adamw), then its key records from the updated theta (prep_key_node). The step
+// counter advances as in k_adamw (the last block to finish).
+__global__ void k_adamw_keys(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
+                             float* __restrict__ v, const AdamWConst hc, int R, int banks,
+                             float4* __restrict__ key_raw, uint32_t* __restrict__ key_cell,
+                             uint32_t* __restrict__ key_rank, uint32_t* __restrict__ cell_count,
+                             const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
+  __shared__ AdamWScal c;
+  __shared__ unsigned long long t_next;
+  if (threadIdx.x == 0) {
+    t_next = ds->adam_t + 1;
+    c = adamw_scal(hc, t_next);
+  }
+  __syncthreads();
+  const AdamWScal cs = c;
+  const int N = R * R * R;
+  PrepOut po;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float t[EF_NCH];
+    const size_t b = (size_t)n * EF_NCH;
+#pragma unroll
+    for (int ch = 0; ch < EF_NCH; ++ch) {
+      float p = theta[b + ch];
+      if (!((hc.frozen_mask >> ch) & 1u)) {  // degree 0: g channels stay exactly 0
+        float mi = m[b + ch], vi = v[b + ch];
+        p = adamw_elem(p, grad[b + ch], mi, vi, (hc.decay_mask >> ch) & 1u, cs);
+        theta[b + ch] = p;
+        m[b + ch] = mi;
+        v[b + ch] = vi;
+      }
+      t[ch] = p;
+    }
+    prep_key_node(n, t, R, banks, key_raw, key_cell, key_rank, cell_count, key_ref, skin2, mu, po);
+  }
+  prep_key_flush(po, ds);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ds->adam_done, 1u) == gridDim.x - 1) {
+      ds->adam_t = t_next;
+      ds->adam_done = 0;
+    }
+  }
+}
+
+int launch_adamw_keys(float* theta, const float* grad, float* m, float* v, const AdamWConst& hc, int R, int banks,
+                      float4* key_raw, uint32_t* key_cell, uint32_t* key_rank, uint32_t* cell_count,
+                      const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s) {
+  const int N = R * R * R;
+  int blocks = (N + 63) / 64;  // 64 threads per block: every SM busy at 32^3
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_adamw_keys<<<blocks, 64, 0, s>>>(theta, grad, m, v, hc, R, banks, key_raw, key_cell, key_rank, cell_count,
+                                     key_ref, skin2, mu, ds);
+  return 1;
 }
 
 int launch_prep_keys(const float* theta, int R, int banks, float4* key_raw, uint32_t* key_cell, uint32_t* key_rank,
