@@ -238,7 +238,9 @@ def run_ours(args, rank, world, local_rank, nccl):
         shapes = [synth.make_shape(shape_name)]
         J_global = edist.global_batch(J, world)
     shape = shapes[0]
-    reduce_grad = world > 1 and S == 1
+    # EFUNC_BENCH_NCCL1=1 at world 1: the N > 1 step (NCCL all-reduce captured in the step graph)
+    # on one rank, a code-path check of the collective's capture (not a multi-GPU measurement)
+    reduce_grad = (world > 1 or nccl) and S == 1
 
     # input pool (> L2); each rank draws its own points
     pool = max(2, min(POOL, int(np.ceil(160e6 / (16 * J * S)))))
@@ -573,6 +575,14 @@ def main():
     shared = os.environ.get("EFUNC_BENCH_SHARED_GPU") == "1"
     dev = local_rank
     nccl = False
+    if world == 1 and os.environ.get("EFUNC_BENCH_NCCL1") == "1":
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        nccl = True
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -587,7 +597,7 @@ def main():
     try:
         run_ours(args, rank, world, dev, nccl)
     finally:
-        if world > 1:
+        if world > 1 or nccl:
             import torch.distributed as dist
             dist.destroy_process_group()
 

@@ -110,3 +110,27 @@ def test_bench_gpus_2_spawns_ranks_without_torchrun():
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
     assert d["config"]["global_batch"] == 2 * 4096
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def test_bench_nccl_allreduce_captured_in_step_graph_single_rank():
+    """EFUNC_BENCH_NCCL1=1: bench.py's N > 1 step (the NCCL all-reduce of the gradient captured
+    inside each batch's CUDA graph) on a one-rank NCCL group: checks that the collective captures
+    and replays with this torch/NCCL, which the multi-GPU scaling run depends on."""
+    env = dict(os.environ, EFUNC_BENCH_NCCL1="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()),
+               EFUNC_BENCH_WATCHDOG="150")
+    env.pop("WORLD_SIZE", None)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        with open(os.path.join(td, "out"), "w") as fo, open(os.path.join(td, "err"), "w") as fe:
+            rc = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "5",
+                                 "--warmup", "3", "--no-cpu-baseline"], env=env, stdout=fo, stderr=fe,
+                                timeout=300, cwd=ROOT).returncode
+        out = open(os.path.join(td, "out")).read()
+        err = open(os.path.join(td, "err")).read()
+    assert rc == 0, err[-3000:]
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out
+    d = json.loads(lines[0])
+    assert d["config"]["launch"] == "cuda-graph per step (NCCL all-reduce inside)", d["config"]
+    assert d["config"]["collective"].startswith("NCCL all_reduce")
+    assert d["value"] > 0
