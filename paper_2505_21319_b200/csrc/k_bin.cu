@@ -99,16 +99,21 @@ __global__ void k_prep_keys(const float* __restrict__ theta, int R, int banks, f
   prep_key_flush(po, ds);
 }
 
-// S6 + S0 fused (13-channel layout): thread per node, AdamW over its channels (adamw_elem: the
-// op order of k_adamw), then its key records from the updated theta (prep_key_node). The step
-// counter advances as in k_adamw (the last block to finish).
-__global__ void k_adamw_keys(float* __restrict__ theta, const float* __restrict__ grad, float* __restrict__ m,
-                             float* __restrict__ v, const AdamWConst hc, int R, int banks,
-                             float4* __restrict__ key_raw, uint32_t* __restrict__ key_cell,
-                             uint32_t* __restrict__ key_rank, uint32_t* __restrict__ cell_count,
-                             const float4* __restrict__ key_ref, float skin2, float mu, DevScalars* ds) {
+// S6 + S0 fused (13-channel layout): a block takes a tile of AK_NODES nodes; its threads run AdamW
+// over the tile's AK_NODES x 13 elements in element order (coalesced; adamw_elem: the op order of
+// k_adamw) and stage the updated theta in shared memory, then one thread per node writes the
+// node's key records (prep_key_node). The step counter advances as in k_adamw (the last block).
+constexpr int AK_NODES = 64, AK_THREADS = 128;
+__global__ void __launch_bounds__(AK_THREADS) k_adamw_keys(float* __restrict__ theta, const float* __restrict__ grad,
+                                                           float* __restrict__ m, float* __restrict__ v,
+                                                           const AdamWConst hc, int R, int banks,
+                                                           float4* __restrict__ key_raw, uint32_t* __restrict__ key_cell,
+                                                           uint32_t* __restrict__ key_rank, uint32_t* __restrict__ cell_count,
+                                                           const float4* __restrict__ key_ref, float skin2, float mu,
+                                                           DevScalars* ds) {
   __shared__ AdamWScal c;
   __shared__ unsigned long long t_next;
+  __shared__ float tile[AK_NODES * EF_NCH];
   if (threadIdx.x == 0) {
     t_next = ds->adam_t + 1;
     c = adamw_scal(hc, t_next);
@@ -117,22 +122,26 @@ __global__ void k_adamw_keys(float* __restrict__ theta, const float* __restrict_
   const AdamWScal cs = c;
   const int N = R * R * R;
   PrepOut po;
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float t[EF_NCH];
-    const size_t b = (size_t)n * EF_NCH;
-#pragma unroll
-    for (int ch = 0; ch < EF_NCH; ++ch) {
-      float p = theta[b + ch];
+  for (int n0 = blockIdx.x * AK_NODES; n0 < N; n0 += gridDim.x * AK_NODES) {
+    const int nn = min(AK_NODES, N - n0);
+    const size_t e0 = (size_t)n0 * EF_NCH;
+    for (int i = threadIdx.x; i < nn * EF_NCH; i += AK_THREADS) {
+      const int ch = i % EF_NCH;
+      float p = theta[e0 + i];
       if (!((hc.frozen_mask >> ch) & 1u)) {  // degree 0: g channels stay exactly 0
-        float mi = m[b + ch], vi = v[b + ch];
-        p = adamw_elem(p, grad[b + ch], mi, vi, (hc.decay_mask >> ch) & 1u, cs);
-        theta[b + ch] = p;
-        m[b + ch] = mi;
-        v[b + ch] = vi;
+        float mi = m[e0 + i], vi = v[e0 + i];
+        p = adamw_elem(p, grad[e0 + i], mi, vi, (hc.decay_mask >> ch) & 1u, cs);
+        theta[e0 + i] = p;
+        m[e0 + i] = mi;
+        v[e0 + i] = vi;
       }
-      t[ch] = p;
+      tile[i] = p;
     }
-    prep_key_node(n, t, R, banks, key_raw, key_cell, key_rank, cell_count, key_ref, skin2, mu, po);
+    __syncthreads();
+    if (threadIdx.x < nn)
+      prep_key_node(n0 + threadIdx.x, &tile[threadIdx.x * EF_NCH], R, banks, key_raw, key_cell, key_rank, cell_count,
+                    key_ref, skin2, mu, po);
+    __syncthreads();
   }
   prep_key_flush(po, ds);
   __syncthreads();
@@ -149,9 +158,9 @@ int launch_adamw_keys(float* theta, const float* grad, float* m, float* v, const
                       float4* key_raw, uint32_t* key_cell, uint32_t* key_rank, uint32_t* cell_count,
                       const float4* key_ref, float skin2, float mu, DevScalars* ds, cudaStream_t s) {
   const int N = R * R * R;
-  int blocks = (N + 63) / 64;  // 64 threads per block: every SM busy at 32^3
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  k_adamw_keys<<<blocks, 64, 0, s>>>(theta, grad, m, v, hc, R, banks, key_raw, key_cell, key_rank, cell_count,
+  int blocks = (N + AK_NODES - 1) / AK_NODES;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_adamw_keys<<<blocks, AK_THREADS, 0, s>>>(theta, grad, m, v, hc, R, banks, key_raw, key_cell, key_rank, cell_count,
                                      key_ref, skin2, mu, ds);
   return 1;
 }

@@ -515,12 +515,11 @@ constexpr uint32_t IT_NORMAL = 0, IT_ENUM = 1, IT_SKIP = 2;
 // Part 1 of a work item: the box and its candidate ids (into Lw, or the all-keys list in dense
 // mode). Returns IT_NORMAL with L, wn, o set; IT_ENUM for an overflowed brick (fit_item_enum
 // builds its own chunks); IT_SKIP for out-of-domain items (queued for the split kernels).
-__device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint32_t item, uint32_t* Lw,
+__device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint32_t item, const int4 it, uint32_t* Lw,
                                                    const uint32_t*& L, uint32_t& wn, float3& o) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
   const int lane = threadIdx.x & 31;
-  const int4 it = A.items[item];
   const int nact = it.y;
   const bool dense = F.iota != nullptr;  // cutoff_T = inf: every key is a candidate, no lists
   if (F.pre) {  // k_fit_lists built this item's candidate ids (unless it had no list / no room)
@@ -570,12 +569,11 @@ __device__ __forceinline__ uint32_t fit_item_build(const FitArgs& F, const uint3
 }
 
 // Part 2 of a work item: forward, loss, backward over the candidate ids L[0 .. wn).
-__device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_t item, FitSmem& S,
+__device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_t item, const int4 it, FitSmem& S,
                                                  const uint32_t* L, const uint32_t wn, const float3 o) {
   const FwdArgs& A = F.f;
   const KeysView& kv = A.kv;
   const int lane = threadIdx.x & 31;
-  const int4 it = A.items[item];
   const int nact = it.y;
   const bool act = lane < nact;
   const int64_t js = (int64_t)it.x + lane;
@@ -685,13 +683,15 @@ __device__ __forceinline__ void fit_item_compute(const FitArgs& F, const uint32_
 #endif
 }
 
+// the item record is loaded once here and handed to both parts
 __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, FitSmem& S, uint32_t* Lw) {
   const uint32_t* L;
   uint32_t wn;
   float3 o;
-  const uint32_t t = fit_item_build(F, item, Lw, L, wn, o);
+  const int4 it = F.f.items[item];
+  const uint32_t t = fit_item_build(F, item, it, Lw, L, wn, o);
   if (t == IT_ENUM) fit_item_enum(F, item, S, Lw);
-  else if (t == IT_NORMAL) fit_item_compute(F, item, S, L, wn, o);
+  else if (t == IT_NORMAL) fit_item_compute(F, item, it, S, L, wn, o);
 }
 
 __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(const FitArgs F) {
@@ -1307,7 +1307,7 @@ __device__ __forceinline__ void fit_item_tc_any(const FitArgs& F, const uint32_t
   const uint32_t* L;
   uint32_t wn;
   float3 o;
-  const uint32_t ty = fit_item_build(F, item, Lw, L, wn, o);
+  const uint32_t ty = fit_item_build(F, item, F.f.items[item], Lw, L, wn, o);
   if (ty == IT_ENUM) fit_item_enum(F, item, S2, Lw);
   else if (ty == IT_NORMAL) fit_item_tc(F, item, S, L, wn, o);
 }

@@ -150,3 +150,21 @@ def test_dense_eikonal_fused_parity(R, J):
     assert abs(float(L.item()) - (Lm + Le)) <= 1e-5 * (Lm + Le)
     check_grads(g.cpu().numpy(), orc.backward(th, R, q, f, r, h))
     assert m.stats()["candidate_pairs"] == J * 2 * R ** 3
+
+
+def test_tensor_core_fit_path_parity():
+    """The A/B tensor-core fit kernel (k_fit_tc: mma.sync, 3xTF32 contractions; EFUNC_FIT_TC=1, read
+    once per process) on the fused-path oracle checks: C1 parity, the full-density R = 32 batch and
+    the deterministic bitwise test, in a child process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EFUNC_FIT_TC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        os.path.join(root, "tests", "test_gpu_bench_configs.py"),
+                        "-k", "fused_parity_c1 or full_density_r32 and not eik or deterministic_fit_bitwise"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and " failed" not in r.stdout
