@@ -1315,6 +1315,7 @@ __device__ __forceinline__ void fit_item_tc_any(const FitArgs& F, const uint32_t
 #ifndef TC_MIN_BLOCKS
 #define TC_MIN_BLOCKS 4
 #endif
+static_assert(148 * TC_MIN_BLOCKS * FT_WARPS <= SCRATCH_WARPS, "one scratch slot per warp");
 __global__ void __launch_bounds__(32 * FT_WARPS, TC_MIN_BLOCKS) k_fit_tc(const FitArgs F) {
   __shared__ TcSmem smem[FT_WARPS];
   __shared__ FitSmem smem2[FT_WARPS];  // the overflowed-brick path (fit_item_enum)
