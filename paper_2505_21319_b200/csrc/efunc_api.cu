@@ -213,11 +213,14 @@ int variant_channels(int variant, int degree, ef::VarLayout* L) {
 }
 
 // the per-rebuild counters k_prep_keys / k_adamw_keys accumulate into
+// (one fill launch; lists_invalid starts every rebuild at force, so no reset is needed after it)
 efunc_status reset_key_counters(efunc_t* h, cudaStream_t s, int force) {
-  CK(cudaMemsetAsync(h->cell_count, 0, sizeof(uint32_t) * (h->n_cells + 1), s));
-  CK(cudaMemsetAsync(&h->ds->bl_min, 0x7f, sizeof(float), s));  // 3.39e38
-  if (force) CK(cudaMemsetAsync(&h->ds->lists_invalid, 1, sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(&h->ds->keys_resort, force ? 1 : 0, sizeof(uint32_t), s));
+  FillSegs f;
+  f.add(h->cell_count, sizeof(uint32_t) * (h->n_cells + 1), 0u);
+  f.add(&h->ds->bl_min, sizeof(float), 0x7f7f7f7fu);  // 3.39e38
+  f.add(&h->ds->lists_invalid, sizeof(uint32_t), force ? 1u : 0u);
+  f.add(&h->ds->keys_resort, sizeof(uint32_t), force ? 1u : 0u);
+  h->launches += launch_fill_segs(f, s);
   return EFUNC_OK;
 }
 
@@ -246,7 +249,6 @@ efunc_status rebuild_keys(efunc_t* h, cudaStream_t s, int force = 0, int prepped
   h->launches += launch_brick_lists(keys_view(h), h->bg, cutoff_log2(h->cfg), h->bl_pool, h->bl_pool_cap,
                                     h->bl_off, h->bl_n, h->ds, h->scratch, s);
   h->launches += launch_list_snapshot(h->key_raw, h->key_ref, h->n_keys, h->ds, s);
-  CK(cudaMemsetAsync(&h->ds->lists_invalid, 0, sizeof(uint32_t), s));
   CK(cudaGetLastError());
   h->have_fwd = 0;
   return EFUNC_OK;
@@ -360,13 +362,16 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   RET(ensure_queries(h, J));
   const uint32_t nb = h->bg.n_codes;             // bricks
   const uint32_t nbins = nb * h->bg.qsub + 1;    // sub-cell bins + the out-of-domain bin
-  CK(cudaMemsetAsync(h->bin_count, 0, sizeof(uint32_t) * (nbins + 1), s));
+  FillSegs fz;  // the bin histogram and the per-forward counters, one fill launch
+  fz.add(h->bin_count, sizeof(uint32_t) * (nbins + 1), 0u);
   // fused path: each query's rank inside its bin comes from the histogram's atomic (no fill
   // counters, no second atomic pass); the other paths sort stably instead
   const bool ranked = with_mh && !h->cfg.deterministic;
   static_assert(offsetof(DevScalars, kept_pairs_offset) + sizeof(unsigned long long) == sizeof(DevScalars),
                 "the per-forward counters end DevScalars");
-  CK(cudaMemsetAsync(&h->ds->overflow_items, 0, sizeof(DevScalars) - offsetof(DevScalars, overflow_items), s));
+  static_assert(offsetof(DevScalars, overflow_items) % 4 == 0 && sizeof(DevScalars) % 4 == 0, "u32 fill");
+  fz.add(&h->ds->overflow_items, sizeof(DevScalars) - offsetof(DevScalars, overflow_items), 0u);
+  h->launches += launch_fill_segs(fz, s);
   h->launches += launch_query_bins(q, o_used, J, h->bg, h->NC, h->inv_h, h->q_bin, h->bin_count,
                                    ranked ? h->q_tmp : nullptr, h->ds, s);
   h->launches += launch_scan_u32(h->bin_count, h->bin_start, nbins + 1, h->scan_tmp, s);
@@ -707,8 +712,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   h->launches += launch_forward_slow(a, eik, s);
   BwdArgs b = bwd_args(h, nullptr, nullptr, grad, eik);
   b.list = h->slow_items;
-  b.list_n = &h->ds->slow_n;
-  CK(cudaMemsetAsync(&h->ds->bwd_next, 0, sizeof(uint32_t), s));
+  b.list_n = &h->ds->slow_n;  // (bwd_next is still 0 from prep_queries: k_fit and k_forward use other cursors)
   if (det) {  // fixed point with the unit k_det_bound set, then folded into grad
     h->launches += launch_backward_list_det(b, s);
     h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);

@@ -298,6 +298,18 @@ __device__ __forceinline__ float adamw_elem(float p, const float g, float& mi, f
 int launch_mean_shift(float* theta, int R, const float* surf, int64_t N, float bw,
                       cudaStream_t s);
 int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s);
+struct FillSeg {
+  uint32_t* p;
+  uint32_t n;  // u32 words
+  uint32_t v;
+};
+struct FillSegs {
+  static constexpr int MAX = 4;
+  FillSeg s[MAX];
+  int k = 0;
+  void add(void* p, size_t bytes, uint32_t v) { s[k++] = FillSeg{static_cast<uint32_t*>(p), (uint32_t)(bytes / 4), v}; }
+};
+int launch_fill_segs(const FillSegs& f, cudaStream_t s);
 int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s);
 // NEXT-4 (k_var.cu): variant layouts and the degree-2 forward / backward
 int launch_var_unpack(const float* tv, int n, const VarLayout& L, float* t13, float* tH, cudaStream_t s);

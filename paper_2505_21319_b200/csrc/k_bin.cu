@@ -526,6 +526,28 @@ int launch_fill_zero_f32(float* p, int64_t n, cudaStream_t s) {
   return 1;
 }
 
+// Several u32 fills in one launch (replaces a run of cudaMemsetAsync calls: a memset node costs a
+// few microseconds of graph-node gap each, a kernel node ~0.3 us)
+__global__ void k_fill_segs(const FillSegs f) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+#pragma unroll
+  for (int i = 0; i < FillSegs::MAX; ++i) {
+    if (i >= f.k) break;
+    const FillSeg g = f.s[i];
+    for (uint32_t j = t; j < g.n; j += stride) g.p[j] = g.v;
+  }
+}
+
+int launch_fill_segs(const FillSegs& f, cudaStream_t s) {
+  uint32_t mx = 0;
+  for (int i = 0; i < f.k; ++i) mx = mx > f.s[i].n ? mx : f.s[i].n;
+  if (mx == 0) return 0;
+  uint32_t blocks = (mx + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  k_fill_segs<<<blocks, 256, 0, s>>>(f);
+  return 1;
+}
+
 // ------------------------------------------------------------------------------ work items
 // A work item is a balanced run of <= QW queries of one brick (its qsub half-cell bins are
 // contiguous in the sorted stream): ceil(n/QW) items per brick. The brick field is the brick's

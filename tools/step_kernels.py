@@ -19,6 +19,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", default="c2")
 p.add_argument("--steps", type=int, default=5)
 p.add_argument("--split", action="store_true", help="forward + backward instead of forward_backward")
+p.add_argument("--graph", action="store_true", help="replay one CUDA graph per batch (as bench.py)")
 a = p.parse_args()
 J = (1 << 20) if a.config == "c2" else (1 << 22)
 loss = ef.LOSS_MSE if a.config == "c2" else ef.LOSS_MSE_EIKONAL
@@ -45,9 +46,27 @@ def step(i):
 for i in range(10):
     step(i)
 torch.cuda.synchronize()
+run = step
+if a.graph:
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    graphs = []
+    with torch.cuda.stream(cap):
+        for i in range(4):
+            step(i)
+    torch.cuda.synchronize()
+    for i in range(4):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            step(i)
+        graphs.append(g)
+    run = lambda i: graphs[i % 4].replay()  # noqa: E731
+    for i in range(8):
+        run(i)
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for i in range(a.steps):
-        step(i)
+        run(i)
     torch.cuda.synchronize()
 ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 ev.sort(key=lambda e: e.time_range.start)
