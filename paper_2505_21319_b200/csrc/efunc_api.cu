@@ -395,9 +395,11 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   if (nb + 2 <= EF_ITEMS_FUSED_MAX) {  // one single-CTA pass
     h->launches += launch_items_fused(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
   } else {
-    h->launches += launch_items_count(h->bin_start, nb, h->bg.qsub, h->item_cnt, s);
-    h->launches += launch_scan_u32(h->item_cnt, h->item_off, nb + 2, h->scan_tmp, s);
-    h->launches += launch_items_write(h->bin_start, nb, h->bg.qsub, h->item_off, h->items, s);
+    // cost classes need the brick lists (cutoff mode): heavy items first, the lightest last
+    const uint32_t* bl_n = std::isinf(cutoff_log2(h->cfg)) ? nullptr : h->bl_n;
+    h->launches += launch_items_count(h->bin_start, nb, h->bg.qsub, bl_n, h->ds, h->item_cnt, s);
+    h->launches += launch_scan_u32(h->item_cnt, h->item_off, ITEMS_N_AT(nb) + 1, h->scan_tmp, s);
+    h->launches += launch_items_write(h->bin_start, nb, h->bg.qsub, bl_n, h->ds, h->item_off, h->items, s);
   }
   const int64_t items = (J + IQ - 1) / IQ + nb + 1;  // launch bound; kernels read the count
   h->fwd_items_bound = items;
@@ -407,7 +409,7 @@ efunc_status prep_queries(efunc_t* h, const float* q, const float* o_used, int64
   a.perm = h->perm;
   a.J = J;
   a.items = h->items;
-  a.n_items = h->item_off + (nb + 1);
+  a.n_items = h->item_off + ITEMS_N_AT(nb);
   a.T_l = cutoff_log2(h->cfg);
   a.loss_kind = kind;
   const int64_t Jg = (loss && loss->J_global > 0) ? loss->J_global : J;
@@ -489,7 +491,7 @@ BwdArgs bwd_args(efunc_t* h, const float* dL_dO, const float* dL_dG, float* grad
   b.perm = h->perm;
   b.J = h->fwd_J;
   b.items = h->items;
-  b.n_items = h->item_off + (h->bg.n_codes + 1);
+  b.n_items = h->item_off + ITEMS_N_AT(h->bg.n_codes);
   b.T_l = cutoff_log2(h->cfg);
   b.gpad = h->gpad;
   b.gfix = h->gfix;
@@ -546,7 +548,7 @@ FwdArgs saved_fwd_args(efunc_t* h) {
   a.perm = h->perm;
   a.J = h->fwd_J;
   a.items = h->items;
-  a.n_items = h->item_off + (h->bg.n_codes + 1);
+  a.n_items = h->item_off + ITEMS_N_AT(h->bg.n_codes);
   a.T_l = cutoff_log2(h->cfg);
   a.rec = h->rec;
   a.wl_pool = h->wl_pool;
@@ -1502,7 +1504,7 @@ efunc_status efunc_get_stats(efunc_t* h, efunc_stats* out, void* stream) {
   CK(cudaMemcpy(&d, h->ds, sizeof(d), cudaMemcpyDeviceToHost));
   out->J = h->fwd_J;
   uint32_t ni = 0;
-  if (h->fwd_J > 0) CK(cudaMemcpy(&ni, h->item_off + (h->bg.n_codes + 1), sizeof(ni), cudaMemcpyDeviceToHost));
+  if (h->fwd_J > 0) CK(cudaMemcpy(&ni, h->item_off + ITEMS_N_AT(h->bg.n_codes), sizeof(ni), cudaMemcpyDeviceToHost));
   out->items = ni;
   out->candidate_pairs = (double)d.cand_pairs;
   out->kept_pairs = (double)d.kept_pairs;

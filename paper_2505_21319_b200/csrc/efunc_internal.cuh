@@ -229,11 +229,17 @@ int launch_gather_queries_mh(const KeysView& kv, const uint32_t* order, const fl
                              float4* qs, int* perm, float* qmh, float* qf0, cudaStream_t s);
 int launch_scatter_only(const uint32_t* bin, uint32_t n, const uint32_t* bin_start, uint32_t* fill,
                         uint32_t* out_idx, cudaStream_t s, const uint32_t* gate = nullptr);
-int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s);
+int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* bl_n,
+                       const DevScalars* ds, uint32_t* cnt, cudaStream_t s);
+int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* bl_n,
+                       const DevScalars* ds, const uint32_t* off, int4* items, cudaStream_t s);
 int launch_items_fused(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* item_off, int4* items,
                        cudaStream_t s);
-int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
-                       cudaStream_t s);
+// work items in cost classes (k_items_count): item_off[ITEMS_N_AT(nb)] = the number of items
+#ifndef EF_ITEM_CLASSES
+#define EF_ITEM_CLASSES 3
+#endif
+#define ITEMS_N_AT(nb) (EF_ITEM_CLASSES * ((nb) + 1))
 int launch_forward(const FwdArgs& a, int want_g, int64_t n_items, cudaStream_t s);
 int launch_forward_slow(const FwdArgs& a, int want_g, cudaStream_t s);
 int launch_backward(const BwdArgs& a, int64_t n_items, cudaStream_t s);

@@ -559,27 +559,50 @@ __device__ __forceinline__ void brick_range(const uint32_t* bin_start, uint32_t 
   n = e - s;
 }
 
+// Work items in EF_ITEM_CLASSES cost classes, in one exclusive scan: slot k (nb + 1) + c holds brick
+// c's item count if the brick is in class k, else 0; slot K (nb + 1) = 0 (-> the item count).
+// Class 0: the brick list is longer than the average (or overflowed, or the out-of-domain bin);
+// class k < K - 1: longer than 2^-k of the average; the last class: the rest. Heavy items come
+// first and the lightest (volume) items last, each class in Morton order, so the persistent
+// kernels' tail is made of short items (bl_n = null: everything in class 0).
+__device__ __forceinline__ uint32_t item_class(const uint32_t* bl_n, const DevScalars* ds, uint32_t c, uint32_t nb) {
+  if (!bl_n || c == nb) return 0;
+  const uint32_t l = bl_n[c];
+  if (l == BL_OVERFLOW) return 0;
+  const float r = (float)l * (float)nb / fmaxf((float)ds->pool_used, 1.0f);  // list length / average
+  uint32_t k = 0;
+  float t = 1.0f;
+  while (k + 1 < (uint32_t)EF_ITEM_CLASSES && !(r > t)) {
+    ++k;
+    t *= 0.5f;
+  }
+  return k;
+}
+
 __global__ void k_items_count(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t qsub,
-                              uint32_t* __restrict__ cnt) {
+                              const uint32_t* __restrict__ bl_n, const DevScalars* ds, uint32_t* __restrict__ cnt) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb + 1; c += gridDim.x * blockDim.x) {
     if (c == nb + 1) {
-      cnt[c] = 0;
+      cnt[ITEMS_N_AT(nb)] = 0;
       continue;
     }
     uint32_t s, n;
     brick_range(bin_start, c, nb, qsub, s, n);
-    cnt[c] = (n + IQ - 1) / IQ;
+    const uint32_t m = (n + IQ - 1) / IQ;
+    const uint32_t k = item_class(bl_n, ds, c, nb);
+    for (uint32_t j = 0; j < (uint32_t)EF_ITEM_CLASSES; ++j) cnt[j * (nb + 1) + c] = j == k ? m : 0u;
   }
 }
 
 __global__ void k_items_write(const uint32_t* __restrict__ bin_start, uint32_t nb, uint32_t qsub,
+                              const uint32_t* __restrict__ bl_n, const DevScalars* ds,
                               const uint32_t* __restrict__ off, int4* __restrict__ items) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nb; c += gridDim.x * blockDim.x) {
     uint32_t s, n;
     brick_range(bin_start, c, nb, qsub, s, n);
     if (n == 0) continue;
     const uint32_t m = (n + IQ - 1) / IQ;
-    const uint32_t o = off[c];
+    const uint32_t o = off[item_class(bl_n, ds, c, nb) * (nb + 1) + c];
     const int brick = (c == nb) ? -1 : (int)c;
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t a = (uint32_t)(((uint64_t)i * n) / m), b = (uint32_t)(((uint64_t)(i + 1) * n) / m);
@@ -604,7 +627,8 @@ __global__ void __launch_bounds__(1024) k_items_fused(const uint32_t* __restrict
     }
     uint32_t total;
     const uint32_t off = block_excl_scan_1024(m, s_w, &total) + carry;
-    if (c <= nb + 1) item_off[c] = off;  // item_off[nb + 1]: the number of items
+    if (c <= nb + 1) item_off[c] = off;
+    if (c == nb + 1) item_off[ITEMS_N_AT(nb)] = off;  // the number of items
     const int brick = (c == nb) ? -1 : (int)c;
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t a = (uint32_t)(((uint64_t)i * n) / m), b = (uint32_t)(((uint64_t)(i + 1) * n) / m);
@@ -621,14 +645,15 @@ int launch_items_fused(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, ui
   return 1;
 }
 
-int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, uint32_t* cnt, cudaStream_t s) {
-  k_items_count<<<grid_for(nb + 2, 256), 256, 0, s>>>(bin_start, nb, qsub, cnt);
+int launch_items_count(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* bl_n,
+                       const DevScalars* ds, uint32_t* cnt, cudaStream_t s) {
+  k_items_count<<<grid_for(nb + 2, 256), 256, 0, s>>>(bin_start, nb, qsub, bl_n, ds, cnt);
   return 1;
 }
 
-int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* off, int4* items,
-                       cudaStream_t s) {
-  k_items_write<<<grid_for(nb + 1, 128), 128, 0, s>>>(bin_start, nb, qsub, off, items);
+int launch_items_write(const uint32_t* bin_start, uint32_t nb, uint32_t qsub, const uint32_t* bl_n,
+                       const DevScalars* ds, const uint32_t* off, int4* items, cudaStream_t s) {
+  k_items_write<<<grid_for(nb + 1, 128), 128, 0, s>>>(bin_start, nb, qsub, bl_n, ds, off, items);
   return 1;
 }
 
