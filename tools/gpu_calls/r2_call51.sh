@@ -1,0 +1,6 @@
+# k_fit mixed fetch (heavy and light items alternately while both last) vs class order (mix0)
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_configs.py -x -q -k "fused_parity_c1 or full_density or stale or c2_full or dense" > gpurun_out/r2c51_pytest.txt 2>&1
+tail -2 gpurun_out/r2c51_pytest.txt
+for r in 1 2 3; do bash tools/variants.sh --no-cpu-baseline --no-e2e; done > gpurun_out/r2c51_ab.txt 2>&1
+cat gpurun_out/r2c51_ab.txt
