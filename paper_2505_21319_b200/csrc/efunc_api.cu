@@ -1051,8 +1051,10 @@ efunc_status efunc_create(const efunc_config* cfg, const float* theta_host, efun
     CK(dalloc(&h->bin_count, nbins + 1));
     CK(dalloc(&h->bin_start, nbins + 1));
     CK(dalloc(&h->bin_fill, nbins + 1));
-    CK(dalloc(&h->item_cnt, nbins + 1));
-    CK(dalloc(&h->item_off, nbins + 1));
+    // the work-item scan runs over ITEMS_N_AT(nb) + 1 slots (cost classes); qsub >= 8 makes that fit
+    const size_t nitem_slots = std::max(nbins + 1, (size_t)ITEMS_N_AT((size_t)h->bg.n_codes) + 1);
+    CK(dalloc(&h->item_cnt, nitem_slots));
+    CK(dalloc(&h->item_off, nitem_slots));
     RET(ensure_scan_tmp(h, nbins + 1));
     CK(dalloc(&h->gpad, (size_t)h->n_nodes * 16));
     CK(cudaMemset(h->gpad, 0, sizeof(float) * (size_t)h->n_nodes * 16));
