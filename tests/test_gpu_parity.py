@@ -256,6 +256,14 @@ def test_c2_pou_full_size():
     r = synth.rng(43).normal(size=J).astype(np.float32) / J
     g = m.backward(dL_dO=dev(r)).cpu().numpy().astype(np.float64)
     assert abs(g[:, 1].sum() + g[:, 9].sum() - r.astype(np.float64).sum()) <= 1e-4 * np.abs(r).sum()
+    # the fused path (k_fit over the work items in their cost-class order) covers every query once:
+    # O = P(q) at all 2^20 queries, and sum_i dL/dc_i = sum_j r_j = sum_j 2 (P(q_j) - o_j) / J
+    gf, Of, _ = m.forward_backward(dev(q), dev(o), loss=ef.LOSS_MSE, want_O=True, want_loss=False)
+    P = A + q.astype(np.float64) @ B
+    assert nw(Of.cpu().numpy(), P) <= 2e-6
+    rf = 2.0 * (P - o.astype(np.float64)) / J
+    gf = gf.cpu().numpy().astype(np.float64)
+    assert abs(gf[:, 1].sum() + gf[:, 9].sum() - rf.sum()) <= 1e-4 * np.abs(rf).sum()
 
 
 # ----------------------------------------------------------------------------- edge cases
