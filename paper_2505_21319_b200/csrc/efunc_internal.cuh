@@ -313,7 +313,9 @@ struct FillSegs {
   static constexpr int MAX = 4;
   FillSeg s[MAX];
   int k = 0;
-  void add(void* p, size_t bytes, uint32_t v) { s[k++] = FillSeg{static_cast<uint32_t*>(p), (uint32_t)(bytes / 4), v}; }
+  void add(void* p, size_t bytes, uint32_t v) {  // callers add at most MAX segments of whole u32 words
+    if (k < MAX) s[k++] = FillSeg{static_cast<uint32_t*>(p), (uint32_t)(bytes / 4), v};
+  }
 };
 int launch_fill_segs(const FillSegs& f, cudaStream_t s);
 int launch_zero_channels(float* theta, int n_nodes, uint32_t mask, cudaStream_t s);
