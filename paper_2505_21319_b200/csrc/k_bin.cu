@@ -1,10 +1,12 @@
 // k_bin.cu — S0 key prep and S1 binning kernels.
 //
 // S0 (PAPER.md:L456 parameter space, L908 beta = e^s): theta [R^3][13] -> 2R^3 key records
-//    {x,y,z, beta*log2e | c, gx, gy, gz}; cell id per key; per-cell histogram; min beta.
-// S1: deterministic counting sort (histogram -> exclusive scan -> atomic scatter -> per-bin
-//    rank by original index). The final order is a stable sort by bin, independent of the
-//    atomic scatter order, so work items (and therefore every fp32 sum) are reproducible.
+//    {x,y,z, beta*log2e | c, gx, gy, gz}; cell id per key; per-cell histogram; min beta
+//    (k_prep_keys, or k_adamw_keys fused with the S6 AdamW update of the same pass).
+// S1: queries -> (brick, sub-cell) Morton bins, histogram -> exclusive scan -> scatter (rank from
+//    the histogram atomic; the stable radix sort in deterministic mode), then work items of <= 32
+//    queries per brick, laid out in cost classes (heavy bricks first, Morton order within a class).
+// Also the one-launch fills (k_fill_segs) that replace runs of memset nodes in the step graph.
 #include "efunc_internal.cuh"
 
 namespace ef {
