@@ -666,6 +666,7 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
   f.iota = dense ? h->iota : nullptr;
   f.iota_n = h->iota_n;
   f.item_o = h->item_o;
+  f.n_heavy = h->item_off + (h->bg.n_codes + 1);  // the exclusive scan at the first class-1 slot
   f.gfix = det ? h->gfix : nullptr;
   f.umax = &h->ds->umax;
   f.fix_overflow = &h->ds->fix_overflow;

@@ -172,6 +172,7 @@ struct FitArgs {
   uint32_t iota_n;        // their count (2R^3 with both banks)
   int pre;                // 1: k_fit_lists built the items' candidate ids (f.wl_*) and box centres
   float4* item_o;         // [items] box centre of each item (k_fit_lists -> k_fit)
+  const uint32_t* n_heavy;  // items of cost class 0 (the first n_heavy items)
   // deterministic mode: 64-bit fixed-point accumulation (BwdArgs::gfix) with the unit umax * 2^-FIX_BITS,
   // umax an a-priori bound of max_j |r_j| (k_det_bound); null gfix: float reds into gpad
   unsigned long long* gfix;

@@ -694,12 +694,36 @@ __device__ __forceinline__ void fit_item(const FitArgs& F, const uint32_t item, 
   else if (t == IT_NORMAL) fit_item_compute(F, item, it, S, L, wn, o);
 }
 
+#ifndef FT_HSPLIT
+#define FT_HSPLIT 4  // the heavy class is fetched from this many interleaved Morton streams
+#endif
+// fetch g: while g < the heavy-class count, the item at stream g % S, position g / S (the heavy
+// items in flight come from S regions of the surface: fewer concurrent reds on the same keys)
+__device__ __forceinline__ int64_t fetch_item_hsplit(const FitArgs& F) {
+  const uint32_t n = *F.f.n_items, nh = *F.n_heavy, len = (nh + FT_HSPLIT - 1) / FT_HSPLIT;
+  for (;;) {
+    uint32_t g = 0;
+    if ((threadIdx.x & 31) == 0) g = atomicAdd(&F.f.ds->fit_next, 1u);
+    g = __shfl_sync(~0u, g, 0);
+    if (g >= len * FT_HSPLIT) {
+      const uint32_t it = nh + (g - len * FT_HSPLIT);
+      return it < n ? (int64_t)it : -1;
+    }
+    const uint32_t it = (g % FT_HSPLIT) * len + g / FT_HSPLIT;
+    if (it < nh) return (int64_t)it;
+  }
+}
+
 __global__ void __launch_bounds__(32 * FT_WARPS, FT_MIN_WARPS / FT_WARPS) k_fit(const FitArgs F) {
   __shared__ FitSmem smem[FT_WARPS];
   const int w = threadIdx.x >> 5;
   uint32_t* L = F.scratch + (size_t)(blockIdx.x * FT_WARPS + w) * SCRATCH_STRIDE;
   for (;;) {
+#if FT_HSPLIT > 1
+    const int64_t item = F.n_heavy ? fetch_item_hsplit(F) : fetch_item(&F.f.ds->fit_next, F.f.n_items, nullptr, nullptr);
+#else
     const int64_t item = fetch_item(&F.f.ds->fit_next, F.f.n_items, nullptr, nullptr);
+#endif
     if (item < 0) break;
     fit_item(F, (uint32_t)item, smem[w], L);
   }
