@@ -266,18 +266,39 @@ def run_ours(args, rank, world, local_rank, nccl):
     m.mean_shift_init(surf_d)
     hp = ef.AdamW()
     grad = m._grad_zeros()
+    # EFUNC_BENCH_P2P=1 (with an NCCL group): the gradient lives in torch symmetric memory and the
+    # library's fold adds it into every rank's copy (NVLS multimem.red through the multicast
+    # address, else red.v4 over the NVLink peer mappings; efunc_set_grad_peers) between two
+    # symmetric-memory barriers, instead of the NCCL all-reduce after the fold
+    p2p = None
+    if nccl and S == 1 and os.environ.get("EFUNC_BENCH_P2P") == "1":
+        import torch.distributed._symmetric_memory as symm_mem
+        gsym = symm_mem.empty(grad.numel(), device=f"cuda:{dev}", dtype=torch.float32)
+        p2p = symm_mem.rendezvous(gsym, dist.group.WORLD.group_name)
+        m.set_grad_peers(p2p.buffer_ptrs, p2p.multicast_ptr)
+        grad = gsym.view(grad.shape)
+
+    def reduce_pre():  # every rank's copy is zero before any rank adds into it
+        if p2p is not None:
+            p2p.barrier(channel=0)
+
+    def reduce_post():  # the sum is complete in this rank's copy
+        if p2p is not None:
+            p2p.barrier(channel=1)
+        elif reduce_grad:
+            edist.allreduce_grad(grad)
 
     # fused path (default): efunc_forward_backward runs the fused fit kernel k_fit for the MSE loss;
     # --split: efunc_forward + efunc_backward (k_item_lists, k_forward_keys, k_backward)
     def step_calls(i):
         grad.zero_()
+        reduce_pre()
         if args.split:
             m.forward(qd[i], od[i], loss=loss, J_global=J_global, want_O=False, want_loss=False)
             m.backward(grad=grad)
         else:
             m.forward_backward(qd[i], od[i], loss=loss, J_global=J_global, grad=grad, want_loss=False)
-        if reduce_grad:
-            edist.allreduce_grad(grad)
+        reduce_post()
         m.adamw_step(grad, hp)
 
     # The step is replayed from a CUDA graph per input batch (the same ABI calls captured once; the
@@ -380,6 +401,8 @@ def run_ours(args, rank, world, local_rank, nccl):
     clocks = clk.summary()
     value = (J_global if S == 1 else n_pts * world) * args.steps / sec
 
+    if p2p is not None and world == 1:
+        m.set_grad_peers([], 0)  # the single-rank e2e path (efunc_fit_step) folds into its own workspace
     # e2e: same steps through the public API with pinned host inputs, H2D + loss D2H inside
     e2e = None
     if not args.no_e2e:
@@ -409,9 +432,9 @@ def run_ours(args, rank, world, local_rank, nccl):
                 qbuf.copy_(hq[i], non_blocking=True)
                 obuf.copy_(ho[i], non_blocking=True)
                 grad.zero_()
+                reduce_pre()
                 _, _, L = m.forward_backward(qbuf, obuf, loss=loss, J_global=J_global, grad=grad)
-                if reduce_grad:
-                    edist.allreduce_grad(grad)
+                reduce_post()
                 m.adamw_step(grad, hp)
                 lpin[slot].copy_(L.view(-1), non_blocking=True)
             for w in range(3):
@@ -431,6 +454,8 @@ def run_ours(args, rank, world, local_rank, nccl):
 
     # paper context (Table 4, J = 16384 at 32^3): our forward, backward and fused fwd+bwd on the
     # first 16384 points of a batch (eager launches, CUDA events, after warm-up)
+    if p2p is not None:
+        m.set_grad_peers([], 0)  # the Table-4 context below runs on rank 0 alone: local folds only
     t4 = None
     if R == 32 and S == 1 and rank == 0:
         nq = PAPER_T4["J"]
@@ -519,9 +544,15 @@ def run_ours(args, rank, world, local_rank, nccl):
             "config": {"workload": label, "R": R, "points_per_step_per_gpu": n_pts,
                        "global_batch": J_global if S == 1 else n_pts * world, "shapes_per_gpu": S,
                        "cutoff_T": 20.0, "parallelism": f"dp{world}" if S == 1 else f"replicas{world}",
-                       "launch": ("cuda-graph per step" + (" (NCCL all-reduce inside)" if reduce_grad else ""))
+                       "launch": ("cuda-graph per step" + ((" (fused fold + peer reduction and its barriers inside)"
+                                                             if p2p is not None else " (NCCL all-reduce inside)")
+                                                            if reduce_grad else ""))
                                  if use_graph else (graph_note or "eager"),
-                       "collective": ("NCCL all_reduce (sum, fp32) of the R^3 x 13 gradient" if nccl else
+                       "collective": (("fused fold + " + ("NVLS multimem.red" if p2p.multicast_ptr else
+                                                            f"red.v4 into {len(p2p.buffer_ptrs)} peer copies")
+                                       + " of the R^3 x 13 gradient (torch symmetric memory, 2 barriers)")
+                                      if p2p is not None else
+                                      "NCCL all_reduce (sum, fp32) of the R^3 x 13 gradient" if nccl else
                                       "gloo all_reduce (shared-GPU code-path run, not a measurement)")
                                      if reduce_grad else None,
                        "deterministic": bool(args.deterministic),

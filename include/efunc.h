@@ -274,6 +274,19 @@ EFUNC_API efunc_status efunc_set_adam_state(efunc_t* h, const float* m_host, con
 /* efunc_set_counting — 1: the forward also counts kept pairs (a - m <= T) for
  * efunc_get_stats (slower; diagnostics only). */
 EFUNC_API efunc_status efunc_set_counting(efunc_t* h, int32_t on);
+/* efunc_set_grad_peers — data-parallel gradient reduction fused into the gradient fold (SURVEY
+ * §8(e); the loss is a batch mean, so the full-batch gradient is the sum of the
+ * ranks' shard gradients). peers[0..n_peers) are device pointers, valid on this handle's device,
+ * to every rank's copy of one symmetric gradient buffer of n_params floats (this rank's own copy
+ * included: e.g. torch symmetric memory's buffer_ptrs over NVLink/NVSwitch peer mappings); mc is
+ * its NVLS multicast address or NULL. When set, efunc_forward_backward / efunc_backward add their
+ * gradient into every rank's copy (multimem.red.add.v4.f32 through mc if given, else one
+ * red.global.add.v4.f32 per peer) instead of into `grad`; the caller zeroes its own copy and
+ * synchronises the ranks before the call, and synchronises them again before reading the sum (its
+ * own copy). n_params must be a multiple of 4 (R^3 x 13 channels with R even; checked). n_peers = 0
+ * and mc = NULL restore the local fold. The float path only (EFUNC_EINVAL in deterministic mode).
+ * Host pointer array, copied. */
+EFUNC_API efunc_status efunc_set_grad_peers(efunc_t* h, void* const* peers, int32_t n_peers, void* mc);
 /* efunc_set_timing — slots > 0: every efunc_backward / efunc_forward_backward call records a
  * CUDA event pair around its dominant kernel (k_backward, or k_fit when fused) on the call's
  * stream, into slot (call index mod slots); the records also work inside CUDA-graph capture

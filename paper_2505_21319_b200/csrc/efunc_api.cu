@@ -333,7 +333,7 @@ void free_all(efunc_t* h) {
   dfree(h->q_bin); dfree(h->bin_count); dfree(h->bin_start); dfree(h->bin_fill); dfree(h->q_tmp);
   dfree(h->q_order); dfree(h->qs); dfree(h->perm); dfree(h->rec); dfree(h->gs); dfree(h->us); dfree(h->hs);
   dfree(h->qmh); dfree(h->qf0); dfree(h->loss_part); dfree(h->io_q); dfree(h->io_o); dfree(h->io_loss);
-  dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad);
+  dfree(h->items); dfree(h->item_cnt); dfree(h->item_off); dfree(h->gpad); dfree(h->peer_grad);
   dfree(h->bl_pool); dfree(h->bl_off); dfree(h->bl_n); dfree(h->key_ref); dfree(h->gfix);
   dfree(h->wl_pool); dfree(h->wl_off); dfree(h->wl_n); dfree(h->slow_items); dfree(h->item_o);
   dfree(h->scratch); dfree(h->iota); dfree(h->dn_zm); dfree(h->dn_dq);
@@ -534,7 +534,9 @@ efunc_status do_backward(efunc_t* h, const float* dL_dO, const float* dL_dG, flo
     const int slot = timing_begin(h, s);
     h->launches += launch_backward(b, h->fwd_items_bound, s);
     timing_end(h, slot, s);
-    h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+    h->launches += (h->n_peers > 0 || h->mc_grad)
+                       ? launch_fold_peers(h->gpad, h->n_nodes, h->peer_grad, h->n_peers, h->mc_grad, s)
+                       : launch_fold(h->gpad, grad, h->n_nodes, s);
   }
   CK(cudaGetLastError());
   return EFUNC_OK;
@@ -721,7 +723,9 @@ efunc_status do_forward_backward(efunc_t* h, const float* q, const float* o, int
     h->launches += launch_fold_fix(h->gfix, &h->ds->umax, grad, h->n_nodes, s);
   } else {
     h->launches += launch_backward(b, h->fwd_items_bound, s);
-    h->launches += launch_fold(h->gpad, grad, h->n_nodes, s);
+    h->launches += (h->n_peers > 0 || h->mc_grad)
+                       ? launch_fold_peers(h->gpad, h->n_nodes, h->peer_grad, h->n_peers, h->mc_grad, s)
+                       : launch_fold(h->gpad, grad, h->n_nodes, s);
   }
   if (loss_out) h->launches += launch_sum_partials(h->loss_part, a.n_items, 1, loss_out, s);
   CK(cudaGetLastError());
@@ -1438,6 +1442,28 @@ efunc_status efunc_set_counting(efunc_t* h, int32_t on) {
   }
   if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
   h->count_kept = on ? 1 : 0;
+  return EFUNC_OK;
+}
+
+efunc_status efunc_set_grad_peers(efunc_t* h, void* const* peers, int32_t n_peers, void* mc) {
+  if (h && !h->kids.empty()) return fail(h, EFUNC_EINVAL, "batched handles (n_shapes > 1) are replicas: no reduction");
+  if (!h) return fail(nullptr, EFUNC_EINVAL, "NULL handle");
+  if (n_peers < 0 || n_peers > 1024 || (n_peers > 0 && !peers)) return fail(h, EFUNC_EINVAL, "bad peer list");
+  if ((n_peers > 0 || mc) && h->cfg.deterministic)
+    return fail(h, EFUNC_EINVAL, "the fused peer reduction is the float path (not deterministic mode)");
+  if ((n_peers > 0 || mc) && h->vmode) return fail(h, EFUNC_EINVAL, "the 13-channel layout only");
+  if (((int64_t)h->n_nodes * EF_NCH) % 4) return fail(h, EFUNC_EINVAL, "n_params must be a multiple of 4");
+  DeviceGuard dg(h->cfg.device);
+  CK(cudaDeviceSynchronize());
+  drop_fit_graph(h);
+  dfree(h->peer_grad);
+  h->n_peers = 0;
+  h->mc_grad = static_cast<float*>(mc);
+  if (n_peers > 0) {
+    CK(dalloc(&h->peer_grad, (size_t)n_peers));
+    CK(cudaMemcpy(h->peer_grad, peers, sizeof(float*) * (size_t)n_peers, cudaMemcpyHostToDevice));
+    h->n_peers = n_peers;
+  }
   return EFUNC_OK;
 }
 

@@ -259,6 +259,8 @@ int launch_dense_fit(const FitArgs& a, int64_t n_items, float2* zm, float4* dq, 
 int launch_fit_eik(const FitArgs& a, int64_t n_items, cudaStream_t s);
 int launch_sum_partials(const float* part, const uint32_t* n, int mult, float* out, cudaStream_t s);
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s);
+// the fold fused with the ranks' gradient reduction (efunc_set_grad_peers)
+int launch_fold_peers(float* gpad, int n_nodes, float* const* peers, int n_peers, float* mc, cudaStream_t s);
 int launch_backward_det(const BwdArgs& a, int64_t n_items, cudaStream_t s);
 int launch_fold_fix(unsigned long long* gfix, const float* umax, float* grad, int n_nodes, cudaStream_t s);
 struct AdamWConst {  // the efunc_adamw hyper-parameters (doubles, like torch's python floats)
@@ -392,6 +394,9 @@ struct efunc {
   ef::DevScalars* ds = nullptr;
   float* fit_grad = nullptr;
   float* gpad = nullptr;            // [R^3][16] padded gradient accumulator (kept zero between calls)
+  float** peer_grad = nullptr;      // efunc_set_grad_peers: device array of every rank's gradient copy
+  int n_peers = 0;
+  float* mc_grad = nullptr;         // and its NVLS multicast address (or null)
   unsigned long long* gfix = nullptr;  // [R^3][16] fixed-point accumulator (deterministic mode)
   // brick lists
   uint32_t* bl_pool = nullptr;

@@ -407,6 +407,44 @@ __global__ void k_fold(float* __restrict__ gpad, float* __restrict__ grad, int n
   }
 }
 
+// The fold fused with the data-parallel reduction: thread i takes gradient floats 4i .. 4i+3 of the
+// [R^3][13] layout (their gpad slots, zeroed after reading) and adds the float4 into every rank's
+// copy of the symmetric gradient buffer: one NVLS multimem.red through the multicast address, or
+// one red.global.add.v4 per peer mapping (NVLink P2P). gpad slot of channel c: the grid bank's 5
+// channels at 0..4, the offset bank's 8 at 8..15 (k_fold's map).
+__device__ __forceinline__ int gpad_slot(const int c) { return c < 5 ? c : c + 3; }
+
+__global__ void k_fold_peers(float* __restrict__ gpad, int n_nodes, float* const* __restrict__ peers, int n_peers,
+                             float* __restrict__ mc) {
+  const int64_t n4 = (int64_t)n_nodes * EF_NCH / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t f = 4 * i + k;
+      const int64_t n = f / EF_NCH;
+      float* p = gpad + n * 16 + gpad_slot((int)(f - n * EF_NCH));
+      v[k] = *p;
+      *p = 0.0f;
+    }
+    if (mc) {
+      asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + 4 * i), "f"(v[0]),
+                   "f"(v[1]), "f"(v[2]), "f"(v[3])
+                   : "memory");
+    } else {
+      for (int r = 0; r < n_peers; ++r) red_v4(peers[r] + 4 * i, v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
+int launch_fold_peers(float* gpad, int n_nodes, float* const* peers, int n_peers, float* mc, cudaStream_t s) {
+  const int64_t n4 = (int64_t)n_nodes * EF_NCH / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_fold_peers<<<blocks, 256, 0, s>>>(gpad, n_nodes, peers, n_peers, mc);
+  return 1;
+}
+
 int launch_fold(float* gpad, float* grad, int n_nodes, cudaStream_t s) {
   int blocks = (n_nodes + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;

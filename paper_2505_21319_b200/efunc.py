@@ -29,7 +29,7 @@ EXPORTED = ["efunc_create", "efunc_destroy", "efunc_forward", "efunc_backward", 
             "efunc_set_params", "efunc_get_adam_state", "efunc_set_adam_state", "efunc_set_counting",
             "efunc_get_stats", "efunc_check", "efunc_set_timing", "efunc_get_kernel_ms", "efunc_sync", "efunc_last_error",
             "efunc_mesh", "efunc_channels", "efunc_cosine_replicate", "efunc_cosine_combine",
-            "efunc_abi_version"]
+            "efunc_abi_version", "efunc_set_grad_peers"]
 
 
 class Config(C.Structure):
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "efunc_check": [P, P],
         "efunc_sync": [P],
         "efunc_set_timing": [P, i32],
+        "efunc_set_grad_peers": [P, P, i32, P],
         "efunc_get_kernel_ms": [P, P, i32],
         "efunc_mesh": [P, i32, P, P, f32, P, P, P, P, i64, i64, C.POINTER(i64), C.POINTER(i64), P],
         "efunc_cosine_replicate": [P, i64, i32, P, P],
@@ -390,6 +391,17 @@ class EFunc:
     def sync(self):
         """wait for the pipelined (host_io 2) fit steps"""
         self._ok(self.lib.efunc_sync(self.h))
+
+    def set_grad_peers(self, peer_ptrs, mc_ptr: int = 0):
+        """Fuse the data-parallel gradient reduction into the fold: forward_backward / backward add
+        their gradient into every rank's copy of a symmetric buffer (peer_ptrs: device addresses of
+        all ranks' copies, e.g. torch symmetric memory buffer_ptrs; mc_ptr: its NVLS multicast
+        address or 0). The caller zeroes its copy and synchronises the ranks before the call and
+        again before reading it. An empty list and mc_ptr = 0 restore the local fold."""
+        ptrs = [int(p) for p in peer_ptrs]
+        arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs) if ptrs else None
+        self._ok(self.lib.efunc_set_grad_peers(self.h, C.cast(arr, C.c_void_p) if arr is not None else None,
+                                               len(ptrs), C.c_void_p(int(mc_ptr)) if mc_ptr else None))
 
     def set_timing(self, slots: int):
         """Record CUDA events around the dominant kernel of each backward/forward_backward call."""

@@ -134,3 +134,49 @@ def test_bench_nccl_allreduce_captured_in_step_graph_single_rank():
     assert d["config"]["launch"] == "cuda-graph per step (NCCL all-reduce inside)", d["config"]
     assert d["config"]["collective"].startswith("NCCL all_reduce")
     assert d["value"] > 0
+
+
+def test_bench_fused_peer_reduction_single_rank():
+    """EFUNC_BENCH_P2P=1 on a one-rank NCCL group: the gradient in torch symmetric memory, the
+    library's fold adding it into every rank's copy (efunc_set_grad_peers: here the rank's own copy)
+    between two symmetric-memory barriers, all captured in the step graph. The code path of the
+    fused fold + peer reduction; its sum over ranks is the gloo-checked algebra above."""
+    env = dict(os.environ, EFUNC_BENCH_NCCL1="1", EFUNC_BENCH_P2P="1", MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(_free_port()), EFUNC_BENCH_WATCHDOG="150")
+    env.pop("WORLD_SIZE", None)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        with open(os.path.join(td, "out"), "w") as fo, open(os.path.join(td, "err"), "w") as fe:
+            rc = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "5",
+                                 "--warmup", "3", "--no-cpu-baseline"], env=env, stdout=fo, stderr=fe,
+                                timeout=300, cwd=ROOT).returncode
+        out = open(os.path.join(td, "out")).read()
+        err = open(os.path.join(td, "err")).read()
+    assert rc == 0, err[-3000:]
+    d = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["collective"].startswith("fused fold + "), d["config"]
+    assert d["value"] > 0
+
+
+def test_fused_peer_fold_equals_local_fold():
+    """efunc_set_grad_peers with this device's own buffer as the only peer: the fused fold adds the
+    same gradient the local fold writes (up to the order of the float atomics in the fit kernel)."""
+    import paper_2505_21319_b200 as ef
+    from workloads import synth
+    R, J = 16, 1 << 14
+    tor = synth.Torus()
+    th = synth.fitted_like_theta(R, tor, 3)
+    q, o = synth.sample_batch(tor, J, seed=4)
+    qd, od = torch.as_tensor(q).cuda(), torch.as_tensor(o).cuda()
+    m = ef.EFunc(R, th)
+    g0, _, _ = m.forward_backward(qd, od, loss=ef.LOSS_MSE)
+    buf = torch.zeros_like(g0)
+    m.set_grad_peers([buf.data_ptr()], 0)
+    gdummy = torch.zeros_like(g0)
+    m.forward_backward(qd, od, loss=ef.LOSS_MSE, grad=gdummy)
+    torch.cuda.synchronize()
+    m.set_grad_peers([], 0)
+    assert float(gdummy.abs().max()) == 0.0  # the local grad is untouched
+    # float reds in a different order: equal up to rounding of the atomic sums
+    scale = float(g0.abs().max())
+    assert float((buf - g0).abs().max()) <= 1e-5 * scale
